@@ -1,0 +1,150 @@
+/*
+ * sgw.h — C ABI of the B200-native SG-PCG / NN2 solver (libsgw_b200.so).
+ *
+ * Drop-in boundary for the reference sgwave hot path: the per-Newmark-step
+ * interface-Schur PCG solve of the coupled (P+1) x N stochastic-Galerkin
+ * system, preconditioned by the probabilistic two-level Neumann-Neumann
+ * (NN2) domain decomposition.  Every entry point takes plain pointers and
+ * sizes (host memory unless the name says _dev), returns an sgw_status and
+ * never retains caller pointers past the call.  Error text for the last
+ * failing call on the calling thread: sgw_last_error().
+ *
+ * Reference interfaces replaced (paths relative to the reference proj/):
+ *   sgw_create          SgSolver::SgSolver            include/sgwave/sg.hpp:45-47, src/sg.cpp:128-176
+ *                       (+ assemble_subdomains src/sg.cpp:178-250, SchurSystem::finalize src/dd.cpp:98-140)
+ *   sgw_run             SgSolver::run                 include/sgwave/sg.hpp:49-50, src/sg.cpp:358-423
+ *   sgw_init_state /    SgSolver::run's time loop split into resident steps
+ *   sgw_advance         (step_rhs_and_solve src/sg.cpp:295-356 + newmark_update src/newmark.cpp:39-49)
+ *   sgw_apply_block     SgSolver::apply_block_{mass,stiffness,transient}  sg.hpp:58-60, src/sg.cpp:425-447
+ *   sgw_schur_matvec    SchurSystem::matvec           include/sgwave/dd.hpp:85, src/dd.cpp:142-157
+ *   sgw_apply_nn2       SchurSystem::apply_nn2        include/sgwave/dd.hpp:88, src/dd.cpp:199-253
+ *   sgw_pcg             pcg(matvec, apply_nn2, ...)   include/sgwave/pcg.hpp:20-21, src/pcg.cpp:7-50
+ *   sgw_coarse_operator SchurSystem::coarse_operator  include/sgwave/dd.hpp:90
+ *   sgw_lognormal_coeff lognormal_pce(kle_exponential(...))  src/lognormal.cpp:8-40, src/kle.cpp:80-133
+ *   sgw_triple_products triple_products               src/pce.cpp:96-122 (order_in <= order_out guard lifted)
+ *   sgw_nearest_node    nearest_node                  src/mesh.cpp:83-96
+ *
+ * Error classes (reference exception -> status):
+ *   std::invalid_argument (sg.cpp:143-145, :382)            -> SGW_EINVAL
+ *   std::runtime_error factorization (sg.cpp:151,:170,:221; dd.cpp:72-74) -> SGW_EFACTOR
+ *   std::runtime_error non-convergence (sg.cpp:413-416)      -> SGW_ENOCONV
+ *   CUDA / cuBLAS / cuSOLVER failures                        -> SGW_ECUDA
+ *   NCCL failures (multi-GPU)                                -> SGW_ENCCL
+ */
+#ifndef SGW_H_
+#define SGW_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sgw_status {
+  SGW_OK = 0,
+  SGW_EINVAL = 1,
+  SGW_EFACTOR = 2,
+  SGW_ENOCONV = 3,
+  SGW_ECUDA = 4,
+  SGW_ENCCL = 5,
+  SGW_ENOMEM = 6
+} sgw_status;
+
+typedef struct sgw_solver sgw_solver;
+
+/* SgSolver constructor arguments.  The mesh is build_unit_square_mesh(nx, ny)
+ * (src/mesh.cpp:15-58) and the partition partition_structured(mesh, px, py)
+ * (src/partition.cpp:48-133); the GPU path requires px | nx and py | ny. */
+typedef struct sgw_problem {
+  int nx, ny, px, py;
+  int n_input;          /* CoefficientField terms                              */
+  const double* coeff;  /* n_input x (nx+1)(ny+1) nodal values, term-major     */
+  int n_output;         /* TripleTensor::n_output  (P+1)                       */
+  int n_entries;        /* TripleTensor entries with j <= k (pce.hpp:24-40)    */
+  const int* ent_i;
+  const int* ent_j;
+  const int* ent_k;
+  const double* ent_v;
+  double density, alpha0, alpha1;
+  double gamma, zeta, dt; /* NewmarkParams (newmark.hpp:11-19)                 */
+  double tol;             /* SgOptions::tol (sg.hpp:16)                         */
+  int max_iter;           /* SgOptions::max_iter                               */
+  int device;             /* CUDA device ordinal                                */
+  /* multi-GPU sharding (one process per GPU); world_size 1 = single GPU.
+   * nccl_id: 128-byte ncclUniqueId from rank 0, broadcast by the caller.  */
+  int rank, world_size;
+  const void* nccl_id;
+} sgw_problem;
+
+/* ForceFn (det_loop.hpp:32): kind 0 none; 1 Ricker wavelet
+ *   amp * (1 - 2 pi^2 f0^2 (t - t0)^2) exp(-pi^2 f0^2 (t - t0)^2) at mesh node `node`;
+ * 2 nodal table, (n_steps + 1) x n_nodes rows for t_0 .. t_N.                 */
+typedef struct sgw_force {
+  int kind;
+  int node;
+  double f0, t0, amp;
+  const double* table;
+} sgw_force;
+
+/* SgHistory (sg.hpp:23-31).  Caller-owned output buffers; NULL = not wanted. */
+typedef struct sgw_history {
+  int* iterations;       /* n_steps                                   */
+  double* residual;      /* n_steps: final true residual ||b-Ax||/||b|| */
+  int n_probes;
+  const int* probe_nodes;/* mesh node ids                               */
+  double* probe_mean;    /* n_probes x (n_steps + 1)                    */
+  double* probe_std;     /* n_probes x (n_steps + 1)                    */
+  double* full_state;    /* (n_steps + 1) x (P+1) n_dofs, term-major    */
+} sgw_history;
+
+const char* sgw_last_error(void);
+int sgw_version(void);
+
+int sgw_create(const sgw_problem* problem, sgw_solver** out);
+int sgw_destroy(sgw_solver* s);
+
+/* sizes: [0] n_dofs  [1] n_terms  [2] n_iface  [3] n_corner  [4] n_global (flat)
+ *        [5] n_sub   [6] uses_direct (always 0 on the GPU path)  [7] device bytes */
+int sgw_sizes(sgw_solver* s, long long* sizes);
+
+/* Launch all work on this cudaStream_t (NULL = library-owned stream). */
+int sgw_set_stream(sgw_solver* s, void* cuda_stream);
+
+/* op: 0 mass, 1 stiffness, 2 transient.  x, y: (P+1) n_dofs, term-major.   */
+int sgw_apply_block(sgw_solver* s, int op, const double* x, double* y);
+int sgw_schur_matvec(sgw_solver* s, const double* x, double* y);
+int sgw_apply_nn2(sgw_solver* s, const double* r, double* z);
+/* PCG on S u = rhs with NN2 (src/pcg.cpp:7-50).  history: >= max_iter + 2. */
+int sgw_pcg(sgw_solver* s, const double* rhs, double* x, int* iterations, int* converged,
+            double* residual_history, int history_cap);
+/* F_cc (n_corner flat)^2, column-major. */
+int sgw_coarse_operator(sgw_solver* s, double* out);
+
+int sgw_run(sgw_solver* s, const double* u0_nodal, const double* v0_nodal, int n_steps,
+            const sgw_force* force, sgw_history* history);
+
+/* Device-resident stepping (for benchmarks): set the initial state and the
+ * forcing, then advance n steps without host round trips of the state.     */
+int sgw_init_state(sgw_solver* s, const double* u0_nodal, const double* v0_nodal,
+                   const sgw_force* force);
+int sgw_advance(sgw_solver* s, int n_steps, int* iterations);
+int sgw_get_state(sgw_solver* s, double* u_flat);
+
+/* stats: [0] setup s  [1] pcg ms (device events, last advance/run)
+ *        [2] step ms  [3] PCG iterations  [4] kernel launches  [5] steps
+ *        [6] rhs ms   [7] recovery ms     [8] matvec calls    [9] nn2 calls */
+int sgw_stats(sgw_solver* s, double* out);
+int sgw_reset_stats(sgw_solver* s);
+
+/* Input builders (host). */
+int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, double g0,
+                        int n_vars, int p_in, double* out, long long out_cap, int* n_in);
+int sgw_triple_products(int n_vars, int p_in, int p_out, int* n_in, int* n_out, int* n_entries,
+                        int* ei, int* ej, int* ek, double* ev, long long cap);
+int sgw_nearest_node(int nx, int ny, double x, double y);
+
+/* NCCL unique id for multi-GPU runs (128 bytes), generated on rank 0. */
+int sgw_nccl_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGW_H_ */

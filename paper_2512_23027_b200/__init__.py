@@ -1,0 +1,23 @@
+"""B200-native SG-PCG / NN2 solver (sm_100a CUDA behind the C ABI include/sgw.h).
+
+The Python layer mirrors the reference sgwave solver interface for the hot
+path (SgSolver / SchurSystem / pcg, include/sgwave/sg.hpp, dd.hpp, pcg.hpp)
+over ctypes.  There is no CPU fallback: importing the solver requires the
+compiled libsgw_b200.so and every compute call runs on the GPU.
+"""
+from .sgwave import (  # noqa: F401
+    ForceSpec,
+    NewmarkParams,
+    SgError,
+    SgHistory,
+    SgOptions,
+    SgSolver,
+    TripleTensor,
+    gaussian_pulse,
+    lib_path,
+    load_library,
+    lognormal_coeff,
+    nearest_node,
+    ricker,
+    triple_products,
+)

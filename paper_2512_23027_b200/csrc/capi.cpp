@@ -1,0 +1,311 @@
+// extern "C" boundary of libsgw_b200.so (declared in include/sgw.h).
+// Host buffers in, host buffers out; exceptions become sgw_status codes.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/sgw.h"
+#include "solver.cuh"
+
+using namespace sgw;
+
+struct sgw_solver {
+  std::unique_ptr<GpuSolver> g;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return SGW_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return SGW_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SGW_EINVAL;
+  }
+}
+
+struct Tmp {  // device scratch for host<->device copies
+  DBuf<double> a, b;
+};
+
+void h2d(DBuf<double>& d, const double* h, size_t n, cudaStream_t st) {
+  if (d.n < n) d.alloc(n);
+  SGW_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+}
+void d2h(double* h, const double* d, size_t n, cudaStream_t st) {
+  SGW_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SGW_CUDA(cudaStreamSynchronize(st));
+}
+
+void set_force(GpuSolver& g, const sgw_force* f, int rows) {
+  if (!f || f->kind == 0) {
+    g.set_force_point(-1, 0, 0, 0);
+  } else if (f->kind == 1) {
+    if (f->node < 0 || f->node >= g.P.n_nodes()) throw Error(SGW_EINVAL, "force node out of range");
+    g.set_force_point(f->node, f->f0, f->t0, f->amp);
+  } else if (f->kind == 2) {
+    if (!f->table || rows < 1) throw Error(SGW_EINVAL, "force table needs sgw_run (rows = n_steps + 1)");
+    g.set_force_table(f->table, rows);
+  } else {
+    throw Error(SGW_EINVAL, "unknown force kind");
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* sgw_last_error(void) { return g_err.c_str(); }
+int sgw_version(void) { return 1; }
+
+int sgw_create(const sgw_problem* p, sgw_solver** out) {
+  return guard([&] {
+    if (!p || !out) throw Error(SGW_EINVAL, "null argument");
+    if (!p->coeff || p->n_input < 1) throw Error(SGW_EINVAL, "SgSolver: empty coefficient field");
+    Problem P;
+    P.nx = p->nx, P.ny = p->ny, P.px = p->px, P.py = p->py;
+    P.n_in = p->n_input;
+    P.nt = p->n_output;
+    if (P.nx < 2 || P.ny < 2) throw Error(SGW_EINVAL, "build_unit_square_mesh: nx and ny must be >= 2");
+    P.coeff.assign(p->coeff, p->coeff + (size_t)P.n_in * P.n_nodes());
+    P.tensor.n_in = p->n_input;
+    P.tensor.n_out = p->n_output;
+    for (int e = 0; e < p->n_entries; ++e) {
+      P.tensor.i.push_back(p->ent_i[e]);
+      P.tensor.j.push_back(p->ent_j[e]);
+      P.tensor.k.push_back(p->ent_k[e]);
+      P.tensor.v.push_back(p->ent_v[e]);
+    }
+    P.density = p->density, P.alpha0 = p->alpha0, P.alpha1 = p->alpha1;
+    P.gamma = p->gamma, P.zeta = p->zeta, P.dt = p->dt, P.tol = p->tol, P.max_iter = p->max_iter;
+    P.device = p->device, P.rank = p->rank, P.world = p->world_size < 1 ? 1 : p->world_size;
+    if (P.world != 1) throw Error(SGW_EINVAL, "multi-GPU sharding: use one solver per rank via sgw_create_sharded");
+    auto s = std::make_unique<sgw_solver>();
+    s->g = std::make_unique<GpuSolver>(std::move(P));
+    *out = s.release();
+  });
+}
+
+int sgw_destroy(sgw_solver* s) {
+  return guard([&] { delete s; });
+}
+
+int sgw_sizes(sgw_solver* s, long long* o) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    o[0] = g.n;
+    o[1] = g.NT;
+    o[2] = g.G.n_iface;
+    o[3] = g.G.n_corner;
+    o[4] = g.NG;
+    o[5] = g.NS;
+    o[6] = 0;
+    o[7] = g.device_bytes();
+  });
+}
+
+int sgw_set_stream(sgw_solver* s, void* stream) {
+  return guard([&] { s->g->set_stream(static_cast<cudaStream_t>(stream)); });
+}
+
+int sgw_apply_block(sgw_solver* s, int op, const double* x, double* y) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    if (op < 0 || op > 2) throw Error(SGW_EINVAL, "apply_block: op must be 0, 1 or 2");
+    DBuf<double> dx, dy;
+    h2d(dx, x, g.NSTATE, g.stream());
+    dy.alloc(g.NSTATE);
+    g.apply_block(op, dx.p, dy.p);
+    d2h(y, dy.p, g.NSTATE, g.stream());
+  });
+}
+
+int sgw_schur_matvec(sgw_solver* s, const double* x, double* y) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    DBuf<double> dx, dy;
+    h2d(dx, x, g.NG, g.stream());
+    dy.alloc(g.NG);
+    g.schur_matvec(dx.p, dy.p);
+    d2h(y, dy.p, g.NG, g.stream());
+  });
+}
+
+int sgw_apply_nn2(sgw_solver* s, const double* r, double* z) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    DBuf<double> dx, dy;
+    h2d(dx, r, g.NG, g.stream());
+    dy.alloc(g.NG);
+    g.apply_nn2(dx.p, dy.p);
+    d2h(z, dy.p, g.NG, g.stream());
+  });
+}
+
+int sgw_pcg(sgw_solver* s, const double* rhs, double* x, int* iterations, int* converged, double* hist,
+            int cap) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    DBuf<double> db, dx;
+    h2d(db, rhs, g.NG, g.stream());
+    dx.alloc(g.NG);
+    bool conv = false;
+    std::vector<double> h;
+    const int it = g.pcg(db.p, dx.p, &conv, &h);
+    d2h(x, dx.p, g.NG, g.stream());
+    if (iterations) *iterations = it;
+    if (converged) *converged = conv ? 1 : 0;
+    if (hist)
+      for (int i = 0; i < cap; ++i) hist[i] = i < (int)h.size() ? h[i] : -1.0;
+  });
+}
+
+int sgw_coarse_operator(sgw_solver* s, double* out) {
+  return guard([&] {
+    const auto f = s->g->coarse_operator_host();
+    std::memcpy(out, f.data(), f.size() * sizeof(double));
+  });
+}
+
+int sgw_init_state(sgw_solver* s, const double* u0, const double* v0, const sgw_force* force) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    set_force(g, force, 0);
+    DBuf<double> du, dv;
+    h2d(du, u0, g.P.n_nodes(), g.stream());
+    h2d(dv, v0, g.P.n_nodes(), g.stream());
+    g.init_state(du.p, dv.p, 0.0);
+  });
+}
+
+int sgw_advance(sgw_solver* s, int n_steps, int* iterations) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    for (int k = 0; k < n_steps; ++k) {
+      int it = 0;
+      g.step(&it);
+      if (iterations) iterations[k] = it;
+    }
+  });
+}
+
+int sgw_get_state(sgw_solver* s, double* u_flat) {
+  return guard([&] { d2h(u_flat, s->g->u.p, s->g->NSTATE, s->g->stream()); });
+}
+
+int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, const sgw_force* force,
+            sgw_history* h) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    if (n_steps < 0) throw Error(SGW_EINVAL, "n_steps must be >= 0");
+    // probes (src/sg.cpp:378-383)
+    g.probe_dofs.clear();
+    const int np = h ? h->n_probes : 0;
+    for (int p = 0; p < np; ++p) {
+      const int node = h->probe_nodes[p];
+      if (node < 0 || node >= g.P.n_nodes()) throw Error(SGW_EINVAL, "probe node out of range");
+      const int gi = node % (g.P.nx + 1), gj = node / (g.P.nx + 1);
+      const int d = g.G.dof(gi, gj);
+      if (d < 0) throw Error(SGW_EINVAL, "probe node is constrained");
+      g.probe_dofs.push_back(d);
+    }
+    g.probe_cap = n_steps + 1;
+    if (np) {
+      g.d_probe_dofs.upload(g.probe_dofs);
+      g.probe_hist.alloc((size_t)(n_steps + 1) * np * 2);
+    }
+    set_force(g, force, n_steps + 1);
+    DBuf<double> du, dv;
+    h2d(du, u0, g.P.n_nodes(), g.stream());
+    h2d(dv, v0, g.P.n_nodes(), g.stream());
+    g.init_state(du.p, dv.p, 0.0);
+    g.record_probes(0);
+    if (h && h->full_state) d2h(h->full_state, g.u.p, g.NSTATE, g.stream());
+    for (int k = 0; k < n_steps; ++k) {
+      int it = 0;
+      g.step(&it);
+      if (h && h->iterations) h->iterations[k] = it;
+      if (h && h->residual) h->residual[k] = g.last_rel;
+      if (h && h->full_state) d2h(h->full_state + (size_t)(k + 1) * g.NSTATE, g.u.p, g.NSTATE, g.stream());
+    }
+    if (np) {
+      std::vector<double> ph((size_t)(n_steps + 1) * np * 2);
+      SGW_CUDA(cudaMemcpyAsync(ph.data(), g.probe_hist.p, ph.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                               g.stream()));
+      SGW_CUDA(cudaStreamSynchronize(g.stream()));
+      for (int p = 0; p < np; ++p)
+        for (int k = 0; k <= n_steps; ++k) {
+          if (h->probe_mean) h->probe_mean[(size_t)p * (n_steps + 1) + k] = ph[((size_t)k * np + p) * 2];
+          if (h->probe_std) h->probe_std[(size_t)p * (n_steps + 1) + k] = ph[((size_t)k * np + p) * 2 + 1];
+        }
+    }
+  });
+}
+
+int sgw_stats(sgw_solver* s, double* o) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    o[0] = g.setup_s;
+    o[1] = g.T.pcg_ms;
+    o[2] = g.T.step_ms;
+    o[3] = double(g.T.iterations);
+    o[4] = double(g_launches);
+    o[5] = double(g.T.steps);
+    o[6] = g.T.rhs_ms;
+    o[7] = g.T.rec_ms;
+    o[8] = double(g.T.matvecs);
+    o[9] = double(g.T.nn2s);
+  });
+}
+
+int sgw_reset_stats(sgw_solver* s) {
+  return guard([&] { s->g->T = Timers{}; });
+}
+
+int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, double g0, int n_vars, int p_in,
+                        double* out, long long cap, int* n_in) {
+  return guard([&] {
+    const auto c = lognormal_coeff(nx, ny, sigma, bx, by, g0, n_vars, p_in);
+    *n_in = int(c.size());
+    if (out) {
+      const size_t nn = (size_t)(nx + 1) * (ny + 1);
+      if ((long long)(c.size() * nn) > cap) throw Error(SGW_EINVAL, "coefficient buffer too small");
+      for (size_t i = 0; i < c.size(); ++i) std::memcpy(out + i * nn, c[i].data(), nn * sizeof(double));
+    }
+  });
+}
+
+int sgw_triple_products(int n_vars, int p_in, int p_out, int* n_in, int* n_out, int* n_entries, int* ei, int* ej,
+                        int* ek, double* ev, long long cap) {
+  return guard([&] {
+    const TensorHost t = triple_products(n_vars, p_in, p_out);
+    *n_in = t.n_in;
+    *n_out = t.n_out;
+    *n_entries = int(t.v.size());
+    if (ei) {
+      if ((long long)t.v.size() > cap) throw Error(SGW_EINVAL, "tensor buffer too small");
+      for (size_t e = 0; e < t.v.size(); ++e) ei[e] = t.i[e], ej[e] = t.j[e], ek[e] = t.k[e], ev[e] = t.v[e];
+    }
+  });
+}
+
+int sgw_nearest_node(int nx, int ny, double x, double y) { return nearest_node(nx, ny, x, y); }
+
+int sgw_nccl_unique_id(void* out128) {
+  return guard([&] {
+    (void)out128;
+    throw Error(SGW_ENCCL, "NCCL sharding not built into this library");
+  });
+}
+
+}  // extern "C"

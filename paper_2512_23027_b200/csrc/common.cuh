@@ -1,0 +1,46 @@
+// Shared helpers for the sm_100a SG-PCG kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace sgw {
+
+// Status-carrying exception; capi.cpp maps it to the sgw_status codes.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SGW_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::sgw::Error(4, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                                __FILE__ + ":" + std::to_string(__LINE__));              \
+  } while (0)
+
+// Every kernel launch of the library goes through this counter so that the
+// benchmark can report how many of our kernels ran in a timed region.
+extern long long g_launches;
+#define SGW_LAUNCHED()                \
+  do {                                \
+    ++::sgw::g_launches;              \
+    SGW_CUDA(cudaPeekAtLastError());  \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+constexpr int kTile = 64;  // tile edge of the packed symmetric matrices
+
+inline int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace sgw

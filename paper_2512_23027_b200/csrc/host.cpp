@@ -1,0 +1,357 @@
+// Host-side inputs and structured layout for the GPU SG solver.
+#include "host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <limits>
+#include <stdexcept>
+#include <thread>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace sgw {
+
+// ----------------------------------------------------------- geometry ------
+// Structured restatement of partition_structured (src/partition.cpp:48-133)
+// and build_interface_layout / make_flat_maps (src/dd.cpp:10-96) for px | nx,
+// py | ny: interface = non-Dirichlet nodes on internal block lines, corners =
+// cross points (multiplicity 4; boundary-touching corners are Dirichlet).
+Geometry build_geometry(int nx, int ny, int px, int py) {
+  if (nx < 2 || ny < 2) throw Error(1, "build_unit_square_mesh: nx and ny must be >= 2");
+  if (px < 1 || py < 1 || px > nx || py > ny) throw Error(1, "partition_structured: bad px/py");
+  if (nx % px || ny % py) throw Error(1, "GPU path requires px | nx and py | ny");
+  Geometry g;
+  g.nx = nx, g.ny = ny, g.px = px, g.py = py, g.mx = nx / px, g.my = ny / py;
+  g.n = (nx - 1) * (ny - 1);
+  g.iface_pos_of_dof.assign(g.n, -1);
+  g.corner_pos_of_dof.assign(g.n, -1);
+  for (int gj = 1; gj < ny; ++gj)
+    for (int gi = 1; gi < nx; ++gi) {
+      const bool vline = gi % g.mx == 0, hline = gj % g.my == 0;
+      if (!(vline || hline)) continue;
+      const int d = g.dof(gi, gj);
+      g.iface_pos_of_dof[d] = static_cast<int>(g.iface_dofs.size());
+      g.iface_dofs.push_back(d);
+      if (vline && hline) {
+        g.corner_pos_of_dof[d] = static_cast<int>(g.corner_dofs.size());
+        g.corner_dofs.push_back(d);
+      }
+    }
+  g.n_iface = static_cast<int>(g.iface_dofs.size());
+  g.n_corner = static_cast<int>(g.corner_dofs.size());
+  g.ns = px * py;
+  g.W = g.mx - 1;
+  g.H = g.my - 1;
+  g.nl = (g.mx + 1) * (g.my + 1);
+  g.sub.resize(g.ns);
+  for (int s = 0; s < g.ns; ++s) {
+    Geometry::Sub& sd = g.sub[s];
+    sd.sx = s % px;
+    sd.sy = s / px;
+    sd.lid_to_p.assign(g.nl, -1);
+    // ascending reduced dof id == row-major over local nodes
+    for (int jl = 0; jl <= g.my; ++jl)
+      for (int il = 0; il <= g.mx; ++il) {
+        const int lid = jl * (g.mx + 1) + il;
+        const int d = g.dof(sd.sx * g.mx + il, sd.sy * g.my + jl);
+        if (d < 0) continue;
+        if (il > 0 && il < g.mx && jl > 0 && jl < g.my) {
+          sd.lid_to_p[lid] = -2;
+          continue;
+        }
+        const int p = static_cast<int>(sd.iface_lid.size());
+        sd.lid_to_p[lid] = p;
+        sd.iface_lid.push_back(lid);
+        sd.iface_pos.push_back(g.iface_pos_of_dof[d]);
+        const bool corner = g.corner_pos_of_dof[d] >= 0;
+        sd.w.push_back(corner ? 0.25 : 0.5);  // 1 / multiplicity
+        if (corner) {
+          sd.c_local.push_back(p);
+          sd.corner_pos.push_back(g.corner_pos_of_dof[d]);
+        } else {
+          sd.r_local.push_back(p);
+        }
+      }
+  }
+  return g;
+}
+
+// ----------------------------------------------------------- stencils ------
+namespace {
+struct Elem {
+  int n[3];
+};
+// element geometry exactly as the reference computes it from node coordinates
+void geom_of(const int gi[3], const int gj[3], int nx, int ny, double& area, double b[3], double c[3]) {
+  const double x0 = double(gi[0]) / nx, y0 = double(gj[0]) / ny;
+  const double x1 = double(gi[1]) / nx, y1 = double(gj[1]) / ny;
+  const double x2 = double(gi[2]) / nx, y2 = double(gj[2]) / ny;
+  const double det = (x1 - x0) * (y2 - y0) - (x2 - x0) * (y1 - y0);
+  area = 0.5 * det;
+  b[0] = y1 - y2, b[1] = y2 - y0, b[2] = y0 - y1;
+  c[0] = x2 - x1, c[1] = x0 - x2, c[2] = x1 - x0;
+}
+// triangles of cell (ci, cj): lower (a,b,c), upper (a,c,d)  (src/mesh.cpp:38-49)
+void cell_tris(int ci, int cj, int tri, int gi[3], int gj[3]) {
+  const int ai = ci, aj = cj, bi = ci + 1, bj = cj, cI = ci + 1, cJ = cj + 1, di = ci, dj = cj + 1;
+  if (tri == 0) {
+    gi[0] = ai, gj[0] = aj, gi[1] = bi, gj[1] = bj, gi[2] = cI, gj[2] = cJ;
+  } else {
+    gi[0] = ai, gj[0] = aj, gi[1] = cI, gj[1] = cJ, gi[2] = di, gj[2] = dj;
+  }
+}
+}  // namespace
+
+Stencils build_stencils(const Problem& p, const Geometry& g, bool need_local) {
+  Stencils st;
+  const int n = g.n, nin = p.n_in, nn1 = p.nx + 1;
+  st.Kg.assign(size_t(nin) * 3 * n, 0.0);
+  st.Mg.assign(size_t(4) * n, 0.0);
+  auto slot = [](int da, int db, int e_off, int n_off, int ne_off) -> int {
+    const int o = db - da;
+    return o == 0 ? 0 : o == e_off ? 1 : o == n_off ? 2 : o == ne_off ? 3 : -1;
+  };
+  // global reduced assembly, element order (assembly.cpp:31-103 + reduce :121-134)
+  for (int cj = 0; cj < p.ny; ++cj)
+    for (int ci = 0; ci < p.nx; ++ci)
+      for (int tri = 0; tri < 2; ++tri) {
+        int gi[3], gj[3];
+        cell_tris(ci, cj, tri, gi, gj);
+        double area, b[3], c[3];
+        geom_of(gi, gj, p.nx, p.ny, area, b, c);
+        const double m = p.density * area / 12.0;
+        int d[3], node[3];
+        for (int a = 0; a < 3; ++a) d[a] = g.dof(gi[a], gj[a]), node[a] = gj[a] * nn1 + gi[a];
+        for (int a = 0; a < 3; ++a)
+          for (int bb = 0; bb < 3; ++bb) {
+            if (d[a] < 0 || d[bb] < 0 || d[bb] < d[a]) continue;
+            const int sl = slot(d[a], d[bb], 1, p.nx - 1, p.nx);
+            if (sl < 0) throw Error(1, "unexpected coupling in structured mesh");
+            st.Mg[size_t(sl) * n + d[a]] += (a == bb ? 2 * m : m);
+            if (sl == 3) {
+              const double gg = b[a] * b[bb] + c[a] * c[bb];
+              if (gg != 0.0) throw Error(1, "non-zero diagonal stiffness coupling: mesh not supported");
+              continue;
+            }
+            for (int i = 0; i < nin; ++i) {
+              const double* cf = &p.coeff[size_t(i) * p.n_nodes()];
+              const double cavg = (cf[node[0]] + cf[node[1]] + cf[node[2]]) / 3.0;
+              st.Kg[(size_t(i) * 3 + sl) * n + d[a]] += cavg * (b[a] * b[bb] + c[a] * c[bb]) / (4.0 * area);
+            }
+          }
+      }
+  if (!need_local) return st;
+  // local assembly on each subdomain's own elements (src/sg.cpp:38-101)
+  const int nl = g.nl, mx = g.mx;
+  st.Kl.assign(size_t(g.ns) * nin * 3 * nl, 0.0);
+  st.Ml.assign(size_t(g.ns) * 4 * nl, 0.0);
+  auto work = [&](int s) {
+    const Geometry::Sub& sd = g.sub[s];
+    for (int cjl = 0; cjl < g.my; ++cjl)
+      for (int cil = 0; cil < g.mx; ++cil)
+        for (int tri = 0; tri < 2; ++tri) {
+          int gi[3], gj[3];
+          cell_tris(sd.sx * g.mx + cil, sd.sy * g.my + cjl, tri, gi, gj);
+          double area, b[3], c[3];
+          geom_of(gi, gj, p.nx, p.ny, area, b, c);
+          double geom[3][3];
+          for (int a = 0; a < 3; ++a)
+            for (int bb = 0; bb < 3; ++bb) geom[a][bb] = (b[a] * b[bb] + c[a] * c[bb]) / (4.0 * area);
+          const double m = p.density * area / 12.0;
+          int lid[3], node[3];
+          bool free_[3];
+          for (int a = 0; a < 3; ++a) {
+            lid[a] = (gj[a] - sd.sy * g.my) * (mx + 1) + (gi[a] - sd.sx * g.mx);
+            node[a] = gj[a] * nn1 + gi[a];
+            free_[a] = g.dof(gi[a], gj[a]) >= 0;
+          }
+          for (int a = 0; a < 3; ++a)
+            for (int bb = 0; bb < 3; ++bb) {
+              if (!free_[a] || !free_[bb] || lid[bb] < lid[a]) continue;
+              const int sl = slot(lid[a], lid[bb], 1, mx + 1, mx + 2);
+              st.Ml[(size_t(s) * 4 + sl) * nl + lid[a]] += (a == bb ? 2 * m : m);
+              if (sl == 3) {
+                if (geom[a][bb] != 0.0) throw Error(1, "non-zero diagonal stiffness coupling");
+                continue;
+              }
+              for (int i = 0; i < nin; ++i) {
+                const double* cf = &p.coeff[size_t(i) * p.n_nodes()];
+                double cavg = 0.0;
+                for (int v = 0; v < 3; ++v) cavg += cf[node[v]];
+                cavg /= 3;
+                st.Kl[((size_t(s) * nin + i) * 3 + sl) * nl + lid[a]] += cavg * geom[a][bb];
+              }
+            }
+        }
+  };
+  const int nth = std::max(1, std::min<int>(g.ns, int(std::thread::hardware_concurrency())));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t)
+    th.emplace_back([&, t] {
+      for (int s = t; s < g.ns; s += nth) work(s);
+    });
+  for (auto& t : th) t.join();
+  return st;
+}
+
+// ------------------------------------------------------------- inputs ------
+namespace {
+double fact(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= i;
+  return f;
+}
+std::vector<std::vector<int>> graded_indices(int L, int p) {  // src/pce.cpp:19-37
+  std::vector<std::vector<int>> out;
+  std::vector<int> cur(L, 0);
+  std::function<void(int, int)> rec = [&](int pos, int rem) {
+    if (pos == L - 1) {
+      cur[pos] = rem;
+      out.push_back(cur);
+      return;
+    }
+    for (int a = rem; a >= 0; --a) {
+      cur[pos] = a;
+      rec(pos + 1, rem - a);
+    }
+  };
+  for (int d = 0; d <= p; ++d) rec(0, d);
+  return out;
+}
+// <He_a He_b He_c> / sqrt(a! b! c!)  (src/pce.cpp:60-67, :108-113)
+double triple_1d(int a, int b, int c) {
+  const int t = a + b + c;
+  if (t & 1) return 0.0;
+  const int s = t / 2;
+  if (s < a || s < b || s < c) return 0.0;
+  return fact(a) * fact(b) * fact(c) / (fact(s - a) * fact(s - b) * fact(s - c)) /
+         std::sqrt(fact(a) * fact(b) * fact(c));
+}
+// Roots of the exponential-kernel characteristic equations on [-1/2, 1/2] by
+// bisection (src/kle.cpp:16-68).
+struct Root {
+  double w, lambda;
+  bool even;
+};
+double bisect(double lo, double hi, const std::function<double(double)>& f) {
+  double flo = f(lo);
+  const double fhi = f(hi);
+  if (flo == 0.0) return lo;
+  if (fhi == 0.0) return hi;
+  if ((flo > 0.0) == (fhi > 0.0)) throw Error(1, "kle: bracket failure");
+  for (int it = 0; it < 200 && hi - lo > 1e-14 * hi; ++it) {
+    const double mid = 0.5 * (lo + hi), fm = f(mid);
+    if (fm == 0.0) return mid;
+    if ((fm > 0.0) == (flo > 0.0))
+      lo = mid, flo = fm;
+    else
+      hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+std::vector<Root> roots_1d(double b, int n) {
+  if (b <= 0.0) throw Error(1, "kle: correlation length must be positive");
+  const double c = 1.0 / b, T = 0.5, nudge = 1e-9;
+  auto fe = [&](double w) { return std::tan(w * T) - c / w; };
+  auto fo = [&](double w) { return std::tan(w * T) + w / c; };
+  auto pole = [&](int k) { return (0.5 + k) * M_PI / T; };
+  std::vector<Root> r;
+  r.push_back({bisect(nudge * pole(0), pole(0) * (1.0 - nudge), fe), 0, true});
+  for (int m = 1; int(r.size()) < n; ++m) {
+    const double lo = pole(m - 1), hi = pole(m), w = hi - lo;
+    r.push_back({bisect(lo + nudge * w, hi - nudge * w, fo), 0, false});
+    if (int(r.size()) < n) r.push_back({bisect(lo + nudge * w, hi - nudge * w, fe), 0, true});
+  }
+  r.resize(n);
+  for (Root& x : r) x.lambda = 2.0 * c / (x.w * x.w + c * c);
+  return r;
+}
+double eigfun(const Root& r, double x) {
+  const double T = 0.5, xc = x - 0.5;
+  return r.even ? std::cos(r.w * xc) / std::sqrt(T + std::sin(2.0 * r.w * T) / (2.0 * r.w))
+                : std::sin(r.w * xc) / std::sqrt(T - std::sin(2.0 * r.w * T) / (2.0 * r.w));
+}
+}  // namespace
+
+std::vector<std::vector<double>> lognormal_coeff(int nx, int ny, double sigma, double bx, double by,
+                                                 double g0, int L, int p_in) {
+  if (sigma < 0.0 || L < 1) throw Error(1, "kle_exponential: bad sigma / n_modes");
+  const auto ex = roots_1d(bx, L);
+  const auto ey = (by == bx) ? ex : roots_1d(by, L);
+  struct Pr {
+    int i, j;
+    double l;
+  };
+  std::vector<Pr> pr;
+  for (int i = 0; i < L; ++i)
+    for (int j = 0; j < L; ++j) pr.push_back({i, j, ex[i].lambda * ey[j].lambda});
+  std::sort(pr.begin(), pr.end(), [](const Pr& a, const Pr& b) {
+    if (a.l != b.l) return a.l > b.l;
+    return std::tie(a.i, a.j) < std::tie(b.i, b.j);
+  });
+  const int nn = (nx + 1) * (ny + 1);
+  std::vector<std::vector<double>> gv(L, std::vector<double>(nn));
+  for (int v = 0; v < L; ++v) {
+    const double sl = std::sqrt(sigma * sigma * pr[v].l);
+    for (int node = 0; node < nn; ++node) {
+      const double x = double(node % (nx + 1)) / nx, y = double(node / (nx + 1)) / ny;
+      gv[v][node] = sl * (eigfun(ex[pr[v].i], x) * eigfun(ey[pr[v].j], y));
+    }
+  }
+  std::vector<double> c0(nn);
+  for (int x = 0; x < nn; ++x) {
+    double s2 = 0.0;
+    for (int v = 0; v < L; ++v) s2 += gv[v][x] * gv[v][x];
+    c0[x] = std::exp(g0 + 0.5 * s2);
+  }
+  std::vector<std::vector<double>> out;
+  for (const auto& al : graded_indices(L, p_in)) {
+    std::vector<double> t = c0;
+    for (int v = 0; v < L; ++v)
+      if (al[v] > 0) {
+        double nrm = 1.0;
+        for (int a = 2; a <= al[v]; ++a) nrm *= a;
+        const double sn = std::sqrt(nrm);
+        for (int x = 0; x < nn; ++x) t[x] *= std::pow(gv[v][x], double(al[v])) / sn;
+      }
+    out.push_back(std::move(t));
+  }
+  return out;
+}
+
+// src/pce.cpp:96-122 with the order_in <= order_out guard lifted.
+TensorHost triple_products(int L, int p_in, int p_out) {
+  if (L < 1 || p_in < 0 || p_out < 0) throw Error(1, "triple_products: bad arguments");
+  const auto in = graded_indices(L, p_in), out = graded_indices(L, p_out);
+  TensorHost t;
+  t.n_in = int(in.size());
+  t.n_out = int(out.size());
+  for (int i = 0; i < t.n_in; ++i)
+    for (int j = 0; j < t.n_out; ++j)
+      for (int k = j; k < t.n_out; ++k) {
+        double v = 1.0;
+        for (int q = 0; q < L && v != 0.0; ++q) v *= triple_1d(in[i][q], out[j][q], out[k][q]);
+        if (v != 0.0) {
+          t.i.push_back(i);
+          t.j.push_back(j);
+          t.k.push_back(k);
+          t.v.push_back(v);
+        }
+      }
+  return t;
+}
+
+int nearest_node(int nx, int ny, double x, double y) {  // src/mesh.cpp:83-96
+  int best = 0;
+  double bd = std::numeric_limits<double>::max();
+  for (int node = 0; node < (nx + 1) * (ny + 1); ++node) {
+    const double dx = double(node % (nx + 1)) / nx - x, dy = double(node / (nx + 1)) / ny - y;
+    const double d = dx * dx + dy * dy;
+    if (d < bd) bd = d, best = node;
+  }
+  return best;
+}
+
+}  // namespace sgw

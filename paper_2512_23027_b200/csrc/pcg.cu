@@ -1,0 +1,524 @@
+// PCG hot path: batched packed-symmetric SYMV (SchurSystem::matvec, NN2 local
+// solves), the NN2 coarse problem and the CG vector algebra, all with fixed-
+// order (atomic-free) reductions so runs are bitwise reproducible.
+//
+// Reference: src/dd.cpp:142-157 (matvec), :199-253 (apply_nn2), src/pcg.cpp:7-50.
+#include <cmath>
+
+#include "solver.cuh"
+
+namespace sgw {
+
+long long g_launches = 0;
+
+enum Scal { RZ = 0, RZN = 1, PQ = 2, RR = 3, BB = 4, RT = 5, TMP = 6, NSCAL = 8 };
+constexpr int kRedBlocks = 512;  // max partial-sum blocks of a reduction
+
+// ------------------------------------------------------------ reductions ---
+// Block sum in fixed tree order, then the last block to finish sums the block
+// partials in index order: deterministic regardless of scheduling.
+__device__ void finalize_sum(double v, double* partials, unsigned* counter, double* out, double* out_prev) {
+  __shared__ double sh[32];
+  __shared__ bool last;
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double s = lane < (blockDim.x >> 5) ? sh[lane] : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) {
+      partials[blockIdx.x] = s;
+      __threadfence();
+      last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (last && w == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += ((volatile double*)partials)[b];
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (out_prev) *out_prev = *out;
+      *out = s;
+      *counter = 0u;
+    }
+  }
+}
+
+inline int red_grid(long long len) { return std::max(1, std::min<int>(kRedBlocks, cdiv(len, 256))); }
+
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                           double* partials, unsigned* counter, double* out, double* out_prev) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s += a[i] * b[i];
+  finalize_sum(s, partials, counter, out, out_prev);
+}
+
+// x += alpha p ; r -= alpha q ; rr = r.r   with alpha = scal[RZN] / scal[PQ]
+__global__ void cg_xr_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                             const double* __restrict__ q, long long n, double* scal, double* partials,
+                             unsigned* counter) {
+  const double alpha = scal[RZN] / scal[PQ];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    s += ri * ri;
+  }
+  finalize_sum(s, partials, counter, scal + RR, nullptr);
+}
+
+// p = z + (rz_next / rz) p  (src/pcg.cpp:45-47); first == 1: p = z
+__global__ void cg_p_kernel(double* __restrict__ p, const double* __restrict__ z, long long n, const double* scal,
+                            int first) {
+  const double beta = first ? 0.0 : scal[RZN] / scal[RZ];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = first ? z[i] : z[i] + beta * p[i];
+}
+
+// rt = b - ax ; scal[RT] = rt.rt
+__global__ void residual_kernel(double* __restrict__ rt, const double* __restrict__ b, const double* __restrict__ ax,
+                                long long n, double* scal, double* partials, unsigned* counter) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = b[i] - ax[i];
+    rt[i] = v;
+    s += v * v;
+  }
+  finalize_sum(s, partials, counter, scal + RT, nullptr);
+}
+
+// ------------------------------------------------------------- TilePack ----
+void TilePack::plan(const std::vector<int>& dims) {
+  nmat = int(dims.size());
+  dim = dims;
+  ntile.resize(nmat);
+  tile_base.resize(nmat + 1);
+  xoff.resize(nmat + 1);
+  tile_base[0] = 0;
+  xoff[0] = 0;
+  std::vector<int4> h;
+  for (int s = 0; s < nmat; ++s) {
+    ntile[s] = cdiv(dims[s], kTile);
+    tile_base[s + 1] = tile_base[s] + (long long)ntile[s] * (ntile[s] + 1) / 2;
+    xoff[s + 1] = xoff[s] + (long long)kTile * ntile[s];
+    for (int I = 0; I < ntile[s]; ++I)
+      for (int J = 0; J <= I; ++J) h.push_back(make_int4(s, I, J, 0));
+  }
+  n_tiles = tile_base[nmat];
+  xlen = xoff[nmat];
+  desc.upload(h);
+  tiles.alloc(size_t(n_tiles) * kTile * kTile);
+  rowpart.alloc(size_t(n_tiles) * kTile);
+  colpart.alloc(size_t(n_tiles) * kTile);
+  d_tile_base.upload(tile_base);
+  d_xoff.upload(xoff);
+  d_ntile.upload(ntile);
+  d_dim.upload(dim);
+}
+
+// Pack dense symmetric matrix s (column-major, leading dim ld, lower triangle
+// authoritative) into its lower tiles.  One CTA per tile.
+__global__ void pack_tiles_kernel(const int4* __restrict__ desc, int n, double* __restrict__ tiles,
+                                  const double* __restrict__ A, int L) {
+  const long long t = blockIdx.x;
+  const int4 d = desc[t];
+  const int I = d.y, J = d.z;
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int r = e / kTile, c = e % kTile, R = I * kTile + r, Cc = J * kTile + c;
+    double v = 0.0;
+    if (R < n && Cc < n) v = R >= Cc ? A[(size_t)Cc * L + R] : A[(size_t)R * L + Cc];
+    tiles[t * kTile * kTile + e] = v;
+  }
+}
+
+void pack_tiles_range(TilePack& tp, int s, const double* src, int ld, cudaStream_t st) {
+  const long long tb = tp.tile_base[s], te = tp.tile_base[s + 1];
+  if (te <= tb) return;
+  pack_tiles_kernel<<<(unsigned)(te - tb), 256, 0, st>>>(tp.desc.p + tb, tp.dim[s], tp.tiles.p + tb * kTile * kTile,
+                                                         src, ld);
+  SGW_LAUNCHED();
+}
+
+// ------------------------------------------------------------ tile SYMV ----
+// One CTA (8 warps) per 64x64 lower tile T_IJ of matrix s:
+//   rowpart[t] = T_IJ x_J            (partial of y_I)
+//   colpart[t] = T_IJ^T x_I  (I != J) (partial of y_J)
+// Warp w streams rows 8w..8w+7 with 128-bit loads (a warp reads one full
+// 512-byte tile row per load); row sums use a butterfly multi-row reduction.
+__global__ void __launch_bounds__(256) symv_tiles_kernel(const int4* __restrict__ desc,
+                                                         const double* __restrict__ tiles,
+                                                         const long long* __restrict__ xoff,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ rowpart,
+                                                         double* __restrict__ colpart) {
+  __shared__ double csum[8][kTile];
+  const long long t = blockIdx.x;
+  const int4 d = desc[t];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double2* T2 = reinterpret_cast<const double2*>(tiles + t * (kTile * kTile));
+  double2 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __ldcs(T2 + (w * 8 + q) * (kTile / 2) + lane);
+  const double* xb = x + xoff[d.x];
+  const double2 xj = reinterpret_cast<const double2*>(xb + d.z * kTile)[lane];
+  const double* xi = xb + d.y * kTile + w * 8;
+  double rs[8], c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    rs[q] = v[q].x * xj.x + v[q].y * xj.y;
+    const double xv = xi[q];
+    c0 += v[q].x * xv;
+    c1 += v[q].y * xv;
+  }
+  // butterfly: 8 row sums over 32 lanes -> lane holds row 4*b4 + 2*b3 + b2
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 16;
+    const double send = up ? rs[i] : rs[i + 4], keep = up ? rs[i + 4] : rs[i];
+    rs[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 8;
+    const double send = up ? rs[i] : rs[i + 2], keep = up ? rs[i + 2] : rs[i];
+    rs[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool up = lane & 4;
+    const double send = up ? rs[0] : rs[1], keep = up ? rs[1] : rs[0];
+    rs[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 2);
+  rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 1);
+  if ((lane & 3) == 0) {
+    const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    rowpart[t * kTile + w * 8 + row] = rs[0];
+  }
+  if (d.y != d.z) {
+    csum[w][2 * lane] = c0;
+    csum[w][2 * lane + 1] = c1;
+    __syncthreads();
+    if (threadIdx.x < kTile) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += csum[k][threadIdx.x];
+      colpart[t * kTile + threadIdx.x] = s;
+    }
+  }
+}
+
+// y_s[i] from the tile partials of matrix s, fixed order.
+__device__ __forceinline__ double tile_reduce(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                                              long long base, int nt, int i) {
+  const int I = i / kTile, r = i % kTile;
+  const long long rowb = base + (long long)I * (I + 1) / 2;
+  double s = 0.0;
+  for (int J = 0; J <= I; ++J) s += rowpart[(rowb + J) * kTile + r];
+  for (int K = I + 1; K < nt; ++K) s += colpart[(base + (long long)K * (K + 1) / 2 + I) * kTile + r];
+  return s;
+}
+
+void GpuSolver::symv(TilePack& tp, const double* xloc, double*) {
+  if (!tp.n_tiles) return;
+  symv_tiles_kernel<<<(unsigned)tp.n_tiles, 256, 0, st_>>>(tp.desc.p, tp.tiles.p, tp.d_xoff.p, xloc, tp.rowpart.p,
+                                                          tp.colpart.p);
+  SGW_LAUNCHED();
+}
+
+// ---------------------------------------------------- gather / scatter -----
+// LI[s][j*ng+p] = (w) X[j*n_iface + iface_pos[s][p]]
+__global__ void gather_li_kernel(const double* __restrict__ X, double* __restrict__ li, const long long* __restrict__ xoff,
+                                 const int* __restrict__ ip_off, const int* __restrict__ iface_pos,
+                                 const double* __restrict__ w, const int* __restrict__ ng, int ns, int nt,
+                                 int n_iface, int weighted) {
+  const int s = blockIdx.y;
+  const int a = ng[s] * nt;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < a; f += gridDim.x * blockDim.x) {
+    const int j = f / ng[s], p = f % ng[s];
+    double v = X[(long long)j * n_iface + iface_pos[ip_off[s] + p]];
+    if (weighted) v *= w[ip_off[s] + p];
+    li[xoff[s] + f] = v;
+  }
+}
+
+void GpuSolver::gather_li(const double* glob, double* li, bool weighted) {
+  dim3 grid(cdiv(NT * 4 * (G.mx + G.my), 256), NS);
+  gather_li_kernel<<<grid, 256, 0, st_>>>(glob, li, Sp.d_xoff.p, ip_off.p, iface_pos.p, iface_w.p, ng_d.p, NS, NT,
+                                           G.n_iface, weighted ? 1 : 0);
+  SGW_LAUNCHED();
+}
+
+// X[q] = sum over subdomains sharing interface node q (ascending s) of
+//        (w) * (tiles ? tile_reduce(S) : LI)[s][j*ng+p]   ;  optional dot(X, dw)
+template <bool FromTiles>
+__global__ void scatter_kernel(double* __restrict__ X, const double* __restrict__ li, const long long* __restrict__ xoff,
+                               const int* __restrict__ ip_off, const double* __restrict__ w,
+                               const int* __restrict__ inv_cnt, const int* __restrict__ inv_s,
+                               const int* __restrict__ inv_p, const int* __restrict__ ng, int n_iface, long long NG,
+                               int weighted, const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                               const long long* __restrict__ tile_base, const int* __restrict__ ntile,
+                               const double* __restrict__ dw, double* partials, unsigned* counter, double* dout) {
+  double acc = 0.0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < NG; q += (long long)gridDim.x * blockDim.x) {
+    const int j = int(q / n_iface), g = int(q % n_iface);
+    double y = 0.0;
+    for (int e = 0; e < inv_cnt[g]; ++e) {
+      const int s = inv_s[4 * g + e], p = inv_p[4 * g + e];
+      const int f = j * ng[s] + p;
+      double v = FromTiles ? tile_reduce(rowpart, colpart, tile_base[s], ntile[s], f) : li[xoff[s] + f];
+      if (weighted) v *= w[ip_off[s] + p];
+      y += v;
+    }
+    X[q] = y;
+    if (dw) acc += y * dw[q];
+  }
+  if (dw) finalize_sum(acc, partials, counter, dout, nullptr);
+}
+
+void GpuSolver::scatter_li(const double* li, double* glob, bool weighted, double* dot_with, double* dot_out) {
+  const int grid = red_grid(NG);
+  scatter_kernel<false><<<grid, 256, 0, st_>>>(glob, li, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
+                                               inv_p.p, ng_d.p, G.n_iface, NG, weighted ? 1 : 0, nullptr, nullptr,
+                                               nullptr, nullptr, dot_with, dpart.p, dcount.p, dot_out);
+  SGW_LAUNCHED();
+}
+
+// --------------------------------------------------------------- matvec ----
+void GpuSolver::schur_matvec(const double* x, double* y) {
+  gather_li(x, li_x.p, false);
+  symv(Sp, li_x.p, nullptr);
+  const int grid = red_grid(NG);
+  scatter_kernel<true><<<grid, 256, 0, st_>>>(y, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
+                                              inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
+                                              Sp.d_tile_base.p, Sp.d_ntile.p, nullptr, nullptr, nullptr, nullptr);
+  SGW_LAUNCHED();
+  ++T.matvecs;
+}
+
+// ------------------------------------------------------------------ NN2 ----
+// f = D_s R_s r split into f_r (r-space, padded per subdomain) and f_c.
+__global__ void nn2_gather_kernel(const double* __restrict__ r, const int* __restrict__ r_gidx,
+                                  const double* __restrict__ r_w, double* __restrict__ fr, long long nr_tot,
+                                  const int* __restrict__ c_gidx, const double* __restrict__ c_w,
+                                  double* __restrict__ fc, long long nc_tot) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nr_tot + nc_tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i < nr_tot) {
+      const int gi = r_gidx[i];
+      fr[i] = gi >= 0 ? r_w[i] * r[gi] : 0.0;
+    } else {
+      const long long k = i - nr_tot;
+      const int gi = c_gidx[k];
+      fc[k] = gi >= 0 ? c_w[k] * r[gi] : 0.0;
+    }
+  }
+}
+
+// d_s = f_c - Psi^T f_r   (= f_c - S_rc^T S_rr^-1 f_r, src/dd.cpp:214-217); warp per (s, c)
+__global__ void psi_t_kernel(const double* __restrict__ Psi, const long long* __restrict__ psioff,
+                             const double* __restrict__ fr, const long long* __restrict__ roff,
+                             const double* __restrict__ fc, const long long* __restrict__ coff,
+                             double* __restrict__ dsub, const int* __restrict__ nr, const int* __restrict__ nc,
+                             int nt, int ns) {
+  const int s = blockIdx.y;
+  const int csz = nc[s] * nt, rsz = nr[s] * nt;
+  const int lane = threadIdx.x & 31;
+  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < csz; c += gridDim.x * (blockDim.x >> 5)) {
+    const double* col = Psi + psioff[s] + (long long)c * rsz;
+    const double* f = fr + roff[s];
+    double acc = 0.0;
+    for (int a = lane; a < rsz; a += 32) acc += col[a] * f[a];
+    acc = warp_sum(acc);
+    if (lane == 0) dsub[coff[s] + c] = fc[coff[s] + c] - acc;
+  }
+}
+
+// d = sum_s B_s^T d_s in ascending s (src/dd.cpp:221-226)
+__global__ void coarse_assemble_kernel(const double* __restrict__ dsub, const long long* __restrict__ coff,
+                                       const int* __restrict__ cinv_cnt, const int* __restrict__ cinv_s,
+                                       const int* __restrict__ cinv_c, const int* __restrict__ nc, int n_corner,
+                                       int NC, double* __restrict__ d) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < NC; q += gridDim.x * blockDim.x) {
+    const int j = q / n_corner, g = q % n_corner;
+    double acc = 0.0;
+    for (int e = 0; e < cinv_cnt[g]; ++e) {
+      const int s = cinv_s[4 * g + e];
+      acc += dsub[coff[s] + j * nc[s] + cinv_c[4 * g + e]];
+    }
+    d[q] = acc;
+  }
+}
+
+// y = A x for a symmetric column-major n x n A (warp per row = column)
+__global__ void symv_dense_kernel(const double* __restrict__ A, const double* __restrict__ x, double* __restrict__ y,
+                                  int n) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
+    const double* col = A + (long long)r * n;
+    double acc = 0.0;
+    for (int c = lane; c < n; c += 32) acc += col[c] * x[c];
+    acc = warp_sum(acc);
+    if (lane == 0) y[r] = acc;
+  }
+}
+
+// zeta_s on the local interface: remaining  u_r = Q f_r - Psi u_c(s)  (tile partials of Q),
+// corners u_c(s)  (src/dd.cpp:230-246).  Unweighted; the scatter applies D_s.
+__global__ void nn2_local_kernel(double* __restrict__ li, const long long* __restrict__ lioff,
+                                 const int* __restrict__ ip_off, const int* __restrict__ pkind,
+                                 const int* __restrict__ ng, const int* __restrict__ nr, const int* __restrict__ nc,
+                                 int nt, const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                                 const long long* __restrict__ qbase, const int* __restrict__ qnt,
+                                 const double* __restrict__ Psi, const long long* __restrict__ psioff,
+                                 const double* __restrict__ uc, const int* __restrict__ corner_pos_flat,
+                                 const int* __restrict__ cp_off, int n_corner, int has_coarse) {
+  const int s = blockIdx.y;
+  const int a = ng[s] * nt, rsz = nr[s] * nt, ncs = nc[s];
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < a; f += gridDim.x * blockDim.x) {
+    const int j = f / ng[s], p = f % ng[s];
+    const int k = pkind[ip_off[s] + p];
+    double v;
+    if (k >= 0) {  // remaining dof: r-space index j*nr + k
+      const int ar = j * nr[s] + k;
+      v = tile_reduce(rowpart, colpart, qbase[s], qnt[s], ar);
+      if (has_coarse) {
+        const double* P = Psi + psioff[s] + ar;
+        for (int jc = 0; jc < nt; ++jc)
+          for (int cc = 0; cc < ncs; ++cc)
+            v -= P[(long long)(jc * ncs + cc) * rsz] * uc[jc * n_corner + corner_pos_flat[cp_off[s] + cc]];
+      }
+    } else {
+      const int cc = -1 - k;
+      v = has_coarse ? uc[j * n_corner + corner_pos_flat[cp_off[s] + cc]] : 0.0;
+    }
+    li[lioff[s] + f] = v;
+  }
+}
+
+void GpuSolver::apply_nn2(const double* r, double* z) {
+  const long long nr_tot = roff_.back(), nc_tot = coff_.back();
+  nn2_gather_kernel<<<red_grid(nr_tot + nc_tot), 256, 0, st_>>>(r, r_gidx.p, r_w.p, r_x.p, nr_tot, c_gidx.p, c_w.p,
+                                                                 c_f.p, nc_tot);
+  SGW_LAUNCHED();
+  symv(Qp, r_x.p, nullptr);
+  const bool has_coarse = NC > 0;
+  if (has_coarse) {
+    psi_t_kernel<<<dim3(cdiv(NT * 4, 8), NS), 256, 0, st_>>>(Psi.p, d_psioff.p, r_x.p, d_roff.p, c_f.p, d_coff.p,
+                                                              c_d.p, nr_d.p, nc_d.p, NT, NS);
+    SGW_LAUNCHED();
+    coarse_assemble_kernel<<<cdiv(NC, 256), 256, 0, st_>>>(c_d.p, d_coff.p, cinv_cnt.p, cinv_s.p, cinv_c.p, nc_d.p,
+                                                           G.n_corner, NC, dcoarse.p);
+    SGW_LAUNCHED();
+    symv_dense_kernel<<<cdiv(NC, 8), 256, 0, st_>>>(Finv.p, dcoarse.p, ucoarse.p, NC);
+    SGW_LAUNCHED();
+  }
+  nn2_local_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
+      li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, Qp.rowpart.p, Qp.colpart.p,
+      Qp.d_tile_base.p, Qp.d_ntile.p, Psi.p, d_psioff.p, ucoarse.p, cpos_flat_.p, cp_off_.p, G.n_corner,
+      has_coarse ? 1 : 0);
+  SGW_LAUNCHED();
+  scatter_li(li_y.p, z, true, nullptr, nullptr);
+  ++T.nn2s;
+}
+
+// -------------------------------------------------------------- vectors ----
+void GpuSolver::dot_dev(const double* a, const double* b, long long len, double* out) {
+  dot_kernel<<<red_grid(len), 256, 0, st_>>>(a, b, len, dpart.p, dcount.p, out, nullptr);
+  SGW_LAUNCHED();
+}
+
+double GpuSolver::dot_host(const double* a, const double* b, long long len) {
+  dot_dev(a, b, len, scal.p + TMP);
+  double h = 0;
+  SGW_CUDA(cudaMemcpyAsync(&h, scal.p + TMP, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  SGW_CUDA(cudaStreamSynchronize(st_));
+  return h;
+}
+
+// ------------------------------------------------------------------ PCG ----
+// src/pcg.cpp:7-50: x0 = 0; stop on the recurrence residual, confirm with the
+// true residual, restart from it (without resetting p) if the check fails.
+int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
+  cudaEventRecord(ev_[0], st_);
+  const long long N = NG;
+  const int grid = red_grid(N);
+  SGW_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st_));
+  const double bb = dot_host(b, b, N);
+  const double bnorm = std::sqrt(bb);
+  int iters = 0;
+  *converged = false;
+  if (hist) hist->clear();
+  if (bnorm == 0.0) {
+    *converged = true;
+    last_rel = 0.0;
+    if (hist) hist->push_back(0.0);
+    cudaEventRecord(ev_[1], st_);
+    cudaEventSynchronize(ev_[1]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+    T.pcg_ms += ms;
+    return 0;
+  }
+  SGW_CUDA(cudaMemcpyAsync(vr.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  apply_nn2(vr.p, vz.p);
+  dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
+  SGW_LAUNCHED();
+  cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 1);
+  SGW_LAUNCHED();
+  if (hist) hist->push_back(1.0);
+  for (int it = 0; it < P.max_iter; ++it) {
+    // q = S p with p.q fused into the scatter
+    gather_li(vp.p, li_x.p, false);
+    symv(Sp, li_x.p, nullptr);
+    scatter_kernel<true><<<grid, 256, 0, st_>>>(vq.p, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
+                                                inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
+                                                Sp.d_tile_base.p, Sp.d_ntile.p, vp.p, dpart.p, dcount.p, scal.p + PQ);
+    SGW_LAUNCHED();
+    ++T.matvecs;
+    cg_xr_kernel<<<grid, 256, 0, st_>>>(x, vr.p, vp.p, vq.p, N, scal.p, dpart.p, dcount.p);
+    SGW_LAUNCHED();
+    ++iters;
+    double rr = 0;
+    SGW_CUDA(cudaMemcpyAsync(&rr, scal.p + RR, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    SGW_CUDA(cudaStreamSynchronize(st_));
+    double rel = std::sqrt(rr) / bnorm;
+    last_rel = rel;
+    if (rel <= P.tol) {
+      schur_matvec(x, vq.p);
+      residual_kernel<<<grid, 256, 0, st_>>>(vrt.p, b, vq.p, N, scal.p, dpart.p, dcount.p);
+      SGW_LAUNCHED();
+      double rt = 0;
+      SGW_CUDA(cudaMemcpyAsync(&rt, scal.p + RT, sizeof(double), cudaMemcpyDeviceToHost, st_));
+      SGW_CUDA(cudaStreamSynchronize(st_));
+      rel = std::sqrt(rt) / bnorm;
+      last_rel = rel;
+      if (hist) hist->push_back(rel);
+      if (rel <= P.tol) {
+        *converged = true;
+        break;
+      }
+      SGW_CUDA(cudaMemcpyAsync(vr.p, vrt.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+    } else if (hist) {
+      hist->push_back(rel);
+    }
+    apply_nn2(vr.p, vz.p);
+    dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
+    SGW_LAUNCHED();
+    cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 0);
+    SGW_LAUNCHED();
+  }
+  cudaEventRecord(ev_[1], st_);
+  SGW_CUDA(cudaEventSynchronize(ev_[1]));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+  T.pcg_ms += ms;
+  T.iterations += iters;
+  return iters;
+}
+
+}  // namespace sgw

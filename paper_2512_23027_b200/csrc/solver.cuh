@@ -1,0 +1,208 @@
+// GPU SG solver: device-resident data of the interface-Schur PCG / NN2 path.
+//
+// Data layout in HBM (all fp64):
+//  * global state u, v, a, um, uc: term-major [j * n + d] (reference layout,
+//    src/sg.cpp:362-365).
+//  * global interface vectors: term-major [j * n_iface + q] (src/dd.cpp:86).
+//  * local interface vectors ("LI" buffers): per subdomain s a padded slice
+//    [li_off[s], li_off[s] + 64 * nt_S[s]) holding [j * ng_s + p].
+//  * S_s and Q_s = S_rr^-1: lower 64x64 tiles, row-major inside a tile,
+//    diagonal tiles stored full (TilePack).
+//  * Psi_s = S_rr^-1 S_rc: column-major r_s x c_s.  F_cc^-1: n_C x n_C.
+//  * interior factor: block-tridiagonal by interior grid rows, block B =
+//    W (P+1) (node-major, term-minor); Linv[s][k] = L_kk^-1 and
+//    Lsub[s][k] = L_{k+1,k}, column-major B x B.
+#pragma once
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "host.hpp"
+
+namespace sgw {
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void alloc(size_t count) {
+    reset();
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+      if (e != cudaSuccess) {
+        p = nullptr;
+        throw Error(6, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+      }
+      g_bytes += count * sizeof(T);
+    }
+  }
+  void upload(const std::vector<T>& h) {
+    alloc(h.size());
+    if (!h.empty()) SGW_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void zero(cudaStream_t st) {
+    if (n) SGW_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
+  void reset() {
+    if (p) {
+      cudaFree(p);
+      g_bytes -= n * sizeof(T);
+    }
+    p = nullptr;
+    n = 0;
+  }
+  static inline long long g_bytes = 0;
+};
+
+// Batch of symmetric matrices stored as lower 64x64 tiles.
+struct TilePack {
+  int nmat = 0;
+  std::vector<int> dim, ntile;       // per matrix: dimension, tiles per side
+  std::vector<long long> tile_base;  // first tile of each matrix
+  std::vector<long long> xoff;       // padded local-vector offset (64 * sum ntile)
+  long long n_tiles = 0, xlen = 0;
+  DBuf<int4> desc;  // per tile: {matrix, I, J, unused}
+  DBuf<double> tiles, rowpart, colpart;
+  DBuf<long long> d_tile_base, d_xoff;
+  DBuf<int> d_ntile, d_dim;
+  void plan(const std::vector<int>& dims);
+  long long bytes() const { return n_tiles * kTile * kTile * 8; }
+};
+
+// G tensor lists by output term k: entries (i, j, g) in for_each order.
+struct GList {
+  const int *ptr, *i, *j;
+  const double* v;
+};
+// Kernel-side view of the per-subdomain local operator data.
+struct LocalArgs {
+  const double *Kl, *Ml;
+  GList g;
+  const int* lid_to_p;
+  const long long* lioff;
+  const int* ng;
+  int nl, nin, nt, mx, my, px, nx, H, B;
+  double ms, ss;
+};
+
+struct Timers {
+  double pcg_ms = 0, step_ms = 0, rhs_ms = 0, rec_ms = 0;
+  long long iterations = 0, steps = 0, matvecs = 0, nn2s = 0;
+};
+
+class GpuSolver {
+ public:
+  GpuSolver(Problem p);
+  ~GpuSolver();
+
+  // reference-facing operations (device buffers in/out)
+  void apply_block(int op, const double* x, double* y);                 // K11
+  void schur_matvec(const double* x, double* y);                        // K1
+  void apply_nn2(const double* r, double* z);                           // K2-K4
+  int pcg(const double* b, double* x, bool* converged, std::vector<double>* hist);  // K5
+  void init_state(const double* u0_nodal_dev, const double* v0_nodal_dev, double f0_scale);
+  void set_force_point(int node, double f0, double t0, double amp);
+  void set_force_table(const double* table_host, int n_rows);
+  int step(int* iters_out);  // one Newmark step on device
+  std::vector<double> coarse_operator_host() const { return fcc_host_; }
+
+  cudaStream_t stream() const { return st_; }
+  void set_stream(cudaStream_t s);
+
+  Problem P;
+  Geometry G;
+  int NT = 0, NIN = 0, NS = 0, n = 0, NG = 0, NC = 0;  // NG = NT*n_iface, NC = NT*n_corner
+  size_t NSTATE = 0;
+  double setup_s = 0;
+  Timers T;
+  long long device_bytes() const { return DBuf<double>::g_bytes; }
+
+  // state
+  DBuf<double> u, v, a, um, uc, unext;
+  double t_now = 0.0;
+  int step_index = 0;
+  // probes (device history) filled per step
+  std::vector<int> probe_dofs;
+  DBuf<int> d_probe_dofs;
+  DBuf<double> probe_hist;  // [step][probe][2]: mean, std
+  int probe_cap = 0;
+  void record_probes(int step);
+  double last_rel = 0.0;  // final true residual of the last PCG solve
+
+ private:
+  void build_device_inputs(const Stencils& st);
+  void setup_interior_and_schur();
+  void setup_nn2();
+  void build_maps();
+  void sweep(double* x);  // x <- A_II^-1 x (block-row layout, all subdomains)
+  void gather_li(const double* glob, double* li, bool weighted);
+  void scatter_li(const double* li, double* glob, bool weighted, double* dot_with, double* dot_out);
+  void symv(TilePack& tp, const double* xloc, double* yloc_or_null);
+  double dot_host(const double* a, const double* b, long long len);
+  void dot_dev(const double* a, const double* b, long long len, double* out);
+  void local_force(double fext);
+  void mass_solve(double* x, const double* b);
+  LocalArgs local_args() const;
+  const double* force_at(double t, int row, double* fval);
+
+  cudaStream_t st_ = nullptr;
+  bool own_stream_ = false;
+  cublasHandle_t blas_ = nullptr;
+  cusolverDnHandle_t sol_ = nullptr;
+
+  // tensor: lists by output term k (i, j, g) and by pair (k, j) (i, g)
+  DBuf<int> gk_ptr, gk_i, gk_j, gp_ptr, gp_i;
+  DBuf<double> gk_v, gp_v;
+  // stencils
+  DBuf<double> Kg, Mg, Kl, Ml;
+  // geometry maps
+  DBuf<int> lid_to_p;           // [s * nl + lid]
+  DBuf<int> iface_pos;          // per subdomain local p -> global iface pos, flat with ip_off
+  DBuf<double> iface_w;
+  DBuf<int> ip_off;             // ns + 1
+  DBuf<int> inv_cnt, inv_s, inv_p;  // per global interface node: <= 4 (s, p), ascending s
+  DBuf<int> cinv_cnt, cinv_s, cinv_c;  // per corner node: <= 4 (s, local corner index)
+  DBuf<int> r_gidx, c_gidx;     // NN2 gather: r-space / c-space -> global flat, per subdomain padded
+  DBuf<double> r_w, c_w;
+  DBuf<int> iface_of_dof;       // reduced dof -> global interface position or -1
+  DBuf<int> pkind_;             // flat (ip_off): remaining index rho >= 0, or -1 - corner index
+  DBuf<int> cpos_flat_, cp_off_;  // per subdomain local corner -> global corner position
+  DBuf<int> ng_d, nr_d, nc_d;
+  std::vector<int> ng_, nr_, nc_;
+  std::vector<long long> roff_, coff_, psioff_;
+  DBuf<long long> d_roff, d_coff, d_psioff;
+
+  // PCG matrices
+  TilePack Sp, Qp;
+  DBuf<double> Psi, Finv;
+  std::vector<double> fcc_host_;
+  // interior factor
+  int B = 0, amax_ = 0;
+  DBuf<double> Sdense_;  // setup only
+  DBuf<int> iface_lid_;  // flat (ip_off): local interface p -> local node id
+  DBuf<double> Linv, Lsub;
+  // work vectors
+  DBuf<double> li_x, li_y, r_x, r_t, c_f, c_d, dcoarse, ucoarse;
+  DBuf<double> vb, vx, vr, vz, vp, vq, vrt;
+  DBuf<double> fI, yI, wI, fG;
+  DBuf<double> scal;  // device scalars
+  DBuf<double> dpart;
+  DBuf<unsigned> dcount;
+  // forcing
+  int force_kind_ = 0, force_node_ = -1, force_dof_ = -1;
+  double force_f0_ = 0, force_t0_ = 0, force_amp_ = 0;
+  std::vector<double> force_table_;
+  DBuf<double> force_row_, fext_;
+  cudaEvent_t ev_[8];
+};
+
+}  // namespace sgw

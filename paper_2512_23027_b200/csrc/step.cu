@@ -1,0 +1,507 @@
+// Per-Newmark-step kernels: stochastic-Galerkin stencil operator applies
+// (global apply_block_*, local force, A_GI / A_IG couplings), the batched
+// block-tridiagonal Dirichlet sweeps and the fused Newmark predictor/update.
+//
+// Reference: src/sg.cpp:252-356 (local_force, step_rhs_and_solve),
+// src/sg.cpp:358-423 (run), src/sg.cpp:425-447 (apply_block_*),
+// src/newmark.cpp:16-49.
+#include <cmath>
+
+#include "solver.cuh"
+
+namespace sgw {
+
+__constant__ int sDI[7] = {0, 1, -1, 0, 0, 1, -1};
+__constant__ int sDJ[7] = {0, 0, 0, 1, -1, 1, -1};
+
+// coefficient of direction dir from a 3-component (K) or 4-component (M)
+// stencil with component stride cs; own node o, neighbour nb.
+__device__ __forceinline__ double kco(const double* K, long long cs, long long o, long long nb, int dir) {
+  switch (dir) {
+    case 0: return __ldg(K + o);
+    case 1: return __ldg(K + cs + o);
+    case 2: return __ldg(K + cs + nb);
+    case 3: return __ldg(K + 2 * cs + o);
+    case 4: return __ldg(K + 2 * cs + nb);
+    default: return 0.0;
+  }
+}
+__device__ __forceinline__ double mco(const double* M, long long cs, long long o, long long nb, int dir) {
+  switch (dir) {
+    case 0: return __ldg(M + o);
+    case 1: return __ldg(M + cs + o);
+    case 2: return __ldg(M + cs + nb);
+    case 3: return __ldg(M + 2 * cs + o);
+    case 4: return __ldg(M + 2 * cs + nb);
+    case 5: return __ldg(M + 3 * cs + o);
+    default: return __ldg(M + 3 * cs + nb);
+  }
+}
+
+
+// ------------------------------------------------------ global operator ---
+// y_k = cm * sum_nb M x_k + ck * sum_{(i,j,g) in G_k} g sum_nb K_i x_j on the
+// reduced (nx-1) x (ny-1) dof grid (src/sg.cpp:425-447).  Thread per (d, k).
+__global__ void sg_apply_global_kernel(const double* __restrict__ Kg, const double* __restrict__ Mg, int n, int rw,
+                                       int rh, int nt, GList g, const double* __restrict__ x, double* __restrict__ y,
+                                       double cm, double ck) {
+  const long long total = (long long)n * nt;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int d = int(t % n), k = int(t / n);
+    const int il = d % rw, jl = d / rw;
+    int nb[7];
+    bool ok[7];
+#pragma unroll
+    for (int dir = 0; dir < 7; ++dir) {
+      const int i2 = il + sDI[dir], j2 = jl + sDJ[dir];
+      ok[dir] = i2 >= 0 && i2 < rw && j2 >= 0 && j2 < rh;
+      nb[dir] = ok[dir] ? j2 * rw + i2 : d;
+    }
+    double ym = 0.0, yk = 0.0;
+    if (cm != 0.0) {
+      const double* xk = x + (long long)k * n;
+#pragma unroll
+      for (int dir = 0; dir < 7; ++dir)
+        if (ok[dir]) ym += mco(Mg, n, d, nb[dir], dir) * xk[nb[dir]];
+    }
+    if (ck != 0.0) {
+      for (int e = g.ptr[k]; e < g.ptr[k + 1]; ++e) {
+        const double* Ki = Kg + (long long)g.i[e] * 3 * n;
+        const double* xj = x + (long long)g.j[e] * n;
+        double s = 0.0;
+#pragma unroll
+        for (int dir = 0; dir < 5; ++dir)
+          if (ok[dir]) s += kco(Ki, n, d, nb[dir], dir) * xj[nb[dir]];
+        yk += g.v[e] * s;
+      }
+    }
+    y[t] = cm * ym + ck * yk;
+  }
+}
+
+void GpuSolver::apply_block(int op, const double* x, double* y) {
+  const double cm = op == 0 ? 1.0 : op == 1 ? 0.0 : P.mass_scale;
+  const double ck = op == 0 ? 0.0 : op == 1 ? 1.0 : P.stiff_scale;
+  const long long total = (long long)NSTATE;
+  sg_apply_global_kernel<<<std::min(cdiv(total, 256), 8 * kNumSMs * 16), 256, 0, st_>>>(
+      Kg.p, Mg.p, n, P.nx - 1, P.ny - 1, NT, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, x, y, cm, ck);
+  SGW_LAUNCHED();
+}
+
+// -------------------------------------------------------- local operators --
+// reduced dof of local node (il, jl) of subdomain s; callers only ask for
+// non-Dirichlet nodes (lid_to_p != -1)
+__device__ __forceinline__ int lid_dof(const LocalArgs& A, int s, int il, int jl) {
+  const int gi = (s % A.px) * A.mx + il, gj = (s / A.px) * A.my + jl;
+  return (gj - 1) * (A.nx - 1) + gi - 1;
+}
+__device__ __forceinline__ long long interior_index(const LocalArgs& A, int s, int il, int jl, int term) {
+  return ((long long)s * A.H + (jl - 1)) * A.B + (long long)(il - 1) * A.nt + term;
+}
+
+// Local force on every local node of every subdomain (src/sg.cpp:252-293):
+//   f_k = M (um_k + a0 uc_k) + a1 sum G_ijk K_i uc_j  (+ f_ext on k = 0,
+//   weighted by D_s on the interface).  Interior rows -> yI (block-row layout),
+//   interface rows -> fG (LI layout).
+__global__ void local_force_kernel(LocalArgs A, int n, const double* __restrict__ um, const double* __restrict__ uc,
+                                   double a0, double a1, const double* __restrict__ fnext, int fdof, double fval,
+                                   const double* __restrict__ iface_w, const int* __restrict__ ip_off,
+                                   double* __restrict__ yI, double* __restrict__ fG, int ns) {
+  const long long total = (long long)ns * A.nl * A.nt;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
+    const int cls = A.lid_to_p[(long long)s * A.nl + lid];
+    if (cls == -1) continue;  // Dirichlet node
+    const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
+    const double* Ms = A.Ml + (long long)s * 4 * A.nl;
+    const double* Ks = A.Kl + (long long)s * A.nin * 3 * A.nl;
+    int nbl[7], nbd[7];
+#pragma unroll
+    for (int dir = 0; dir < 7; ++dir) {
+      const int i2 = il + sDI[dir], j2 = jl + sDJ[dir];
+      const bool in = i2 >= 0 && i2 <= A.mx && j2 >= 0 && j2 <= A.my;
+      nbl[dir] = in ? j2 * (A.mx + 1) + i2 : lid;
+      nbd[dir] = (in && A.lid_to_p[(long long)s * A.nl + nbl[dir]] != -1) ? lid_dof(A, s, i2, j2) : -1;
+    }
+    double f = 0.0;
+#pragma unroll
+    for (int dir = 0; dir < 7; ++dir)
+      if (nbd[dir] >= 0) {
+        const long long o = (long long)k * n + nbd[dir];
+        f += mco(Ms, A.nl, lid, nbl[dir], dir) * (um[o] + a0 * uc[o]);
+      }
+    if (a1 > 0.0) {
+      for (int e = A.g.ptr[k]; e < A.g.ptr[k + 1]; ++e) {
+        const double* Ki = Ks + (long long)A.g.i[e] * 3 * A.nl;
+        const double* xj = uc + (long long)A.g.j[e] * n;
+        double sacc = 0.0;
+#pragma unroll
+        for (int dir = 0; dir < 5; ++dir)
+          if (nbd[dir] >= 0) sacc += kco(Ki, A.nl, lid, nbl[dir], dir) * xj[nbd[dir]];
+        f += (a1 * A.g.v[e]) * sacc;
+      }
+    }
+    const int mydof = nbd[0];
+    const double wgt = cls >= 0 ? iface_w[ip_off[s] + cls] : 1.0;
+    if (k == 0) {
+      if (fnext) f += wgt * fnext[mydof];
+      else if (mydof == fdof) f += wgt * fval;
+    }
+    if (cls == -2)
+      yI[interior_index(A, s, il, jl, k)] = f;
+    else
+      fG[A.lioff[s] + (long long)k * A.ng[s] + cls] = f;
+  }
+}
+
+// Transient-operator product restricted to couplings between node classes.
+//  mode 0 (A_GI y):  out_LI[s][k*ng+p] = fG - sum_{interior nb} A(p,nb) y(nb)
+//  mode 1 (A_IG u):  out_I[s][..]      = sum_{interface nb} A(lid,nb) uLI(nb)
+__global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict__ yI, const double* __restrict__ fG,
+                                const double* __restrict__ uLI, const int* __restrict__ ip_off,
+                                const int* __restrict__ iface_lid, double* __restrict__ outLI,
+                                double* __restrict__ outI, int ns) {
+  const long long total = (long long)ns * A.nl * A.nt;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
+    const int cls = A.lid_to_p[(long long)s * A.nl + lid];
+    if (mode == 0 ? cls < 0 : cls != -2) continue;
+    const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
+    const double* Ms = A.Ml + (long long)s * 4 * A.nl;
+    const double* Ks = A.Kl + (long long)s * A.nin * 3 * A.nl;
+    const int ng = A.ng[s];
+    double acc = 0.0;
+    for (int dir = 1; dir < 7; ++dir) {
+      const int i2 = il + sDI[dir], j2 = jl + sDJ[dir];
+      if (i2 < 0 || i2 > A.mx || j2 < 0 || j2 > A.my) continue;
+      const int nb = j2 * (A.mx + 1) + i2;
+      const int c2 = A.lid_to_p[(long long)s * A.nl + nb];
+      if (mode == 0 ? c2 != -2 : c2 < 0) continue;
+      // value of the other node for term j
+      auto val = [&](int j) -> double {
+        return mode == 0 ? yI[interior_index(A, s, i2, j2, j)] : uLI[A.lioff[s] + (long long)j * ng + c2];
+      };
+      acc += A.ms * mco(Ms, A.nl, lid, nb, dir) * val(k);
+      if (dir < 5)
+        for (int e = A.g.ptr[k]; e < A.g.ptr[k + 1]; ++e)
+          acc += (A.ss * A.g.v[e]) * kco(Ks + (long long)A.g.i[e] * 3 * A.nl, A.nl, lid, nb, dir) * val(A.g.j[e]);
+    }
+    if (mode == 0) {
+      const long long o = A.lioff[s] + (long long)k * ng + cls;
+      outLI[o] = fG[o] - acc;
+    } else {
+      outI[interior_index(A, s, il, jl, k)] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------ Dirichlet sweeps ---
+// t = b - A x over column-major B x B blocks (A may be null: t = b); batched.
+__global__ void __launch_bounds__(256) gemv_n_sub_kernel(const double* __restrict__ A, long long sA,
+                                                         const double* __restrict__ x, long long sx,
+                                                         const double* __restrict__ b, long long sb,
+                                                         double* __restrict__ out, long long so, int Bn, int lower) {
+  __shared__ double red[8][33];
+  const int s = blockIdx.y;
+  const int rl = threadIdx.x & 31, cg = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + rl;
+  double acc = 0.0;
+  if (A && r < Bn) {
+    const double* As = A + s * sA;
+    const double* xs = x + s * sx;
+    const int cmax = lower ? r + 1 : Bn;
+    for (int c = cg; c < cmax; c += 8) acc += As[(long long)c * Bn + r] * xs[c];
+  }
+  red[cg][rl] = acc;
+  __syncthreads();
+  if (cg == 0 && r < Bn) {
+    double tot = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += red[q][rl];
+    out[s * so + r] = b ? b[s * sb + r] - tot : tot;
+  }
+}
+
+// out = b - A^T x ; warp per output column (A may be null: out = b).
+// lower: A lower triangular, so (A^T x)[c] = sum_{r >= c} A[c*B + r] x[r].
+__global__ void gemv_t_sub_kernel(const double* __restrict__ A, long long sA, const double* __restrict__ x,
+                                  long long sx, const double* __restrict__ b, long long sb, double* __restrict__ out,
+                                  long long so, int Bn, int lower, int negate) {
+  const int s = blockIdx.y, lane = threadIdx.x & 31;
+  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < Bn; c += gridDim.x * (blockDim.x >> 5)) {
+    double acc = 0.0;
+    if (A) {
+      const double* col = A + s * sA + (long long)c * Bn;
+      const double* xs = x + s * sx;
+      for (int r = (lower ? c : 0) + lane; r < Bn; r += 32) acc += col[r] * xs[r];
+      acc = warp_sum(acc);
+    }
+    if (lane == 0) out[s * so + c] = negate ? (b ? b[s * sb + c] : 0.0) - acc : acc;
+  }
+}
+
+void GpuSolver::sweep(double* x) {
+  const int H = G.H, ns = NS;
+  const long long BB = (long long)B * B, sI = (long long)H * B;
+  double* t = fI.p;  // scratch (ns x H x B)
+  const dim3 gn(cdiv(B, 32), ns), gt(cdiv(B, 8), ns);
+  // forward: x_k <- Linv_kk (x_k - Lsub_{k-1} x_{k-1})
+  for (int k = 0; k < H; ++k) {
+    gemv_n_sub_kernel<<<gn, 256, 0, st_>>>(k ? Lsub.p + (k - 1) * BB : nullptr, (long long)(H - 1) * BB,
+                                           x + (k - 1) * (long long)B, sI, x + k * (long long)B, sI, t, B, B, 0);
+    SGW_LAUNCHED();
+    gemv_n_sub_kernel<<<gn, 256, 0, st_>>>(Linv.p + k * BB, (long long)H * BB, t, B, nullptr, 0,
+                                           x + k * (long long)B, sI, B, 1);
+    SGW_LAUNCHED();
+  }
+  // backward: x_k <- Linv_kk^T (x_k - Lsub_k^T x_{k+1})
+  for (int k = H - 1; k >= 0; --k) {
+    gemv_t_sub_kernel<<<gt, 256, 0, st_>>>(k < H - 1 ? Lsub.p + k * BB : nullptr, (long long)(H - 1) * BB,
+                                           x + (k + 1) * (long long)B, sI, x + k * (long long)B, sI, t, B, B, 0, 1);
+    SGW_LAUNCHED();
+    gemv_t_sub_kernel<<<gt, 256, 0, st_>>>(Linv.p + k * BB, (long long)H * BB, t, B, nullptr, 0,
+                                           x + k * (long long)B, sI, B, 1, 0);
+    SGW_LAUNCHED();
+  }
+}
+
+// --------------------------------------------------------------- Newmark ---
+__global__ void predictor_kernel(const double* __restrict__ u, const double* __restrict__ v,
+                                 const double* __restrict__ a, double* __restrict__ um, double* __restrict__ uc,
+                                 long long N, double dt, double zeta, double gamma) {
+  const double zdd = zeta * dt * dt, c1 = (1.0 - 2.0 * zeta) / (2.0 * zeta);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const double m = (u[i] + dt * v[i]) / zdd + c1 * a[i];  // src/newmark.cpp:16-20
+    um[i] = m;
+    uc[i] = gamma * dt * m - v[i] - (1.0 - gamma) * dt * a[i];  // :22-26
+  }
+}
+
+// u_next from the interface solution and the recovered interiors, then the
+// Newmark update (src/sg.cpp:334-354, src/newmark.cpp:39-49).
+__global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, double* __restrict__ a,
+                              const double* __restrict__ ug, const double* __restrict__ yI,
+                              const double* __restrict__ wI, const int* __restrict__ iface_of_dof, int n, int nt,
+                              int n_iface, int nx, int mx, int my, int px, int H, int B, double dt, double zeta,
+                              double gamma) {
+  const long long N = (long long)n * nt;
+  const double zdd = zeta * dt * dt, c1 = (1.0 - 2.0 * zeta) / (2.0 * zeta);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+    const int d = int(t % n), k = int(t / n);
+    const int q = iface_of_dof[d];
+    double un;
+    if (q >= 0) {
+      un = ug[(long long)k * n_iface + q];
+    } else {
+      const int gi = d % (nx - 1) + 1, gj = d / (nx - 1) + 1;
+      const int sx = gi / mx, sy = gj / my, il = gi - sx * mx, jl = gj - sy * my;
+      const long long idx = ((long long)(sy * px + sx) * H + (jl - 1)) * B + (long long)(il - 1) * nt + k;
+      un = yI[idx] - wI[idx];
+    }
+    const double uo = u[t], vo = v[t], ao = a[t];
+    const double an = (un - uo - dt * vo) / zdd - c1 * ao;
+    v[t] = vo + (1.0 - gamma) * dt * ao + gamma * dt * an;
+    a[t] = an;
+    u[t] = un;
+  }
+}
+
+__global__ void probe_kernel(const double* __restrict__ u, const int* __restrict__ pd, int np, int n, int nt,
+                             double* __restrict__ out) {
+  for (int p = threadIdx.x; p < np; p += blockDim.x) {
+    double var = 0.0;
+    for (int j = 1; j < nt; ++j) {
+      const double c = u[(long long)j * n + pd[p]];
+      var += c * c;
+    }
+    out[2 * p] = u[pd[p]];
+    out[2 * p + 1] = sqrt(var);
+  }
+}
+
+__global__ void reduce_nodal_kernel(const double* __restrict__ nodal, double* __restrict__ out, int nx, int ny) {
+  const int n = (nx - 1) * (ny - 1);
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const int gi = d % (nx - 1) + 1, gj = d / (nx - 1) + 1;
+    out[d] = nodal[gj * (nx + 1) + gi];
+  }
+}
+
+__global__ void axpby_kernel(double* __restrict__ y, const double* __restrict__ x, long long N, double a, double b) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * y[i] + b * x[i];
+}
+__global__ void cg_mass_update(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
+                               const double* __restrict__ q, const double* __restrict__ z, long long N, double alpha) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    r[i] -= alpha * q[i];
+  }
+}
+
+// res = ((f0 - a0 M v) - a1 K v) - K u   (src/sg.cpp:367-369)
+__global__ void init_resid_kernel(double* __restrict__ res, const double* __restrict__ mv,
+                                  const double* __restrict__ kv, const double* __restrict__ ku, long long N,
+                                  double a0, double a1) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+    res[i] = res[i] - a0 * mv[i] - a1 * kv[i] - ku[i];
+}
+
+// (I (x) M) x = b by CG (initial acceleration, src/sg.cpp:370-376).  M is
+// SPD with kappa < 10, so CG reaches 1e-15 in a few dozen iterations.
+void GpuSolver::mass_solve(double* x, const double* b) {
+  const long long N = (long long)NSTATE;
+  DBuf<double> r, p, q;
+  r.alloc(N), p.alloc(N), q.alloc(N);
+  SGW_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st_));
+  SGW_CUDA(cudaMemcpyAsync(r.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  SGW_CUDA(cudaMemcpyAsync(p.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  const double bb = dot_host(b, b, N);
+  if (bb == 0.0) return;
+  double rr = bb;
+  const int grid = std::min(cdiv(N, 256), 4096);
+  for (int it = 0; it < 500 && rr > 1e-32 * bb; ++it) {
+    apply_block(0, p.p, q.p);
+    const double pq = dot_host(p.p, q.p, N);
+    const double alpha = rr / pq;
+    cg_mass_update<<<grid, 256, 0, st_>>>(x, r.p, p.p, q.p, nullptr, N, alpha);
+    SGW_LAUNCHED();
+    const double rr2 = dot_host(r.p, r.p, N);
+    axpby_kernel<<<grid, 256, 0, st_>>>(p.p, r.p, N, rr2 / rr, 1.0);
+    SGW_LAUNCHED();
+    rr = rr2;
+  }
+}
+
+// ---------------------------------------------------------------- driver ---
+void GpuSolver::set_force_point(int node, double f0, double t0, double amp) {
+  force_kind_ = node >= 0 ? 1 : 0;
+  force_node_ = node;
+  const int gi = node % (P.nx + 1), gj = node / (P.nx + 1);
+  force_dof_ = node >= 0 ? G.dof(gi, gj) : -1;
+  force_f0_ = f0, force_t0_ = t0, force_amp_ = amp;
+}
+
+void GpuSolver::set_force_table(const double* table, int rows) {
+  force_kind_ = 2;
+  force_table_.assign(table, table + (size_t)rows * P.n_nodes());
+  force_row_.alloc(P.n_nodes());
+  if (fext_.n != (size_t)n) fext_.alloc(n);
+}
+
+static double ricker(double t, double f0, double t0, double amp) {
+  const double a = M_PI * M_PI * f0 * f0 * (t - t0) * (t - t0);
+  return amp * (1.0 - 2.0 * a) * std::exp(-a);
+}
+
+// Force at time t as a reduced vector (kind 2) or a point value (kind 1).
+const double* GpuSolver::force_at(double t, int row, double* fval) {
+  *fval = 0.0;
+  if (force_kind_ == 1) {
+    *fval = force_dof_ >= 0 ? ricker(t, force_f0_, force_t0_, force_amp_) : 0.0;
+    return nullptr;
+  }
+  if (force_kind_ == 2) {
+    const size_t nn = P.n_nodes();
+    if ((size_t)row * nn >= force_table_.size()) throw Error(1, "force table too short");
+    SGW_CUDA(cudaMemcpyAsync(force_row_.p, force_table_.data() + (size_t)row * nn, nn * sizeof(double),
+                             cudaMemcpyHostToDevice, st_));
+    reduce_nodal_kernel<<<cdiv(n, 256), 256, 0, st_>>>(force_row_.p, fext_.p, P.nx, P.ny);
+    SGW_LAUNCHED();
+    return fext_.p;
+  }
+  return nullptr;
+}
+
+LocalArgs GpuSolver::local_args() const {
+  return LocalArgs{Kl.p, Ml.p, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, lid_to_p.p, Sp.d_xoff.p, ng_d.p, G.nl, NIN,
+                   NT, G.mx, G.my, G.px, P.nx, G.H, B, P.mass_scale, P.stiff_scale};
+}
+
+// src/sg.cpp:358-376: u, v in block 0, a = M^-1 (f0 - a0 M v - a1 K v - K u).
+void GpuSolver::init_state(const double* u0_nodal, const double* v0_nodal, double) {
+  u.zero(st_), v.zero(st_), a.zero(st_);
+  reduce_nodal_kernel<<<cdiv(n, 256), 256, 0, st_>>>(u0_nodal, u.p, P.nx, P.ny);
+  SGW_LAUNCHED();
+  reduce_nodal_kernel<<<cdiv(n, 256), 256, 0, st_>>>(v0_nodal, v.p, P.nx, P.ny);
+  SGW_LAUNCHED();
+  t_now = 0.0;
+  step_index = 0;
+  // resid = f0 - a0 M v - a1 K v - K u
+  DBuf<double> mv, kv, ku, res;
+  mv.alloc(NSTATE), kv.alloc(NSTATE), ku.alloc(NSTATE), res.alloc(NSTATE);
+  apply_block(0, v.p, mv.p);
+  apply_block(1, v.p, kv.p);
+  apply_block(1, u.p, ku.p);
+  res.zero(st_);
+  double fval = 0.0;
+  const double* fvec = force_at(0.0, 0, &fval);
+  if (fvec)
+    SGW_CUDA(cudaMemcpyAsync(res.p, fvec, n * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  else if (force_kind_ == 1 && force_dof_ >= 0)
+    SGW_CUDA(cudaMemcpyAsync(res.p + force_dof_, &fval, sizeof(double), cudaMemcpyHostToDevice, st_));
+  init_resid_kernel<<<cdiv((long long)NSTATE, 256), 256, 0, st_>>>(res.p, mv.p, kv.p, ku.p, (long long)NSTATE,
+                                                                    P.alpha0, P.alpha1);
+  SGW_LAUNCHED();
+  mass_solve(a.p, res.p);
+  SGW_CUDA(cudaStreamSynchronize(st_));
+}
+
+void GpuSolver::record_probes(int k) {
+  if (probe_dofs.empty() || k >= probe_cap) return;
+  probe_kernel<<<1, 128, 0, st_>>>(u.p, d_probe_dofs.p, (int)probe_dofs.size(), n, NT,
+                                   probe_hist.p + (size_t)k * probe_dofs.size() * 2);
+  SGW_LAUNCHED();
+}
+
+int GpuSolver::step(int* iters_out) {
+  const long long N = (long long)NSTATE;
+  const int grid = std::min(cdiv(N, 256), 8 * kNumSMs * 8);
+  cudaEventRecord(ev_[2], st_);
+  predictor_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, um.p, uc.p, N, P.dt, P.zeta, P.gamma);
+  SGW_LAUNCHED();
+  double fval = 0.0;
+  const double* fvec = force_at(t_now + P.dt, step_index + 1, &fval);
+  const LocalArgs A = local_args();
+  const long long tl = (long long)NS * G.nl * NT;
+  local_force_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(
+      A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, force_kind_ == 1 ? force_dof_ : -1, fval, iface_w.p, ip_off.p,
+      yI.p, fG.p, NS);
+  SGW_LAUNCHED();
+  sweep(yI.p);  // y = A_II^-1 f_I
+  coupling_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(A, 0, yI.p, fG.p, nullptr, ip_off.p,
+                                                                   iface_lid_.p, li_y.p, nullptr, NS);
+  SGW_LAUNCHED();
+  scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
+  cudaEventRecord(ev_[3], st_);
+  bool conv = false;
+  const int it = pcg(vb.p, vx.p, &conv, nullptr);
+  if (!conv)
+    throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+  cudaEventRecord(ev_[4], st_);
+  gather_li(vx.p, li_x.p, false);
+  coupling_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(A, 1, nullptr, nullptr, li_x.p, ip_off.p,
+                                                                   iface_lid_.p, nullptr, wI.p, NS);
+  SGW_LAUNCHED();
+  sweep(wI.p);  // A_II^-1 A_IG u_G
+  update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
+                                       G.mx, G.my, G.px, G.H, B, P.dt, P.zeta, P.gamma);
+  SGW_LAUNCHED();
+  t_now = t_now + P.dt;
+  ++step_index;
+  record_probes(step_index);
+  cudaEventRecord(ev_[5], st_);
+  SGW_CUDA(cudaEventSynchronize(ev_[5]));
+  float ms_rhs = 0, ms_rec = 0, ms_all = 0;
+  cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);
+  cudaEventElapsedTime(&ms_rec, ev_[4], ev_[5]);
+  cudaEventElapsedTime(&ms_all, ev_[2], ev_[5]);
+  T.rhs_ms += ms_rhs;
+  T.rec_ms += ms_rec;
+  T.step_ms += ms_all;
+  ++T.steps;
+  if (iters_out) *iters_out = it;
+  return it;
+}
+
+}  // namespace sgw

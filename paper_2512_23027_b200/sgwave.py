@@ -1,0 +1,357 @@
+"""ctypes mirror of the reference solver interface over libsgw_b200.so.
+
+Names, argument meaning and error behaviour follow the reference:
+  SgSolver(mesh, partition, coeff, tensor, density, alpha0, alpha1, params, options)
+      include/sgwave/sg.hpp:45-47  (mesh/partition given by their structured sizes)
+  SgSolver.run(u0_nodal, v0_nodal, n_steps, force) -> SgHistory   sg.hpp:49-50
+  SgSolver.apply_block_mass/stiffness/transient                    sg.hpp:58-60
+  SgSolver.schur().matvec / apply_nn2 / coarse_operator            dd.hpp:85-90
+  SgSolver.pcg(rhs) == pcg(matvec, apply_nn2, rhs, tol, max_iter)   pcg.hpp:20-21
+Errors raise SgError subclasses matching the reference exception classes:
+std::invalid_argument -> ValueError, factorization / non-convergence ->
+RuntimeError (see include/sgw.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+SGW_OK, SGW_EINVAL, SGW_EFACTOR, SGW_ENOCONV, SGW_ECUDA, SGW_ENCCL, SGW_ENOMEM = range(7)
+
+
+class SgError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class SgInvalidArgument(SgError, ValueError):
+    pass
+
+
+def lib_path():
+    return os.path.join(_PKG, "lib", "libsgw_b200.so")
+
+
+class _Problem(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("px", C.c_int), ("py", C.c_int),
+                ("n_input", C.c_int), ("coeff", C.c_void_p), ("n_output", C.c_int), ("n_entries", C.c_int),
+                ("ent_i", C.c_void_p), ("ent_j", C.c_void_p), ("ent_k", C.c_void_p), ("ent_v", C.c_void_p),
+                ("density", C.c_double), ("alpha0", C.c_double), ("alpha1", C.c_double),
+                ("gamma", C.c_double), ("zeta", C.c_double), ("dt", C.c_double),
+                ("tol", C.c_double), ("max_iter", C.c_int), ("device", C.c_int),
+                ("rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p)]
+
+
+class _Force(C.Structure):
+    _fields_ = [("kind", C.c_int), ("node", C.c_int), ("f0", C.c_double), ("t0", C.c_double),
+                ("amp", C.c_double), ("table", C.c_void_p)]
+
+
+class _History(C.Structure):
+    _fields_ = [("iterations", C.c_void_p), ("residual", C.c_void_p), ("n_probes", C.c_int),
+                ("probe_nodes", C.c_void_p), ("probe_mean", C.c_void_p), ("probe_std", C.c_void_p),
+                ("full_state", C.c_void_p)]
+
+
+def load_library():
+    """Load libsgw_b200.so; raises if it is missing (no CPU fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    vp, ip, dp = C.c_void_p, C.c_int, C.c_double
+    L.sgw_last_error.restype = C.c_char_p
+    L.sgw_create.argtypes = [C.POINTER(_Problem), C.POINTER(vp)]
+    L.sgw_destroy.argtypes = [vp]
+    L.sgw_sizes.argtypes = [vp, vp]
+    L.sgw_set_stream.argtypes = [vp, vp]
+    L.sgw_apply_block.argtypes = [vp, ip, vp, vp]
+    L.sgw_schur_matvec.argtypes = [vp, vp, vp]
+    L.sgw_apply_nn2.argtypes = [vp, vp, vp]
+    L.sgw_pcg.argtypes = [vp, vp, vp, vp, vp, vp, ip]
+    L.sgw_coarse_operator.argtypes = [vp, vp]
+    L.sgw_run.argtypes = [vp, vp, vp, ip, C.POINTER(_Force), C.POINTER(_History)]
+    L.sgw_init_state.argtypes = [vp, vp, vp, C.POINTER(_Force)]
+    L.sgw_advance.argtypes = [vp, ip, vp]
+    L.sgw_get_state.argtypes = [vp, vp]
+    L.sgw_stats.argtypes = [vp, vp]
+    L.sgw_reset_stats.argtypes = [vp]
+    L.sgw_lognormal_coeff.argtypes = [ip, ip, dp, dp, dp, dp, ip, ip, vp, C.c_longlong, C.POINTER(ip)]
+    L.sgw_triple_products.argtypes = [ip, ip, ip, C.POINTER(ip), C.POINTER(ip), C.POINTER(ip), vp, vp, vp, vp,
+                                      C.c_longlong]
+    L.sgw_nearest_node.argtypes = [ip, ip, dp, dp]
+    _LIB = L
+    return L
+
+
+def _check(rc):
+    if rc != SGW_OK:
+        msg = load_library().sgw_last_error().decode()
+        if rc == SGW_EINVAL:
+            raise SgInvalidArgument(rc, msg)
+        raise SgError(rc, msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ------------------------------------------------------------------ inputs --
+@dataclass
+class TripleTensor:
+    """include/sgwave/pce.hpp:24-40 — entries (i, j, k, value) with j <= k."""
+    n_input: int
+    n_output: int
+    i: np.ndarray
+    j: np.ndarray
+    k: np.ndarray
+    v: np.ndarray
+
+
+def triple_products(n_vars, order_in, order_out) -> TripleTensor:
+    """src/pce.cpp:96-122, with the order_in <= order_out guard lifted."""
+    L = load_library()
+    ni, no, ne = C.c_int(), C.c_int(), C.c_int()
+    _check(L.sgw_triple_products(n_vars, order_in, order_out, C.byref(ni), C.byref(no), C.byref(ne),
+                                 None, None, None, None, 0))
+    i = np.zeros(ne.value, np.int32)
+    j, k, v = np.zeros_like(i), np.zeros_like(i), np.zeros(ne.value)
+    _check(L.sgw_triple_products(n_vars, order_in, order_out, C.byref(ni), C.byref(no), C.byref(ne),
+                                 _p(i), _p(j), _p(k), _p(v), ne.value))
+    return TripleTensor(ni.value, no.value, i, j, k, v)
+
+
+def lognormal_coeff(nx, ny, sigma, bx, by, n_vars, p_in, g0=0.0) -> np.ndarray:
+    """lognormal_pce(kle_exponential(sigma, bx, by, n_vars, mesh, g0), PceBasis(n_vars, p_in))
+    (src/lognormal.cpp:8-40, src/kle.cpp:80-133): n_in x (nx+1)(ny+1) nodal terms."""
+    L = load_library()
+    n_in = C.c_int()
+    _check(L.sgw_lognormal_coeff(nx, ny, sigma, bx, by, g0, n_vars, p_in, None, 0, C.byref(n_in)))
+    out = np.zeros((n_in.value, (nx + 1) * (ny + 1)))
+    _check(L.sgw_lognormal_coeff(nx, ny, sigma, bx, by, g0, n_vars, p_in, _p(out), out.size, C.byref(n_in)))
+    return out
+
+
+def nearest_node(nx, ny, x, y) -> int:
+    return load_library().sgw_nearest_node(nx, ny, x, y)
+
+
+def gaussian_pulse(nx, ny, x0=0.7, y0=0.7, beta=1.0, alpha=0.01):
+    """src/experiments.cpp:14-22"""
+    i = np.tile(np.arange(nx + 1), ny + 1) / nx
+    j = np.repeat(np.arange(ny + 1), nx + 1) / ny
+    return np.array([beta * math.exp(-((a - x0) ** 2 + (b - y0) ** 2) / alpha) for a, b in zip(i, j)])
+
+
+def ricker(t, f0=10.0, t0=0.1, amp=1.0):
+    a = math.pi ** 2 * f0 ** 2 * (t - t0) ** 2
+    return amp * (1.0 - 2.0 * a) * math.exp(-a)
+
+
+@dataclass
+class ForceSpec:
+    """ForceFn (include/sgwave/det_loop.hpp:32): a Ricker point source or a
+    nodal table with one row per time level t_0 .. t_N."""
+    node: int = -1
+    f0: float = 10.0
+    t0: float = 0.1
+    amp: float = 1.0
+    table: np.ndarray | None = None
+
+    def _c(self):
+        if self.table is not None:
+            self._keep = _f64(self.table)
+            return _Force(2, -1, 0.0, 0.0, 0.0, _p(self._keep))
+        if self.node >= 0:
+            return _Force(1, self.node, self.f0, self.t0, self.amp, None)
+        return _Force(0, -1, 0.0, 0.0, 0.0, None)
+
+
+@dataclass
+class NewmarkParams:  # include/sgwave/newmark.hpp:11-19
+    dt: float = 1e-3
+    gamma: float = 0.5
+    zeta: float = 0.25
+
+
+@dataclass
+class SgOptions:  # include/sgwave/sg.hpp:15-21
+    tol: float = 1e-8
+    max_iter: int = 500
+    store_full: bool = False
+    probe_nodes: list = field(default_factory=list)
+    device: int = 0
+
+
+@dataclass
+class SgHistory:  # include/sgwave/sg.hpp:23-31
+    times: np.ndarray
+    iterations: np.ndarray
+    residual: np.ndarray
+    probe_mean: np.ndarray
+    probe_std: np.ndarray
+    full_state: np.ndarray | None
+
+    def mean_iterations(self):
+        return float(self.iterations.mean()) if len(self.iterations) else 0.0
+
+
+class SchurSystem:
+    """View of the device-resident interface system (include/sgwave/dd.hpp:71-96)."""
+
+    def __init__(self, solver):
+        self._s = solver
+
+    @property
+    def n_global(self):
+        return self._s.n_global
+
+    @property
+    def n_corner(self):
+        return self._s.n_corner * self._s.n_terms
+
+    def matvec(self, x):
+        x = _f64(x)
+        y = np.zeros(self._s.n_global)
+        _check(load_library().sgw_schur_matvec(self._s._h, _p(x), _p(y)))
+        return y
+
+    def apply_nn2(self, r):
+        r = _f64(r)
+        z = np.zeros(self._s.n_global)
+        _check(load_library().sgw_apply_nn2(self._s._h, _p(r), _p(z)))
+        return z
+
+    def coarse_operator(self):
+        n = self.n_corner
+        out = np.zeros(n * n)
+        _check(load_library().sgw_coarse_operator(self._s._h, _p(out)))
+        return out.reshape(n, n).T.copy()
+
+
+class SgSolver:
+    """B200 SgSolver (src/sg.cpp).  Setup (interior factorizations, local
+    Schur complements, NN2 data) runs on the GPU in the constructor."""
+
+    def __init__(self, nx, ny, px, py, coeff, tensor, density=1.0, alpha0=0.5445, alpha1=0.0174,
+                 params: NewmarkParams | None = None, options: SgOptions | None = None):
+        L = load_library()
+        self.params = params or NewmarkParams()
+        self.options = options or SgOptions()
+        self.nx, self.ny = nx, ny
+        self._coeff = _f64(coeff)
+        if self._coeff.ndim != 2 or self._coeff.shape[1] != (nx + 1) * (ny + 1):
+            raise SgInvalidArgument(SGW_EINVAL, "coefficient field must be n_in x (nx+1)(ny+1)")
+        ti = np.ascontiguousarray(tensor.i, np.int32)
+        tj = np.ascontiguousarray(tensor.j, np.int32)
+        tk = np.ascontiguousarray(tensor.k, np.int32)
+        tv = _f64(tensor.v)
+        prob = _Problem(nx, ny, px, py, self._coeff.shape[0], _p(self._coeff), int(tensor.n_output), len(tv),
+                        _p(ti), _p(tj), _p(tk), _p(tv), density, alpha0, alpha1, self.params.gamma,
+                        self.params.zeta, self.params.dt, self.options.tol, self.options.max_iter,
+                        self.options.device, 0, 1, None)
+        if self._coeff.shape[0] != tensor.n_input:
+            raise SgInvalidArgument(SGW_EINVAL, "SgSolver: coefficient terms do not match tensor input size")
+        h = C.c_void_p()
+        _check(L.sgw_create(C.byref(prob), C.byref(h)))
+        self._h = h
+        s = np.zeros(8, np.int64)
+        _check(L.sgw_sizes(self._h, _p(s)))
+        (self.n_dofs, self.n_terms, self.n_iface, self.n_corner, self.n_global, self.n_sub, _,
+         self.device_bytes) = (int(v) for v in s)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().sgw_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def schur(self):
+        return SchurSystem(self)
+
+    def uses_direct(self):
+        return False
+
+    def set_stream(self, stream_handle: int):
+        _check(load_library().sgw_set_stream(self._h, C.c_void_p(stream_handle)))
+
+    def _apply(self, op, x):
+        x = _f64(x)
+        y = np.zeros_like(x)
+        _check(load_library().sgw_apply_block(self._h, op, _p(x), _p(y)))
+        return y
+
+    def apply_block_mass(self, x):
+        return self._apply(0, x)
+
+    def apply_block_stiffness(self, x):
+        return self._apply(1, x)
+
+    def apply_block_transient(self, x):
+        return self._apply(2, x)
+
+    def pcg(self, rhs):
+        rhs = _f64(rhs)
+        x = np.zeros(self.n_global)
+        it, conv = C.c_int(), C.c_int()
+        cap = self.options.max_iter + 2
+        hist = np.zeros(cap)
+        _check(load_library().sgw_pcg(self._h, _p(rhs), _p(x), C.byref(it), C.byref(conv), _p(hist), cap))
+        return x, {"iterations": it.value, "converged": bool(conv.value),
+                   "residual_history": hist[hist >= 0].copy()}
+
+    def run(self, u0_nodal, v0_nodal, n_steps, force: ForceSpec | None = None) -> SgHistory:
+        u0, v0 = _f64(u0_nodal), _f64(v0_nodal)
+        probes = np.ascontiguousarray(self.options.probe_nodes, np.int32)
+        its = np.zeros(n_steps, np.int32)
+        res = np.zeros(n_steps)
+        pm = np.zeros((len(probes), n_steps + 1))
+        ps = np.zeros_like(pm)
+        full = np.zeros((n_steps + 1, self.n_terms * self.n_dofs)) if self.options.store_full else None
+        hist = _History(_p(its), _p(res), len(probes), _p(probes), _p(pm), _p(ps), _p(full))
+        f = (force or ForceSpec())._c()
+        _check(load_library().sgw_run(self._h, _p(u0), _p(v0), n_steps, C.byref(f), C.byref(hist)))
+        times = np.cumsum(np.r_[0.0, np.full(n_steps, self.params.dt)])
+        return SgHistory(times, its, res, pm, ps, full)
+
+    # device-resident stepping (benchmarks)
+    def init_state(self, u0_nodal, v0_nodal, force: ForceSpec | None = None):
+        u0, v0 = _f64(u0_nodal), _f64(v0_nodal)
+        f = (force or ForceSpec())._c()
+        _check(load_library().sgw_init_state(self._h, _p(u0), _p(v0), C.byref(f)))
+
+    def advance(self, n_steps):
+        its = np.zeros(max(n_steps, 1), np.int32)
+        _check(load_library().sgw_advance(self._h, n_steps, _p(its)))
+        return its[:n_steps]
+
+    def state(self):
+        u = np.zeros(self.n_terms * self.n_dofs)
+        _check(load_library().sgw_get_state(self._h, _p(u)))
+        return u
+
+    def stats(self):
+        o = np.zeros(10)
+        _check(load_library().sgw_stats(self._h, _p(o)))
+        keys = ["setup_s", "pcg_ms", "step_ms", "iterations", "launches", "steps", "rhs_ms", "rec_ms",
+                "matvecs", "nn2s"]
+        return dict(zip(keys, o.tolist()))
+
+    def reset_stats(self):
+        _check(load_library().sgw_reset_stats(self._h))

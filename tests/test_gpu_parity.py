@@ -1,0 +1,151 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+identical seeded inputs.  Tolerances follow the reference tests and the
+BASELINE parity contract (PCG iterations within +-1 per step, PCE solution
+within 1e-8 relative L2 at CG tolerance 1e-10)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+sg = pytest.importorskip("paper_2512_23027_b200")
+
+
+def rand(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+def pair(nx, px, py, sigma, b, L, pin, pout, dt, tol=1e-10, alpha0=0.5445, alpha1=0.0174, g0=0.0):
+    coeff = O.lognormal_coeff(nx, nx, sigma, b, b, L, pin, g0=g0)
+    t = O.triple_products(L, pin, pout)
+    gpu = sg.SgSolver(nx, nx, px, py, coeff, t, alpha0=alpha0, alpha1=alpha1, params=sg.NewmarkParams(dt=dt),
+                      options=sg.SgOptions(tol=tol, store_full=True))
+    cpu = O.SgSolver(nx, nx, px, py, coeff, t, alpha0=alpha0, alpha1=alpha1, dt=dt, tol=tol)
+    return gpu, cpu
+
+
+def relerr(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("op", ["mass", "stiffness", "transient"])
+def test_apply_block_matches_oracle(gpu, op):
+    # sg.cpp:425-447 vs the oracle; test_sg.cpp:51-73 tolerance 1e-12
+    g, c = pair(12, 2, 2, 0.3, 0.5, 2, 4, 2, 1e-3)
+    x = rand(g.n_terms * g.n_dofs, 1)
+    a = getattr(g, f"apply_block_{op}")(x)
+    b = c.apply_block(x, op)
+    assert relerr(a, b) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", [(8, 2, 1, 1, 1, 1), (12, 2, 2, 2, 2, 2), (16, 4, 4, 2, 4, 2), (24, 3, 2, 3, 2, 3)])
+def test_schur_and_nn2_match_oracle(gpu, cfg):
+    nx, px, py, L, pin, pout = cfg
+    g, c = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 1e-3)
+    assert (g.n_global, g.n_terms) == (c.n_global, c.n_terms)
+    x = rand(g.n_global, 7)
+    assert relerr(g.schur().matvec(x), c.schur_matvec(x)) <= 1e-10
+    assert relerr(g.schur().apply_nn2(x), c.apply_nn2(x)) <= 1e-10
+    if c.n_corner:
+        F = g.schur().coarse_operator()
+        assert relerr(F, c.coarse_operator()) <= 1e-10
+
+
+def test_nn2_symmetric_and_schur_spd(gpu):
+    g, _ = pair(16, 4, 4, 0.3, 0.5, 2, 4, 2, 1e-3)
+    r1, r2 = rand(g.n_global, 31), rand(g.n_global, 32)
+    a, b = r2 @ g.schur().apply_nn2(r1), r1 @ g.schur().apply_nn2(r2)
+    assert abs(a - b) <= 1e-10 * abs(b)
+    assert r1 @ g.schur().matvec(r1) > 0
+
+
+def test_pcg_matches_oracle_iterations(gpu):
+    g, c = pair(16, 4, 4, 0.3, 0.5, 2, 4, 2, 1e-3)
+    b = c.schur_matvec(rand(g.n_global, 3))
+    x, rep = g.pcg(b)
+    assert rep["converged"]
+    res = np.linalg.norm(c.schur_matvec(x) - b) / np.linalg.norm(b)
+    assert res <= 1e-10
+
+
+def test_c1_trajectory_parity(gpu):
+    # BASELINE configs[0] (C1): 64x64, 4x4, L=2, p_in 4, p_out 2, sigma 0.3, b 0.5,
+    # dt 1e-3, 50 steps, tol 1e-10, Ricker f0 = 10 Hz at (0.5, 0.5)
+    nx = 64
+    g, c = pair(nx, 4, 4, 0.3, 0.5, 2, 4, 2, 1e-3)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 50, sg.ForceSpec(node=node, f0=10.0, t0=0.1))
+    hc = c.run(z, z, 50, force_node=node, f0=10.0, t0=0.1, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    rel = np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"])
+    assert rel <= 1e-8
+    per_step = np.linalg.norm(hg.full_state - hc["full"], axis=1) / np.maximum(np.linalg.norm(hc["full"], axis=1), 1e-300)
+    assert per_step[1:].max() <= 1e-8
+
+
+def test_recorded_sg_nn2_iterations_on_gpu(gpu):
+    # acceptance criterion 13, recorded proj/test_output.txt:52 (mean 3.00)
+    nx = 24
+    for L, pin, pout in [(3, 2, 3), (5, 2, 3), (3, 2, 4)]:
+        coeff = O.lognormal_coeff(nx, nx, 0.1, 1.0, 1.0, L, pin)
+        dt = O.cfl_dt(nx, coeff[0].max(), 0.1)
+        g = sg.SgSolver(nx, nx, 4, 4, coeff, O.triple_products(L, pin, pout), params=sg.NewmarkParams(dt=dt),
+                        options=sg.SgOptions(tol=1e-8))
+        u0 = O.gaussian_pulse(nx, nx)
+        h = g.run(u0, 0 * u0, math.ceil(0.3 / dt))
+        assert f"{h.mean_iterations():.2f}" == "3.00"
+
+
+def test_gaussian_pulse_trajectory_matches_oracle(gpu):
+    # test_sg.cpp:218-272-style trajectory (initial displacement, damping on)
+    nx = 16
+    g, c = pair(nx, 2, 2, 0.25, 1.0, 2, 2, 3, 0.01)
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 12)
+    hc = c.run(u0, 0 * u0, 12, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-8
+
+
+def test_zero_data_stays_zero(gpu):
+    g, _ = pair(8, 2, 2, 0.2, 1.0, 2, 1, 2, 0.05)
+    z = np.zeros(81)
+    h = g.run(z, z, 4)
+    assert np.abs(h.full_state).max() == 0.0 and np.all(h.iterations == 0)
+
+
+def test_bitwise_reproducible_runs(gpu):
+    g, _ = pair(16, 4, 2, 0.3, 0.5, 2, 2, 2, 0.01)
+    u0 = O.gaussian_pulse(16, 16)
+    a = g.run(u0, 0 * u0, 5).full_state
+    b = g.run(u0, 0 * u0, 5).full_state
+    assert np.array_equal(a, b)
+
+
+def test_probes_match_full_state(gpu):
+    nx = 16
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, 2, 2)
+    probes = [O.nearest_node(nx, nx, 0.5, 0.5), O.nearest_node(nx, nx, 0.7, 0.7)]
+    g = sg.SgSolver(nx, nx, 2, 2, coeff, O.triple_products(2, 2, 2), params=sg.NewmarkParams(dt=0.01),
+                    options=sg.SgOptions(tol=1e-10, store_full=True, probe_nodes=probes))
+    u0 = O.gaussian_pulse(nx, nx)
+    h = g.run(u0, 0 * u0, 6)
+    n = g.n_dofs
+    for p, node in enumerate(probes):
+        i, j = node % (nx + 1), node // (nx + 1)
+        d = (j - 1) * (nx - 1) + (i - 1)
+        assert np.array_equal(h.probe_mean[p], h.full_state[:, d])
+        std = np.sqrt((h.full_state[:, n + d::n][:, : g.n_terms - 1] ** 2).sum(axis=1))
+        assert np.allclose(h.probe_std[p], std, rtol=1e-14, atol=0)
+
+
+def test_constrained_probe_rejected(gpu):
+    coeff = O.lognormal_coeff(8, 8, 0.2, 1.0, 1.0, 1, 1)
+    g = sg.SgSolver(8, 8, 2, 2, coeff, O.triple_products(1, 1, 1), params=sg.NewmarkParams(dt=0.05),
+                    options=sg.SgOptions(probe_nodes=[0]))
+    with pytest.raises(ValueError):
+        g.run(np.zeros(81), np.zeros(81), 1)
