@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""Benchmark of the per-Newmark-step SG-PCG / NN2 solve (BASELINE.json metric).
+
+Ours:      python bench.py [--gpus N --steps K --warmup W]
+Reference: python bench.py --impl reference ...   (CPU oracle restatement of the
+           reference path on the host cores — the reference itself cannot be
+           built here: Eigen3 + vendored doctest/CLI11/json are absent.)
+
+A "step" is one Newmark step of configs[1] (C2): RHS + interior Dirichlet
+solves + interface PCG with NN2 + recovery + update, on device-resident state.
+`value` = PCG GDOF*iter/s = (P+1) N sum(iterations) / PCG device time / 1e9.
+Prints one JSON line (rank 0).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG GDOF·iter/s and s per Newmark step at (P+1)×N; % of HBM roofline"
+UNIT = "GDOF·iter/s"
+
+CONFIGS = {  # BASELINE.json configs
+    "C1": dict(nx=64, px=4, L=2, p_in=4, p_out=2, sigma=0.3, b=0.5, dt=1e-3),
+    "C2": dict(nx=256, px=8, L=3, p_in=6, p_out=3, sigma=0.3, b=0.5, dt=1e-3),
+    "C3": dict(nx=512, px=16, L=4, p_in=6, p_out=3, sigma=0.4, b=0.3, dt=1e-3),
+}
+ALPHA0, ALPHA1, TOL, F0, T0 = 0.5445, 0.0174, 1e-10, 10.0, 0.1
+
+
+def workload_desc(name, c):
+    nt = math.comb(c["L"] + c["p_out"], c["p_out"])
+    return (f"{name}: {c['nx']}x{c['nx']} P1 grid ({(c['nx'] + 1) ** 2} nodes), {c['px']}x{c['px']} subdomains, "
+            f"KL modes {c['L']}, P+1={nt}, p_in={c['p_in']}, sigma={c['sigma']}, corr.len={c['b']}, dt={c['dt']}, "
+            f"Ricker f0={F0} Hz t0={T0} at (0.5,0.5), Newmark beta=1/4 gamma=1/2, "
+            f"alpha0={ALPHA0} alpha1={ALPHA1}, PCG tol {TOL}, fp64")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        rows = [[x.strip() for x in r] for r in rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def cpu_oracle_run(c, warmup, steps, threads):
+    """Oracle (CPU restatement of the reference path): setup untimed, then
+    `warmup` + `steps` Newmark steps; returns PCG GDOF*iter/s and s/step."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    nx = c["nx"]
+    coeff = O.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
+    tensor = O.triple_products(c["L"], c["p_in"], c["p_out"])
+    t0 = time.perf_counter()
+    s = O.SgSolver(nx, nx, c["px"], c["px"], coeff, tensor, alpha0=ALPHA0, alpha1=ALPHA1, dt=c["dt"], tol=TOL,
+                   threads=threads)
+    setup = time.perf_counter() - t0
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    # warm-up steps then timed steps, one continuous trajectory
+    out = s.run(z, z, warmup + steps, force_node=node, f0=F0, t0=T0) if warmup == 0 else None
+    if out is None:
+        w = s.run(z, z, warmup, force_node=node, f0=F0, t0=T0)
+        t_w, pcg_w, it_w = w["t_run"], w["t_pcg"], w["total_iterations"]
+        out = s.run(z, z, warmup + steps, force_node=node, f0=F0, t0=T0)
+        t_run, t_pcg = out["t_run"] - t_w, out["t_pcg"] - pcg_w
+        iters = out["total_iterations"] - it_w
+    else:
+        t_run, t_pcg, iters = out["t_run"], out["t_pcg"], out["total_iterations"]
+    gdof = s.n_terms * (nx + 1) ** 2
+    return {"value": gdof * iters / t_pcg / 1e9, "s_per_step": t_run / steps, "iterations": iters,
+            "setup_s": setup, "pcg_s": t_pcg, "n_terms": s.n_terms}
+
+
+def run_reference(args, c, name):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    r = cpu_oracle_run(c, args.warmup, args.steps, threads)
+    sample = (f"{name} full problem, setup excluded ({r['setup_s']:.1f} s), {args.warmup} warm-up + "
+              f"{args.steps} timed Newmark steps, {threads} threads (std::thread over subdomains)")
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["s_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic KLE inputs; seeds have no effect on the SG solve)",
+            "config": {"workload": workload_desc(name, c), "GDOF": r["n_terms"] * (c["nx"] + 1) ** 2 / 1e9},
+            "s_per_newmark_step": r["s_per_step"], "pcg_iterations": r["iterations"],
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference C++ needs Eigen3 and vendored doctest/CLI11/json (absent): oracle/ restatement timed"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, c, args.config)
+
+    import torch
+    import paper_2512_23027_b200 as sg
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    nx = c["nx"]
+    coeff = sg.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
+    tensor = sg.triple_products(c["L"], c["p_in"], c["p_out"])
+    node = sg.nearest_node(nx, nx, 0.5, 0.5)
+    t0 = time.perf_counter()
+    solver = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, tensor, alpha0=ALPHA0, alpha1=ALPHA1,
+                         params=sg.NewmarkParams(dt=c["dt"]), options=sg.SgOptions(tol=TOL, device=local))
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream.cuda_stream)
+    gdof = solver.n_terms * (nx + 1) ** 2
+    z = np.zeros((nx + 1) ** 2)
+    force = sg.ForceSpec(node=node, f0=F0, t0=T0)
+    solver.init_state(z, z, force)
+    solver.advance(args.warmup)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    torch.cuda.synchronize()
+    barrier()
+    solver.reset_stats()
+    solver.kernel_profile(True)
+    launches0 = solver.stats()["launches"]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        its = solver.advance(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = solver.stats()
+    kp = solver.kernel_profile(False)
+    launches = int(st["launches"] - launches0)
+    pcg_ms, iters = st["pcg_ms"], int(its.sum())
+    if world > 1:
+        t = torch.tensor([ms, pcg_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        n = torch.tensor([float(iters)], device="cuda")
+        torch.distributed.all_reduce(n)
+        ms, pcg_ms, iters_all = float(t[0]), float(t[1]), int(n[0])
+    else:
+        iters_all = iters
+    value = gdof * iters_all / (pcg_ms / 1e3) / 1e9
+
+    peak, peak_src = measured_peaks()
+    # dominant kernel of the timed region
+    classes = {k: v for k, v in kp.items() if isinstance(v, tuple) and v[1] > 0}
+    dom = max(classes, key=lambda k: classes[k][0])
+    dms, dn, dbytes = classes[dom]
+    achieved = dbytes / (dms / dn / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            traffic = json.load(f).get(args.config, {}).get(dom, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    kernels = {k: {"ms_total": v[0], "launches": v[1], "algorithmic_bytes_per_launch": v[2],
+                   "achieved_GBs": (v[2] / (v[0] / v[1] / 1e3) / 1e9) if v[1] else None}
+               for k, v in classes.items()}
+    b_iter = kp["bytes_per_pcg_iteration"]
+    iter_ms = pcg_ms / max(iters, 1)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic KLE/PCE inputs of the config; seeds have no effect on the SG solve)",
+        "config": {"workload": workload_desc(args.config, c), "GDOF": gdof / 1e9,
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "l2": "inputs larger than L2: S+Q tiles stream ~2.7 GB per PCG iteration (L2 126 MB)"},
+        "s_per_newmark_step": ms / args.steps / 1e3,
+        "pcg_iterations": iters_all, "mean_iterations_per_step": iters / args.steps,
+        "setup_s": setup_s,
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+        "pcg_iteration_roofline": {"bytes_per_iteration": b_iter, "ms_per_iteration": iter_ms,
+                                   "achieved": b_iter / (iter_ms / 1e3) / 1e9,
+                                   "frac": b_iter / (iter_ms / 1e3) / 1e9 / peak},
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e:
+        # end to end through the public C ABI with host buffers: sgw_run with a
+        # nodal force table (one row uploaded per step) and host-side history
+        table = np.zeros((args.steps + 1, (nx + 1) ** 2))
+        tt = 0.0
+        for k in range(args.steps + 1):
+            table[k, node] = sg.ricker(tt, F0, T0)
+            tt += c["dt"]
+        solver.options.probe_nodes = [node]
+        torch.cuda.synchronize()
+        barrier()
+        w0 = time.perf_counter()
+        h = solver.run(z, z, args.steps, sg.ForceSpec(table=table))
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        if world > 1:
+            t = torch.tensor([wall], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            wall = float(t[0])
+        e_iters = int(h.iterations.sum()) * world
+        line["e2e"] = {"value": gdof * e_iters / wall / 1e9, "unit": UNIT,
+                       "h2d_bytes_per_step": 8 * (nx + 1) ** 2 + 2 * 8 * (nx + 1) ** 2 / args.steps,
+                       "d2h_bytes_per_step": 8 * (h.iterations.mean() + 2) + 16,
+                       "wall_s": wall, "note": "sgw_run: u0/v0 + one nodal force row per step H2D; "
+                                               "PCG residual scalars + probe history D2H"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        r = cpu_oracle_run(c, 1, args.cpu_steps, threads)
+        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{args.config} full problem, setup excluded ({r['setup_s']:.0f} s), "
+                                          f"1 warm-up + {args.cpu_steps} timed Newmark steps, PCG time only",
+                                "s_per_newmark_step": r["s_per_step"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -134,6 +134,16 @@ int sgw_get_state(sgw_solver* s, double* u_flat);
 int sgw_stats(sgw_solver* s, double* out);
 int sgw_reset_stats(sgw_solver* s);
 
+/* Per-kernel-class device timing (CUDA events around each launch on the
+ * solver stream).  enable: 1 on / 0 off.  out (optional, 12 doubles): for
+ * classes {S tile-SYMV, Q tile-SYMV, interior sweep, SG-operator apply}:
+ * [total ms, launches, algorithmic bytes per launch]; out[12] = algorithmic
+ * bytes of one PCG iteration (SURVEY 8d B_iter).  out needs 13 doubles.     */
+int sgw_kernel_profile(sgw_solver* s, int enable, double* out);
+/* Average device ms of `reps` back-to-back calls of one operation:
+ * which 0 = Schur matvec, 1 = NN2 apply, 2 = global transient SG operator.  */
+int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out_ms);
+
 /* Input builders (host). */
 int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, double g0,
                         int n_vars, int p_in, double* out, long long out_cap, int* n_in);

@@ -269,7 +269,59 @@ int sgw_stats(sgw_solver* s, double* o) {
 }
 
 int sgw_reset_stats(sgw_solver* s) {
-  return guard([&] { s->g->T = Timers{}; });
+  return guard([&] {
+    s->g->T = Timers{};
+    s->g->KP.reset();
+  });
+}
+
+int sgw_kernel_profile(sgw_solver* s, int enable, double* out) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    g.KP.on = enable != 0;
+    if (out) {
+      const double bytes[K_NCLASS] = {g.bytes_S(), g.bytes_Q(), g.bytes_sweep(), g.bytes_sgop()};
+      for (int c = 0; c < K_NCLASS; ++c) {
+        out[3 * c] = g.KP.ms[c];
+        out[3 * c + 1] = double(g.KP.count[c]);
+        out[3 * c + 2] = bytes[c];
+      }
+      out[12] = g.bytes_iter();
+    }
+  });
+}
+
+int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    if (reps < 1) throw Error(SGW_EINVAL, "reps must be >= 1");
+    DBuf<double> x, y;
+    const size_t len = which == 2 ? g.NSTATE : (size_t)g.NG;
+    x.alloc(len), y.alloc(len);
+    std::vector<double> h(len);
+    for (size_t i = 0; i < len; ++i) h[i] = std::sin(0.001 * double(i) + 0.3);
+    SGW_CUDA(cudaMemcpy(x.p, h.data(), len * sizeof(double), cudaMemcpyHostToDevice));
+    auto once = [&] {
+      if (which == 0) g.schur_matvec(x.p, y.p);
+      else if (which == 1) g.apply_nn2(x.p, y.p);
+      else if (which == 2) g.apply_block(2, x.p, y.p);
+      else throw Error(SGW_EINVAL, "bench_kernel: which must be 0 (matvec), 1 (nn2), 2 (sg-op)");
+    };
+    once();
+    cudaEvent_t a, b;
+    SGW_CUDA(cudaEventCreate(&a));
+    SGW_CUDA(cudaEventCreate(&b));
+    SGW_CUDA(cudaEventRecord(a, g.stream()));
+    for (int r = 0; r < reps; ++r) once();
+    SGW_CUDA(cudaEventRecord(b, g.stream()));
+    SGW_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    g.KP.collect();
+    out[0] = ms / reps;
+  });
 }
 
 int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, double g0, int n_vars, int p_in,

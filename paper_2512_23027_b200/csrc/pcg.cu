@@ -225,9 +225,37 @@ __device__ __forceinline__ double tile_reduce(const double* __restrict__ rowpart
 
 void GpuSolver::symv(TilePack& tp, const double* xloc, double*) {
   if (!tp.n_tiles) return;
+  cudaEvent_t e0;
+  KP.begin(&tp == &Sp ? K_SYMV_S : K_SYMV_Q, st_, &e0);
   symv_tiles_kernel<<<(unsigned)tp.n_tiles, 256, 0, st_>>>(tp.desc.p, tp.tiles.p, tp.d_xoff.p, xloc, tp.rowpart.p,
                                                           tp.colpart.p);
   SGW_LAUNCHED();
+  KP.end(st_);
+}
+
+static double packed_bytes(const std::vector<int>& dims) {
+  double b = 0;
+  for (int a : dims) b += 0.5 * double(a) * (a + 1) * 8.0;
+  return b;
+}
+double GpuSolver::bytes_S() const { return packed_bytes(Sp.dim); }
+double GpuSolver::bytes_Q() const { return packed_bytes(Qp.dim); }
+double GpuSolver::bytes_sweep() const {
+  // forward + backward: every Lsub block (dense) and Linv block (lower) read twice
+  const double BB = double(B) * B;
+  return 2.0 * 8.0 * NS * (G.H * 0.5 * (BB + B) + (G.H - 1) * BB);
+}
+// B_iter = 8 [sum_s (a(a+1)/2 + r(r+1)/2 + 2 r c) + n_C (n_C+1)/2 + 12 (P+1) n_G]
+double GpuSolver::bytes_iter() const {
+  double b = bytes_S() + bytes_Q();
+  for (int s = 0; s < NS; ++s) b += 2.0 * 8.0 * double(NT * nr_[s]) * double(NT * nc_[s]);
+  b += 8.0 * 0.5 * double(NC) * (NC + 1);
+  b += 8.0 * 12.0 * NG;
+  return b;
+}
+double GpuSolver::bytes_sgop() const {
+  // SURVEY 8d minimal stored-operator form: 8 n [3 n_in + 2 (P+1)]
+  return 8.0 * n * (3.0 * NIN + 2.0 * NT);
 }
 
 // ---------------------------------------------------- gather / scatter -----

@@ -99,6 +99,51 @@ struct Timers {
   long long iterations = 0, steps = 0, matvecs = 0, nn2s = 0;
 };
 
+// Per-kernel-class device timing (CUDA events around each launch on the
+// solver's stream), enabled for benchmarks only.
+enum KClass { K_SYMV_S = 0, K_SYMV_Q, K_SWEEP, K_SGOP, K_NCLASS };
+struct KProf {
+  bool on = false;
+  double ms[K_NCLASS] = {0};
+  long long count[K_NCLASS] = {0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t get() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+  void begin(int cls, cudaStream_t st, cudaEvent_t* a) {
+    if (!on) return;
+    *a = get();
+    cudaEventRecord(*a, st);
+    pending.push_back({cls, {*a, nullptr}});
+  }
+  void end(cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t b = get();
+    cudaEventRecord(b, st);
+    pending.back().second.second = b;
+  }
+  void collect() {  // after a stream synchronize
+    for (auto& p : pending) {
+      float t = 0;
+      cudaEventElapsedTime(&t, p.second.first, p.second.second);
+      ms[p.first] += t;
+      ++count[p.first];
+    }
+    pending.clear();
+    next = 0;
+  }
+  void reset() {
+    for (int i = 0; i < K_NCLASS; ++i) ms[i] = 0, count[i] = 0;
+  }
+};
+
 class GpuSolver {
  public:
   GpuSolver(Problem p);
@@ -124,7 +169,14 @@ class GpuSolver {
   size_t NSTATE = 0;
   double setup_s = 0;
   Timers T;
+  KProf KP;
   long long device_bytes() const { return DBuf<double>::g_bytes; }
+  // algorithmic bytes: unique symmetric entries of all S_s / Q_s
+  double bytes_S() const;
+  double bytes_Q() const;
+  double bytes_sweep() const;  // one forward+backward interior solve
+  double bytes_sgop() const;   // one global transient SG-operator apply
+  double bytes_iter() const;   // one PCG iteration (SURVEY 8d B_iter)
 
   // state
   DBuf<double> u, v, a, um, uc, unext;

@@ -83,9 +83,12 @@ void GpuSolver::apply_block(int op, const double* x, double* y) {
   const double cm = op == 0 ? 1.0 : op == 1 ? 0.0 : P.mass_scale;
   const double ck = op == 0 ? 0.0 : op == 1 ? 1.0 : P.stiff_scale;
   const long long total = (long long)NSTATE;
+  cudaEvent_t e0;
+  KP.begin(K_SGOP, st_, &e0);
   sg_apply_global_kernel<<<std::min(cdiv(total, 256), 8 * kNumSMs * 16), 256, 0, st_>>>(
       Kg.p, Mg.p, n, P.nx - 1, P.ny - 1, NT, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, x, y, cm, ck);
   SGW_LAUNCHED();
+  KP.end(st_);
 }
 
 // -------------------------------------------------------- local operators --
@@ -245,6 +248,8 @@ void GpuSolver::sweep(double* x) {
   const long long BB = (long long)B * B, sI = (long long)H * B;
   double* t = fI.p;  // scratch (ns x H x B)
   const dim3 gn(cdiv(B, 32), ns), gt(cdiv(B, 8), ns);
+  cudaEvent_t e0;
+  KP.begin(K_SWEEP, st_, &e0);
   // forward: x_k <- Linv_kk (x_k - Lsub_{k-1} x_{k-1})
   for (int k = 0; k < H; ++k) {
     gemv_n_sub_kernel<<<gn, 256, 0, st_>>>(k ? Lsub.p + (k - 1) * BB : nullptr, (long long)(H - 1) * BB,
@@ -263,6 +268,7 @@ void GpuSolver::sweep(double* x) {
                                            x + k * (long long)B, sI, B, 1, 0);
     SGW_LAUNCHED();
   }
+  KP.end(st_);
 }
 
 // --------------------------------------------------------------- Newmark ---
@@ -492,6 +498,7 @@ int GpuSolver::step(int* iters_out) {
   record_probes(step_index);
   cudaEventRecord(ev_[5], st_);
   SGW_CUDA(cudaEventSynchronize(ev_[5]));
+  KP.collect();
   float ms_rhs = 0, ms_rec = 0, ms_all = 0;
   cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);
   cudaEventElapsedTime(&ms_rec, ev_[4], ev_[5]);

@@ -87,6 +87,8 @@ def load_library():
     L.sgw_get_state.argtypes = [vp, vp]
     L.sgw_stats.argtypes = [vp, vp]
     L.sgw_reset_stats.argtypes = [vp]
+    L.sgw_kernel_profile.argtypes = [vp, ip, vp]
+    L.sgw_bench_kernel.argtypes = [vp, ip, ip, vp]
     L.sgw_lognormal_coeff.argtypes = [ip, ip, dp, dp, dp, dp, ip, ip, vp, C.c_longlong, C.POINTER(ip)]
     L.sgw_triple_products.argtypes = [ip, ip, ip, C.POINTER(ip), C.POINTER(ip), C.POINTER(ip), vp, vp, vp, vp,
                                       C.c_longlong]
@@ -355,3 +357,19 @@ class SgSolver:
 
     def reset_stats(self):
         _check(load_library().sgw_reset_stats(self._h))
+
+    KERNEL_CLASSES = ("symv_S", "symv_Q", "interior_sweep", "sg_operator")
+
+    def kernel_profile(self, enable=True):
+        """Per-kernel-class device timings: {class: (total_ms, launches, algorithmic bytes/launch)}."""
+        o = np.zeros(13)
+        _check(load_library().sgw_kernel_profile(self._h, int(enable), _p(o)))
+        out = {c: (o[3 * i], int(o[3 * i + 1]), o[3 * i + 2]) for i, c in enumerate(self.KERNEL_CLASSES)}
+        out["bytes_per_pcg_iteration"] = o[12]
+        return out
+
+    def bench_kernel(self, which, reps=20):
+        """Average device ms of one Schur matvec (0), NN2 apply (1) or SG-operator apply (2)."""
+        o = np.zeros(1)
+        _check(load_library().sgw_bench_kernel(self._h, which, reps, _p(o)))
+        return float(o[0])
