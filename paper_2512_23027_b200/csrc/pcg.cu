@@ -240,11 +240,6 @@ static double packed_bytes(const std::vector<int>& dims) {
 }
 double GpuSolver::bytes_S() const { return packed_bytes(Sp.dim); }
 double GpuSolver::bytes_Q() const { return packed_bytes(Qp.dim); }
-double GpuSolver::bytes_sweep() const {
-  // forward + backward: every Lsub block (dense) and Linv block (lower) read twice
-  const double BB = double(B) * B;
-  return 2.0 * 8.0 * NS * (G.H * 0.5 * (BB + B) + (G.H - 1) * BB);
-}
 // B_iter = 8 [sum_s (a(a+1)/2 + r(r+1)/2 + 2 r c) + n_C (n_C+1)/2 + 12 (P+1) n_G]
 double GpuSolver::bytes_iter() const {
   double b = bytes_S() + bytes_Q();

@@ -370,7 +370,10 @@ GpuSolver::GpuSolver(Problem p) : P(std::move(p)) {
   setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+void destroy_sweep_layout(SweepLayout* p);
+
 GpuSolver::~GpuSolver() {
+  destroy_sweep_layout(sweep_layout_);
   if (blas_) cublasDestroy(blas_);
   if (sol_) cusolverDnDestroy(sol_);
   for (auto& e : ev_) cudaEventDestroy(e);
@@ -516,6 +519,8 @@ void GpuSolver::setup_interior_and_schur() {
       SGW_BLAS(cublasDtrsm(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B, B,
                            &one, D.p + (size_t(s) * H + k) * BB, B, Linv.p + (size_t(s) * H + k) * BB, B));
   SGW_CUDA(cudaStreamSynchronize(st_));
+  D.reset();
+  build_compact_factor();
 }
 
 // ------------------------------------------------------------ NN2 data -----

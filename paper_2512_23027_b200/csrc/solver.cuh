@@ -25,6 +25,8 @@
 
 namespace sgw {
 
+struct SweepLayout;
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -241,7 +243,14 @@ class GpuSolver {
   int B = 0, amax_ = 0;
   DBuf<double> Sdense_;  // setup only
   DBuf<int> iface_lid_;  // flat (ip_off): local interface p -> local node id
-  DBuf<double> Linv, Lsub;
+  DBuf<double> Linv, Lsub;  // dense setup copies (freed after compaction)
+  DBuf<double> Fcomp;       // compact interior factor (sweep.cu)
+  DBuf<long long> sw_off_inv, sw_off_sub;
+  DBuf<int> sw_c0, sw_cuts, sw_ncut;
+  int sweep_cs_ = 1;
+  SweepLayout* sweep_layout_ = nullptr;
+  void build_compact_factor();
+  size_t sweep_smem_bytes() const;
   // work vectors
   DBuf<double> li_x, li_y, r_x, r_t, c_f, c_d, dcoarse, ucoarse;
   DBuf<double> vb, vx, vr, vz, vp, vq, vrt;

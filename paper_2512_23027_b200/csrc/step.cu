@@ -243,34 +243,6 @@ __global__ void gemv_t_sub_kernel(const double* __restrict__ A, long long sA, co
   }
 }
 
-void GpuSolver::sweep(double* x) {
-  const int H = G.H, ns = NS;
-  const long long BB = (long long)B * B, sI = (long long)H * B;
-  double* t = fI.p;  // scratch (ns x H x B)
-  const dim3 gn(cdiv(B, 32), ns), gt(cdiv(B, 8), ns);
-  cudaEvent_t e0;
-  KP.begin(K_SWEEP, st_, &e0);
-  // forward: x_k <- Linv_kk (x_k - Lsub_{k-1} x_{k-1})
-  for (int k = 0; k < H; ++k) {
-    gemv_n_sub_kernel<<<gn, 256, 0, st_>>>(k ? Lsub.p + (k - 1) * BB : nullptr, (long long)(H - 1) * BB,
-                                           x + (k - 1) * (long long)B, sI, x + k * (long long)B, sI, t, B, B, 0);
-    SGW_LAUNCHED();
-    gemv_n_sub_kernel<<<gn, 256, 0, st_>>>(Linv.p + k * BB, (long long)H * BB, t, B, nullptr, 0,
-                                           x + k * (long long)B, sI, B, 1);
-    SGW_LAUNCHED();
-  }
-  // backward: x_k <- Linv_kk^T (x_k - Lsub_k^T x_{k+1})
-  for (int k = H - 1; k >= 0; --k) {
-    gemv_t_sub_kernel<<<gt, 256, 0, st_>>>(k < H - 1 ? Lsub.p + k * BB : nullptr, (long long)(H - 1) * BB,
-                                           x + (k + 1) * (long long)B, sI, x + k * (long long)B, sI, t, B, B, 0, 1);
-    SGW_LAUNCHED();
-    gemv_t_sub_kernel<<<gt, 256, 0, st_>>>(Linv.p + k * BB, (long long)H * BB, t, B, nullptr, 0,
-                                           x + k * (long long)B, sI, B, 1, 0);
-    SGW_LAUNCHED();
-  }
-  KP.end(st_);
-}
-
 // --------------------------------------------------------------- Newmark ---
 __global__ void predictor_kernel(const double* __restrict__ u, const double* __restrict__ v,
                                  const double* __restrict__ a, double* __restrict__ um, double* __restrict__ uc,

@@ -111,6 +111,20 @@ def test_gaussian_pulse_trajectory_matches_oracle(gpu):
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-8
 
 
+@pytest.mark.parametrize("cs", ["1", "2", "4", "8"])
+def test_interior_sweep_every_cluster_size(gpu, monkeypatch, cs):
+    # the batched Dirichlet solve (one thread-block cluster of CS CTAs per
+    # subdomain) must give the oracle trajectory for every cluster size
+    monkeypatch.setenv("SGW_SWEEP_CS", cs)
+    nx = 24
+    g, c = pair(nx, 3, 2, 0.3, 0.5, 2, 4, 2, 2e-3)
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 6)
+    hc = c.run(u0, 0 * u0, 6, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
 def test_zero_data_stays_zero(gpu):
     g, _ = pair(8, 2, 2, 0.2, 1.0, 2, 1, 2, 0.05)
     z = np.zeros(81)
