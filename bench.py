@@ -263,6 +263,7 @@ def main():
                                    "achieved": b_iter / (iter_ms / 1e3) / 1e9,
                                    "frac": b_iter / (iter_ms / 1e3) / 1e9 / peak},
         "kernels": kernels,
+        "pcg_phases_ms_per_iteration": {k: v / max(iters, 1) for k, v in kp["pcg_phases_ms"].items()},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

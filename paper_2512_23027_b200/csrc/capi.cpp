@@ -272,6 +272,7 @@ int sgw_reset_stats(sgw_solver* s) {
   return guard([&] {
     s->g->T = Timers{};
     s->g->KP.reset();
+    SGW_CUDA(cudaMemset(s->g->tphase_.p, 0, 8 * sizeof(double)));
   });
 }
 
@@ -287,6 +288,9 @@ int sgw_kernel_profile(sgw_solver* s, int enable, double* out) {
         out[3 * c + 2] = bytes[c];
       }
       out[12] = g.bytes_iter();
+      double tp[8] = {0};
+      SGW_CUDA(cudaMemcpy(tp, g.tphase_.p, sizeof(tp), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < 8; ++i) out[13 + i] = tp[i] * 1e-6;  // ms per phase, persistent PCG
     }
   });
 }

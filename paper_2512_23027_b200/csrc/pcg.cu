@@ -6,6 +6,7 @@
 #include <cmath>
 
 #include "solver.cuh"
+#include "tiles.cuh"
 
 namespace sgw {
 
@@ -102,13 +103,18 @@ void TilePack::plan(const std::vector<int>& dims) {
   tile_base[0] = 0;
   xoff[0] = 0;
   std::vector<int4> h;
+  std::vector<int2> ht;
   for (int s = 0; s < nmat; ++s) {
     ntile[s] = cdiv(dims[s], kTile);
     tile_base[s + 1] = tile_base[s] + (long long)ntile[s] * (ntile[s] + 1) / 2;
     xoff[s + 1] = xoff[s] + (long long)kTile * ntile[s];
     for (int I = 0; I < ntile[s]; ++I)
-      for (int J = 0; J <= I; ++J) h.push_back(make_int4(s, I, J, 0));
+      for (int J = 0; J <= I; ++J) {
+        h.push_back(make_int4(s, I, J, 0));
+        ht.push_back(make_int2(int(xoff[s] + (long long)I * kTile), int(xoff[s] + (long long)J * kTile)));
+      }
   }
+  tx.upload(ht);
   n_tiles = tile_base[nmat];
   xlen = xoff[nmat];
   desc.upload(h);
@@ -144,12 +150,7 @@ void pack_tiles_range(TilePack& tp, int s, const double* src, int ld, cudaStream
   SGW_LAUNCHED();
 }
 
-// ------------------------------------------------------------ tile SYMV ----
-// One CTA (8 warps) per 64x64 lower tile T_IJ of matrix s:
-//   rowpart[t] = T_IJ x_J            (partial of y_I)
-//   colpart[t] = T_IJ^T x_I  (I != J) (partial of y_J)
-// Warp w streams rows 8w..8w+7 with 128-bit loads (a warp reads one full
-// 512-byte tile row per load); row sums use a butterfly multi-row reduction.
+// One CTA (8 warps) per 64x64 lower tile (tiles.cuh): row / column partials.
 __global__ void __launch_bounds__(256) symv_tiles_kernel(const int4* __restrict__ desc,
                                                          const double* __restrict__ tiles,
                                                          const long long* __restrict__ xoff,
@@ -159,69 +160,11 @@ __global__ void __launch_bounds__(256) symv_tiles_kernel(const int4* __restrict_
   __shared__ double csum[8][kTile];
   const long long t = blockIdx.x;
   const int4 d = desc[t];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const double2* T2 = reinterpret_cast<const double2*>(tiles + t * (kTile * kTile));
-  double2 v[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = __ldcs(T2 + (w * 8 + q) * (kTile / 2) + lane);
   const double* xb = x + xoff[d.x];
-  const double2 xj = reinterpret_cast<const double2*>(xb + d.z * kTile)[lane];
-  const double* xi = xb + d.y * kTile + w * 8;
-  double rs[8], c0 = 0.0, c1 = 0.0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    rs[q] = v[q].x * xj.x + v[q].y * xj.y;
-    const double xv = xi[q];
-    c0 += v[q].x * xv;
-    c1 += v[q].y * xv;
-  }
-  // butterfly: 8 row sums over 32 lanes -> lane holds row 4*b4 + 2*b3 + b2
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool up = lane & 16;
-    const double send = up ? rs[i] : rs[i + 4], keep = up ? rs[i + 4] : rs[i];
-    rs[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const bool up = lane & 8;
-    const double send = up ? rs[i] : rs[i + 2], keep = up ? rs[i + 2] : rs[i];
-    rs[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  {
-    const bool up = lane & 4;
-    const double send = up ? rs[0] : rs[1], keep = up ? rs[1] : rs[0];
-    rs[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 2);
-  rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 1);
-  if ((lane & 3) == 0) {
-    const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    rowpart[t * kTile + w * 8 + row] = rs[0];
-  }
-  if (d.y != d.z) {
-    csum[w][2 * lane] = c0;
-    csum[w][2 * lane + 1] = c1;
-    __syncthreads();
-    if (threadIdx.x < kTile) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s += csum[k][threadIdx.x];
-      colpart[t * kTile + threadIdx.x] = s;
-    }
-  }
+  tile_symv(tiles + t * (kTile * kTile), xb + d.y * kTile, xb + d.z * kTile, d.y == d.z, rowpart + t * kTile,
+            colpart + t * kTile, csum);
 }
 
-// y_s[i] from the tile partials of matrix s, fixed order.
-__device__ __forceinline__ double tile_reduce(const double* __restrict__ rowpart, const double* __restrict__ colpart,
-                                              long long base, int nt, int i) {
-  const int I = i / kTile, r = i % kTile;
-  const long long rowb = base + (long long)I * (I + 1) / 2;
-  double s = 0.0;
-  for (int J = 0; J <= I; ++J) s += rowpart[(rowb + J) * kTile + r];
-  for (int K = I + 1; K < nt; ++K) s += colpart[(base + (long long)K * (K + 1) / 2 + I) * kTile + r];
-  return s;
-}
 
 void GpuSolver::symv(TilePack& tp, const double* xloc, double*) {
   if (!tp.n_tiles) return;
@@ -467,6 +410,7 @@ double GpuSolver::dot_host(const double* a, const double* b, long long len) {
 // src/pcg.cpp:7-50: x0 = 0; stop on the recurrence residual, confirm with the
 // true residual, restart from it (without resetting p) if the check fails.
 int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
+  if (use_fused_) return pcg_fused(b, x, converged, hist);
   cudaEventRecord(ev_[0], st_);
   const long long N = NG;
   const int grid = red_grid(N);

@@ -366,6 +366,7 @@ GpuSolver::GpuSolver(Problem p) : P(std::move(p)) {
   fI.alloc(nI), yI.alloc(nI), wI.alloc(nI);
   scal.alloc(16), scal.zero(st_);
   dpart.alloc(1024), dcount.alloc(4), dcount.zero(st_);
+  setup_fused_pcg();
   SGW_CUDA(cudaStreamSynchronize(st_));
   setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

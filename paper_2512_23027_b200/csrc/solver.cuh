@@ -73,6 +73,7 @@ struct TilePack {
   std::vector<long long> xoff;       // padded local-vector offset (64 * sum ntile)
   long long n_tiles = 0, xlen = 0;
   DBuf<int4> desc;  // per tile: {matrix, I, J, unused}
+  DBuf<int2> tx;    // per tile: local-vector offsets of the I and J segments
   DBuf<double> tiles, rowpart, colpart;
   DBuf<long long> d_tile_base, d_xoff;
   DBuf<int> d_ntile, d_dim;
@@ -251,6 +252,16 @@ class GpuSolver {
   SweepLayout* sweep_layout_ = nullptr;
   void build_compact_factor();
   size_t sweep_smem_bytes() const;
+  // persistent cooperative PCG (pcg_fused.cu)
+  void setup_fused_pcg();
+  int pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist);
+  DBuf<int> smap_, fused_out_;
+  DBuf<double> fused_part_, fused_hist_, li_z_, li_p_, li_xx_, ucl_, wr_;
+ public:
+  DBuf<double> tphase_;  // per-phase ns of the persistent PCG kernel (profiling)
+ private:
+  int fused_grid_ = 0;
+  bool use_fused_ = true;
   // work vectors
   DBuf<double> li_x, li_y, r_x, r_t, c_f, c_d, dcoarse, ucoarse;
   DBuf<double> vb, vx, vr, vz, vp, vq, vrt;

@@ -1,0 +1,81 @@
+// Device pieces of the packed-symmetric 64x64-tile SYMV shared by the
+// standalone kernels (pcg.cu) and the persistent PCG kernel (pcg_fused.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace sgw {
+
+// One 64x64 lower tile T_IJ (row-major, diagonal tiles stored full) times the
+// 64-vectors xI / xJ (shared memory), by 256 threads (8 warps x 8 rows):
+//   rowpart = T_IJ xJ ;  colpart = T_IJ^T xI (I != J).
+// Warp w streams rows 8w..8w+7 with 128-bit loads (one 512-byte row per warp
+// load); the 8 row sums use a butterfly multi-row reduction over the lanes.
+// csum: __shared__ double[8][64] scratch.
+__device__ __forceinline__ void tile_symv(const double* __restrict__ T, const double* xI, const double* xJ,
+                                          bool diag, double* __restrict__ rowpart, double* __restrict__ colpart,
+                                          double (*csum)[kTile]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double2* T2 = reinterpret_cast<const double2*>(T);
+  double2 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __ldcs(T2 + (w * 8 + q) * (kTile / 2) + lane);
+  const double2 xj = reinterpret_cast<const double2*>(xJ)[lane];
+  const double* xi = xI + w * 8;
+  double rs[8], c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    rs[q] = v[q].x * xj.x + v[q].y * xj.y;
+    const double xv = xi[q];
+    c0 += v[q].x * xv;
+    c1 += v[q].y * xv;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 16;
+    const double send = up ? rs[i] : rs[i + 4], keep = up ? rs[i + 4] : rs[i];
+    rs[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 8;
+    const double send = up ? rs[i] : rs[i + 2], keep = up ? rs[i + 2] : rs[i];
+    rs[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool up = lane & 4;
+    const double send = up ? rs[0] : rs[1], keep = up ? rs[1] : rs[0];
+    rs[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 2);
+  rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 1);
+  if ((lane & 3) == 0) {
+    const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    rowpart[w * 8 + row] = rs[0];
+  }
+  if (!diag) {
+    csum[w][2 * lane] = c0;
+    csum[w][2 * lane + 1] = c1;
+    __syncthreads();
+    if (threadIdx.x < kTile) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += csum[k][threadIdx.x];
+      colpart[threadIdx.x] = s;
+    }
+  }
+}
+
+// y_s[i] of matrix s from the tile partials, fixed order: row partials of
+// tiles (I, 0..I), then column partials of tiles (I+1..nt-1, I).
+__device__ __forceinline__ double tile_reduce(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                                              long long base, int nt, int i) {
+  const int I = i / kTile, r = i % kTile;
+  const long long rowb = base + (long long)I * (I + 1) / 2;
+  double s = 0.0;
+  for (int J = 0; J <= I; ++J) s += rowpart[(rowb + J) * kTile + r];
+  for (int K = I + 1; K < nt; ++K) s += colpart[(base + (long long)K * (K + 1) / 2 + I) * kTile + r];
+  return s;
+}
+
+}  // namespace sgw

@@ -71,6 +71,25 @@ def test_pcg_matches_oracle_iterations(gpu):
     assert res <= 1e-10
 
 
+@pytest.mark.parametrize("mode", ["fused", "host"])
+def test_pcg_drivers_agree_with_oracle(gpu, monkeypatch, mode):
+    # persistent cooperative PCG kernel (default) and the host-driven loop
+    if mode == "host":
+        monkeypatch.setenv("SGW_PCG", "host")
+    nx = 32
+    g, c = pair(nx, 4, 2, 0.3, 0.5, 2, 4, 2, 1e-3)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 30, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 30, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+    b = c.schur_matvec(rand(g.n_global, 9))
+    x, rep = g.pcg(b)
+    assert rep["converged"] and len(rep["residual_history"]) == rep["iterations"] + 1
+    assert np.linalg.norm(c.schur_matvec(x) - b) / np.linalg.norm(b) <= 1e-10
+
+
 def test_c1_trajectory_parity(gpu):
     # BASELINE configs[0] (C1): 64x64, 4x4, L=2, p_in 4, p_out 2, sigma 0.3, b 0.5,
     # dt 1e-3, 50 steps, tol 1e-10, Ricker f0 = 10 Hz at (0.5, 0.5)
