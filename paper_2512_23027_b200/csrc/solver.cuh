@@ -246,8 +246,7 @@ class GpuSolver {
   DBuf<int> iface_lid_;  // flat (ip_off): local interface p -> local node id
   DBuf<double> Linv, Lsub;  // dense setup copies (freed after compaction)
   DBuf<double> Fcomp;       // compact interior factor (sweep.cu)
-  DBuf<long long> sw_off_inv, sw_off_sub;
-  DBuf<int> sw_c0, sw_cuts, sw_ncut;
+  DBuf<int> sw_off, sw_cs, sw_cuts, sw_ncut;
   int sweep_cs_ = 1;
   SweepLayout* sweep_layout_ = nullptr;
   void build_compact_factor();
