@@ -244,6 +244,12 @@ def main():
     kernels = {k: {"ms_total": v[0], "launches": v[1], "algorithmic_bytes_per_launch": v[2],
                    "achieved_GBs": (v[2] / (v[0] / v[1] / 1e3) / 1e9) if v[1] else None}
                for k, v in classes.items()}
+    # standalone fused SG-operator apply (apply_block_transient, K11), outside the timed region
+    sgop_ms = solver.bench_kernel(2, reps=20)
+    sgop_bytes = kp["sg_operator"][2]
+    kernels["sg_operator_standalone"] = {"ms_per_launch": sgop_ms, "algorithmic_bytes_per_launch": sgop_bytes,
+                                         "achieved_GBs": sgop_bytes / (sgop_ms / 1e3) / 1e9,
+                                         "frac_of_peak": sgop_bytes / (sgop_ms / 1e3) / 1e9 / peak}
     b_iter = kp["bytes_per_pcg_iteration"]
     iter_ms = pcg_ms / max(iters, 1)
     line = {
