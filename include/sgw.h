@@ -68,8 +68,14 @@ typedef struct sgw_problem {
   double tol;             /* SgOptions::tol (sg.hpp:16)                         */
   int max_iter;           /* SgOptions::max_iter                               */
   int device;             /* CUDA device ordinal                                */
-  /* multi-GPU sharding (one process per GPU); world_size 1 = single GPU.
-   * nccl_id: 128-byte ncclUniqueId from rank 0, broadcast by the caller.  */
+  /* Multi-GPU sharding (one process per GPU); world_size 1 = single GPU.
+   * Rank r owns subdomains [n_sub r / W, n_sub (r+1) / W) (row-major ids);
+   * interface vectors are replicated and every subdomain sum becomes a local
+   * partial sum + ncclAllReduce.  Every entry point is collective: all ranks
+   * call it with the same arguments.  Results (state, probes, PCG output)
+   * are identical on all ranks.
+   * nccl_id: 128-byte ncclUniqueId from sgw_nccl_unique_id on rank 0,
+   * broadcast by the caller (e.g. torch.distributed).                      */
   int rank, world_size;
   const void* nccl_id;
 } sgw_problem;
@@ -154,6 +160,14 @@ int sgw_nearest_node(int nx, int ny, double x, double y);
 
 /* NCCL unique id for multi-GPU runs (128 bytes), generated on rank 0. */
 int sgw_nccl_unique_id(void* out128);
+
+/* In-process sharding on ONE device (tests): world_size solvers, each driven
+ * by its own host thread, exchange through a host-synchronised group
+ * instead of NCCL.  Same ownership and results as the NCCL path.           */
+int sgw_local_group_new(int world_size, void** group);
+int sgw_local_group_free(void* group);
+int sgw_create_local_group(const sgw_problem* problem, int world_size, int rank, void* group,
+                           sgw_solver** out);
 
 #ifdef __cplusplus
 }

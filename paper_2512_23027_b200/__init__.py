@@ -7,8 +7,10 @@ compiled libsgw_b200.so and every compute call runs on the GPU.
 """
 from .sgwave import (  # noqa: F401
     ForceSpec,
+    LocalGroup,
     NewmarkParams,
     SgError,
+    SgInvalidArgument,
     SgHistory,
     SgOptions,
     SgSolver,
@@ -17,7 +19,9 @@ from .sgwave import (  # noqa: F401
     lib_path,
     load_library,
     lognormal_coeff,
+    nccl_unique_id,
     nearest_node,
     ricker,
+    shard_plan,
     triple_products,
 )

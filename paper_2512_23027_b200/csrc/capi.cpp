@@ -68,9 +68,9 @@ extern "C" {
 const char* sgw_last_error(void) { return g_err.c_str(); }
 int sgw_version(void) { return 1; }
 
-int sgw_create(const sgw_problem* p, sgw_solver** out) {
-  return guard([&] {
-    if (!p || !out) throw Error(SGW_EINVAL, "null argument");
+namespace {
+Problem problem_from(const sgw_problem* p) {
+    if (!p) throw Error(SGW_EINVAL, "null argument");
     if (!p->coeff || p->n_input < 1) throw Error(SGW_EINVAL, "SgSolver: empty coefficient field");
     Problem P;
     P.nx = p->nx, P.ny = p->ny, P.px = p->px, P.py = p->py;
@@ -89,11 +89,50 @@ int sgw_create(const sgw_problem* p, sgw_solver** out) {
     P.density = p->density, P.alpha0 = p->alpha0, P.alpha1 = p->alpha1;
     P.gamma = p->gamma, P.zeta = p->zeta, P.dt = p->dt, P.tol = p->tol, P.max_iter = p->max_iter;
     P.device = p->device, P.rank = p->rank, P.world = p->world_size < 1 ? 1 : p->world_size;
-    if (P.world != 1) throw Error(SGW_EINVAL, "multi-GPU sharding: use one solver per rank via sgw_create_sharded");
+    if (P.rank < 0 || P.rank >= P.world) throw Error(SGW_EINVAL, "rank out of range");
+    if (P.world > P.px * P.py) throw Error(SGW_EINVAL, "more ranks than subdomains");
+    return P;
+}
+}  // namespace
+
+int sgw_create(const sgw_problem* p, sgw_solver** out) {
+  return guard([&] {
+    if (!out) throw Error(SGW_EINVAL, "null argument");
+    Problem P = problem_from(p);
+    std::unique_ptr<Comm> comm;
+    if (P.world > 1) {
+      if (!p->nccl_id) throw Error(SGW_EINVAL, "world_size > 1 needs the NCCL unique id of rank 0");
+      comm = make_nccl_comm(p->nccl_id, P.rank, P.world, P.device);
+    }
     auto s = std::make_unique<sgw_solver>();
-    s->g = std::make_unique<GpuSolver>(std::move(P));
+    s->g = std::make_unique<GpuSolver>(std::move(P), std::move(comm));
     *out = s.release();
   });
+}
+
+int sgw_create_local_group(const sgw_problem* p, int world_size, int rank, void* group, sgw_solver** out) {
+  return guard([&] {
+    if (!out || !group) throw Error(SGW_EINVAL, "null argument");
+    auto* g = static_cast<std::shared_ptr<ThreadGroup>*>(group);
+    Problem P = problem_from(p);
+    P.rank = rank, P.world = world_size;
+    if (rank < 0 || rank >= world_size || world_size > P.px * P.py)
+      throw Error(SGW_EINVAL, "rank / world_size out of range");
+    auto s = std::make_unique<sgw_solver>();
+    s->g = std::make_unique<GpuSolver>(std::move(P), make_thread_comm(*g, rank));
+    *out = s.release();
+  });
+}
+
+int sgw_local_group_new(int world_size, void** group) {
+  return guard([&] {
+    if (!group || world_size < 1) throw Error(SGW_EINVAL, "bad argument");
+    *group = new std::shared_ptr<ThreadGroup>(make_thread_group(world_size));
+  });
+}
+
+int sgw_local_group_free(void* group) {
+  return guard([&] { delete static_cast<std::shared_ptr<ThreadGroup>*>(group); });
 }
 
 int sgw_destroy(sgw_solver* s) {
@@ -108,7 +147,7 @@ int sgw_sizes(sgw_solver* s, long long* o) {
     o[2] = g.G.n_iface;
     o[3] = g.G.n_corner;
     o[4] = g.NG;
-    o[5] = g.NS;
+    o[5] = g.G.ns_total;
     o[6] = 0;
     o[7] = g.device_bytes();
   });
@@ -200,7 +239,13 @@ int sgw_advance(sgw_solver* s, int n_steps, int* iterations) {
 }
 
 int sgw_get_state(sgw_solver* s, double* u_flat) {
-  return guard([&] { d2h(u_flat, s->g->u.p, s->g->NSTATE, s->g->stream()); });
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    DBuf<double> full;
+    full.alloc(g.NSTATE);
+    g.gather_state(full.p);
+    d2h(u_flat, full.p, g.NSTATE, g.stream());
+  });
 }
 
 int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, const sgw_force* force,
@@ -222,6 +267,9 @@ int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, cons
     g.probe_cap = n_steps + 1;
     if (np) {
       g.d_probe_dofs.upload(g.probe_dofs);
+      std::vector<int> own(np);
+      for (int q = 0; q < np; ++q) own[q] = g.G.owner_of_dof(g.probe_dofs[q]) == g.rank();
+      g.d_probe_own.upload(own);
       g.probe_hist.alloc((size_t)(n_steps + 1) * np * 2);
     }
     set_force(g, force, n_steps + 1);
@@ -230,13 +278,21 @@ int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, cons
     h2d(dv, v0, g.P.n_nodes(), g.stream());
     g.init_state(du.p, dv.p, 0.0);
     g.record_probes(0);
-    if (h && h->full_state) d2h(h->full_state, g.u.p, g.NSTATE, g.stream());
+    DBuf<double> full;
+    if (h && h->full_state) {
+      full.alloc(g.NSTATE);
+      g.gather_state(full.p);
+      d2h(h->full_state, full.p, g.NSTATE, g.stream());
+    }
     for (int k = 0; k < n_steps; ++k) {
       int it = 0;
       g.step(&it);
       if (h && h->iterations) h->iterations[k] = it;
       if (h && h->residual) h->residual[k] = g.last_rel;
-      if (h && h->full_state) d2h(h->full_state + (size_t)(k + 1) * g.NSTATE, g.u.p, g.NSTATE, g.stream());
+      if (h && h->full_state) {
+        g.gather_state(full.p);
+        d2h(h->full_state + (size_t)(k + 1) * g.NSTATE, full.p, g.NSTATE, g.stream());
+      }
     }
     if (np) {
       std::vector<double> ph((size_t)(n_steps + 1) * np * 2);
@@ -259,7 +315,7 @@ int sgw_stats(sgw_solver* s, double* o) {
     o[1] = g.T.pcg_ms;
     o[2] = g.T.step_ms;
     o[3] = double(g.T.iterations);
-    o[4] = double(g_launches);
+    o[4] = double(g_launches.load());
     o[5] = double(g.T.steps);
     o[6] = g.T.rhs_ms;
     o[7] = g.T.rec_ms;
@@ -359,8 +415,8 @@ int sgw_nearest_node(int nx, int ny, double x, double y) { return nearest_node(n
 
 int sgw_nccl_unique_id(void* out128) {
   return guard([&] {
-    (void)out128;
-    throw Error(SGW_ENCCL, "NCCL sharding not built into this library");
+    if (!out128) throw Error(SGW_EINVAL, "null argument");
+    nccl_unique_id(out128);
   });
 }
 

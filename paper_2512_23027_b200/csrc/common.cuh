@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -25,7 +26,7 @@ struct Error : std::runtime_error {
 
 // Every kernel launch of the library goes through this counter so that the
 // benchmark can report how many of our kernels ran in a timed region.
-extern long long g_launches;
+extern std::atomic<long long> g_launches;
 #define SGW_LAUNCHED()                \
   do {                                \
     ++::sgw::g_launches;              \

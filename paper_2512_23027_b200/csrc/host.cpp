@@ -14,22 +14,26 @@
 namespace sgw {
 
 // ----------------------------------------------------------- geometry ------
-// Structured restatement of partition_structured (src/partition.cpp:48-133)
-// and build_interface_layout / make_flat_maps (src/dd.cpp:10-96) for px | nx,
-// py | ny: interface = non-Dirichlet nodes on internal block lines, corners =
-// cross points (multiplicity 4; boundary-touching corners are Dirichlet).
-Geometry build_geometry(int nx, int ny, int px, int py) {
+// Structured restatement of partition_structured (src/partition.cpp:48-133,
+// floor-division cell ownership, so ragged splits are allowed) and
+// build_interface_layout / make_flat_maps (src/dd.cpp:10-96): interface =
+// non-Dirichlet nodes on internal block lines, corners = cross points
+// (multiplicity 4; boundary-touching corners are Dirichlet).
+Geometry build_geometry(int nx, int ny, int px, int py, int rank, int world) {
   if (nx < 2 || ny < 2) throw Error(1, "build_unit_square_mesh: nx and ny must be >= 2");
   if (px < 1 || py < 1 || px > nx || py > ny) throw Error(1, "partition_structured: bad px/py");
-  if (nx % px || ny % py) throw Error(1, "GPU path requires px | nx and py | ny");
   Geometry g;
-  g.nx = nx, g.ny = ny, g.px = px, g.py = py, g.mx = nx / px, g.my = ny / py;
+  g.nx = nx, g.ny = ny, g.px = px, g.py = py;
+  g.mx = (nx + px - 1) / px, g.my = (ny + py - 1) / py;  // widest block (partition.cpp:70-76)
   g.n = (nx - 1) * (ny - 1);
+  std::vector<char> vl(nx + 1, 0), hl(ny + 1, 0);
+  for (int s = 1; s < px; ++s) vl[Geometry::origin(s, nx, px)] = 1;
+  for (int s = 1; s < py; ++s) hl[Geometry::origin(s, ny, py)] = 1;
   g.iface_pos_of_dof.assign(g.n, -1);
   g.corner_pos_of_dof.assign(g.n, -1);
   for (int gj = 1; gj < ny; ++gj)
     for (int gi = 1; gi < nx; ++gi) {
-      const bool vline = gi % g.mx == 0, hline = gj % g.my == 0;
+      const bool vline = vl[gi], hline = hl[gj];
       if (!(vline || hline)) continue;
       const int d = g.dof(gi, gj);
       g.iface_pos_of_dof[d] = static_cast<int>(g.iface_dofs.size());
@@ -41,23 +45,31 @@ Geometry build_geometry(int nx, int ny, int px, int py) {
     }
   g.n_iface = static_cast<int>(g.iface_dofs.size());
   g.n_corner = static_cast<int>(g.corner_dofs.size());
-  g.ns = px * py;
+  g.ns_total = px * py;
+  if (world < 1 || rank < 0 || rank >= world) throw Error(1, "bad rank / world_size");
+  if (world > g.ns_total) throw Error(1, "more ranks than subdomains");
+  g.world = world;
+  g.s0 = Geometry::first_sub(rank, g.ns_total, world);
+  g.ns = Geometry::first_sub(rank + 1, g.ns_total, world) - g.s0;
   g.W = g.mx - 1;
   g.H = g.my - 1;
   g.nl = (g.mx + 1) * (g.my + 1);
   g.sub.resize(g.ns);
-  for (int s = 0; s < g.ns; ++s) {
-    Geometry::Sub& sd = g.sub[s];
+  for (int sl = 0; sl < g.ns; ++sl) {
+    Geometry::Sub& sd = g.sub[sl];
+    const int s = g.s0 + sl;
     sd.sx = s % px;
     sd.sy = s / px;
+    sd.ox = Geometry::origin(sd.sx, nx, px), sd.oy = Geometry::origin(sd.sy, ny, py);
+    sd.mxs = Geometry::origin(sd.sx + 1, nx, px) - sd.ox, sd.mys = Geometry::origin(sd.sy + 1, ny, py) - sd.oy;
     sd.lid_to_p.assign(g.nl, -1);
     // ascending reduced dof id == row-major over local nodes
-    for (int jl = 0; jl <= g.my; ++jl)
-      for (int il = 0; il <= g.mx; ++il) {
+    for (int jl = 0; jl <= sd.mys; ++jl)
+      for (int il = 0; il <= sd.mxs; ++il) {
         const int lid = jl * (g.mx + 1) + il;
-        const int d = g.dof(sd.sx * g.mx + il, sd.sy * g.my + jl);
+        const int d = g.dof(sd.ox + il, sd.oy + jl);
         if (d < 0) continue;
-        if (il > 0 && il < g.mx && jl > 0 && jl < g.my) {
+        if (il > 0 && il < sd.mxs && jl > 0 && jl < sd.mys) {
           sd.lid_to_p[lid] = -2;
           continue;
         }
@@ -76,6 +88,12 @@ Geometry build_geometry(int nx, int ny, int px, int py) {
       }
   }
   return g;
+}
+
+int Geometry::owner_of_dof(int d) const {
+  if (world == 1 || iface_pos_of_dof[d] >= 0) return 0;
+  const int gi = d % (nx - 1) + 1, gj = d / (nx - 1) + 1;
+  return owner_of_sub((gj * py / ny) * px + gi * px / nx);  // interior: the block of cell (gi, gj)
 }
 
 // ----------------------------------------------------------- stencils ------
@@ -149,11 +167,11 @@ Stencils build_stencils(const Problem& p, const Geometry& g, bool need_local) {
   st.Ml.assign(size_t(g.ns) * 4 * nl, 0.0);
   auto work = [&](int s) {
     const Geometry::Sub& sd = g.sub[s];
-    for (int cjl = 0; cjl < g.my; ++cjl)
-      for (int cil = 0; cil < g.mx; ++cil)
+    for (int cjl = 0; cjl < sd.mys; ++cjl)
+      for (int cil = 0; cil < sd.mxs; ++cil)
         for (int tri = 0; tri < 2; ++tri) {
           int gi[3], gj[3];
-          cell_tris(sd.sx * g.mx + cil, sd.sy * g.my + cjl, tri, gi, gj);
+          cell_tris(sd.ox + cil, sd.oy + cjl, tri, gi, gj);
           double area, b[3], c[3];
           geom_of(gi, gj, p.nx, p.ny, area, b, c);
           double geom[3][3];
@@ -163,7 +181,7 @@ Stencils build_stencils(const Problem& p, const Geometry& g, bool need_local) {
           int lid[3], node[3];
           bool free_[3];
           for (int a = 0; a < 3; ++a) {
-            lid[a] = (gj[a] - sd.sy * g.my) * (mx + 1) + (gi[a] - sd.sx * g.mx);
+            lid[a] = (gj[a] - sd.oy) * (mx + 1) + (gi[a] - sd.ox);
             node[a] = gj[a] * nn1 + gi[a];
             free_[a] = g.dof(gi[a], gj[a]) >= 0;
           }

@@ -10,7 +10,7 @@
 
 namespace sgw {
 
-long long g_launches = 0;
+std::atomic<long long> g_launches{0};
 
 enum Scal { RZ = 0, RZN = 1, PQ = 2, RR = 3, BB = 4, RT = 5, TMP = 6, NSCAL = 8 };
 constexpr int kRedBlocks = 512;  // max partial-sum blocks of a reduction
@@ -263,6 +263,7 @@ void GpuSolver::schur_matvec(const double* x, double* y) {
                                               inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
                                               Sp.d_tile_base.p, Sp.d_ntile.p, nullptr, nullptr, nullptr, nullptr);
   SGW_LAUNCHED();
+  allreduce(y, NG);  // sharded: partial sums over owned subdomains
   ++T.matvecs;
 }
 
@@ -380,6 +381,7 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
     coarse_assemble_kernel<<<cdiv(NC, 256), 256, 0, st_>>>(c_d.p, d_coff.p, cinv_cnt.p, cinv_s.p, cinv_c.p, nc_d.p,
                                                            G.n_corner, NC, dcoarse.p);
     SGW_LAUNCHED();
+    allreduce(dcoarse.p, NC);
     symv_dense_kernel<<<cdiv(NC, 8), 256, 0, st_>>>(Finv.p, dcoarse.p, ucoarse.p, NC);
     SGW_LAUNCHED();
   }
@@ -389,6 +391,7 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
       has_coarse ? 1 : 0);
   SGW_LAUNCHED();
   scatter_li(li_y.p, z, true, nullptr, nullptr);
+  allreduce(z, NG);
   ++T.nn2s;
 }
 
@@ -410,7 +413,7 @@ double GpuSolver::dot_host(const double* a, const double* b, long long len) {
 // src/pcg.cpp:7-50: x0 = 0; stop on the recurrence residual, confirm with the
 // true residual, restart from it (without resetting p) if the check fails.
 int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
-  if (use_fused_) return pcg_fused(b, x, converged, hist);
+  if (use_fused_ && !comm_) return pcg_fused(b, x, converged, hist);
   cudaEventRecord(ev_[0], st_);
   const long long N = NG;
   const int grid = red_grid(N);
@@ -444,8 +447,14 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     symv(Sp, li_x.p, nullptr);
     scatter_kernel<true><<<grid, 256, 0, st_>>>(vq.p, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
                                                 inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
-                                                Sp.d_tile_base.p, Sp.d_ntile.p, vp.p, dpart.p, dcount.p, scal.p + PQ);
+                                                Sp.d_tile_base.p, Sp.d_ntile.p, comm_ ? nullptr : vp.p, dpart.p,
+                                                dcount.p, scal.p + PQ);
     SGW_LAUNCHED();
+    if (comm_) {  // sharded: q is complete only after the sum over ranks
+      allreduce(vq.p, NG);
+      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      SGW_LAUNCHED();
+    }
     ++T.matvecs;
     cg_xr_kernel<<<grid, 256, 0, st_>>>(x, vr.p, vp.p, vq.p, N, scal.p, dpart.p, dcount.p);
     SGW_LAUNCHED();

@@ -520,6 +520,11 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
 
 // --------------------------------------------------------------- host ----
 void GpuSolver::setup_fused_pcg() {
+  tphase_.alloc(8), tphase_.zero(st_);
+  if (comm_) {  // sharded: the host-driven loop with a sum over ranks after each scatter
+    use_fused_ = false;
+    return;
+  }
   // S-space local gather map (padded like Sp): global flat interface index or -1
   std::vector<int> smap(Sp.xlen, -1);
   for (int s = 0; s < NS; ++s) {
@@ -539,7 +544,6 @@ void GpuSolver::setup_fused_pcg() {
   fused_out_.alloc(4);
   fused_hist_.alloc(P.max_iter + 8);
   for (DBuf<double>* b : {&li_z_, &li_p_, &li_xx_}) b->alloc(Sp.xlen), b->zero(st_);  // padding stays 0
-  tphase_.alloc(8), tphase_.zero(st_);
   ucl_.alloc(std::max<long long>(1, coff_.back())), ucl_.zero(st_);
   wr_.alloc(std::max<long long>(1, Qp.xlen)), wr_.zero(st_);
   const char* e = std::getenv("SGW_PCG");

@@ -98,12 +98,20 @@ __global__ void assemble_ii_kernel(SetupArgs A, double* __restrict__ D, double* 
     const int il = i + 1, jl = k + 1, lid = jl * (A.mx + 1) + il;
     const double* Kl_s = A.Kl + (size_t)s * A.nin * 3 * A.nl;
     const double* Ml_s = A.Ml + (size_t)s * 4 * A.nl;
+    const int* cls = A.lid_to_p + (size_t)s * A.nl;
     double* Dk = D + ((size_t)s * A.H + k) * A.B * A.B;
+    // positions of the padded grid that are not interior nodes of a ragged
+    // block (its interface / boundary line, padding) are decoupled unit rows
+    if (cls[lid] != -2) {
+      Dk[(size_t)row * A.B + row] = 1.0;
+      continue;
+    }
     // same grid row: W, self, E
     for (int dir = 0; dir < 3; ++dir) {
       const int i2 = i + kDI[dir];
       if (i2 < 0 || i2 >= A.W) continue;
       const int nb = lid + kDI[dir];
+      if (cls[nb] != -2) continue;
       for (int jt = 0; jt < A.nt; ++jt)
         Dk[(size_t)(i2 * A.nt + jt) * A.B + row] =
             transient_entry(Kl_s, Ml_s, A.nl, A.nin, lid, nb, dir, kt, jt, A.nt, A.ms, A.ss, A.gp_ptr, A.gp_i, A.gp_v);
@@ -115,6 +123,7 @@ __global__ void assemble_ii_kernel(SetupArgs A, double* __restrict__ D, double* 
         const int i2 = i + kDI[dir];
         if (i2 < 0) continue;
         const int nb = lid + kDI[dir] + kDJ[dir] * (A.mx + 1);
+        if (cls[nb] != -2) continue;
         for (int jt = 0; jt < A.nt; ++jt)
           Ek[(size_t)(i2 * A.nt + jt) * A.B + row] =
               transient_entry(Kl_s, Ml_s, A.nl, A.nin, lid, nb, dir, kt, jt, A.nt, A.ms, A.ss, A.gp_ptr, A.gp_i, A.gp_v);
@@ -134,6 +143,7 @@ __global__ void assemble_rhs_kernel(SetupArgs A, int k, double* __restrict__ R, 
     const double* Ml_s = A.Ml + (size_t)s * 4 * A.nl;
     double* Rs = R + (size_t)s * A.B * amax;
     const int ng = A.ng[s];
+    if (A.lid_to_p[(size_t)s * A.nl + lid] != -2) continue;  // unit row of a ragged block
     for (int dir = 1; dir < 7; ++dir) {
       const int nb = lid + kDI[dir] + kDJ[dir] * (A.mx + 1);
       const int p = A.lid_to_p[(size_t)s * A.nl + nb];
@@ -322,14 +332,15 @@ void GpuSolver::build_maps() {
 }
 
 // ---------------------------------------------------------- constructor ----
-GpuSolver::GpuSolver(Problem p) : P(std::move(p)) {
+GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), comm_(std::move(comm)) {
   const auto t0 = std::chrono::steady_clock::now();
   if ((int)P.coeff.size() != P.n_in * P.n_nodes() || P.n_in != P.tensor.n_in)
     throw Error(1, "SgSolver: coefficient terms do not match tensor input size");
   if (P.tensor.n_out < 1) throw Error(1, "SgSolver: tensor has no output terms");
   if (!(P.dt > 0.0)) throw Error(1, "SgSolver: dt must be positive");
-  G = build_geometry(P.nx, P.ny, P.px, P.py);
-  if (G.ns < 2 || G.n_iface == 0) throw Error(1, "GPU path needs an interface (more than one subdomain)");
+  if (comm_ && (comm_->rank() != P.rank || comm_->size() != P.world)) throw Error(1, "communicator / rank mismatch");
+  G = build_geometry(P.nx, P.ny, P.px, P.py, P.rank, P.world);
+  if (G.ns_total < 2 || G.n_iface == 0) throw Error(1, "GPU path needs an interface (more than one subdomain)");
   if (G.W < 1 || G.H < 1) throw Error(1, "GPU path needs interior dofs in every subdomain (mx, my >= 2)");
   NT = P.tensor.n_out;
   NIN = P.n_in;
@@ -364,6 +375,7 @@ GpuSolver::GpuSolver(Problem p) : P(std::move(p)) {
   fG.alloc(Sp.xlen), fG.zero(st_);
   const size_t nI = size_t(NS) * G.H * B;
   fI.alloc(nI), yI.alloc(nI), wI.alloc(nI);
+  yI.zero(st_), wI.zero(st_);  // unit rows of ragged blocks stay zero
   scal.alloc(16), scal.zero(st_);
   dpart.alloc(1024), dcount.alloc(4), dcount.zero(st_);
   setup_fused_pcg();
@@ -609,6 +621,12 @@ void GpuSolver::setup_nn2() {
           fcc[(size_t)gb * NC + ga] += h[(size_t)b2 * cs + a2];
         }
     }
+  }
+  if (NC > 0 && comm_) {  // F_cc = sum over all ranks' subdomains (dd.cpp:128-137)
+    Finv.upload(fcc);
+    allreduce(Finv.p, fcc.size());
+    SGW_CUDA(cudaMemcpyAsync(fcc.data(), Finv.p, fcc.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    SGW_CUDA(cudaStreamSynchronize(st_));
   }
   fcc_host_ = fcc;
   if (NC > 0) {

@@ -20,6 +20,7 @@
 #include <memory>
 #include <vector>
 
+#include "comm.hpp"
 #include "common.cuh"
 #include "host.hpp"
 
@@ -62,7 +63,7 @@ struct DBuf {
     p = nullptr;
     n = 0;
   }
-  static inline long long g_bytes = 0;
+  static inline std::atomic<long long> g_bytes{0};
 };
 
 // Batch of symmetric matrices stored as lower 64x64 tiles.
@@ -93,7 +94,7 @@ struct LocalArgs {
   const int* lid_to_p;
   const long long* lioff;
   const int* ng;
-  int nl, nin, nt, mx, my, px, nx, H, B;
+  int nl, nin, nt, mx, my, px, nx, py, ny, H, B, s0;
   double ms, ss;
 };
 
@@ -149,7 +150,7 @@ struct KProf {
 
 class GpuSolver {
  public:
-  GpuSolver(Problem p);
+  explicit GpuSolver(Problem p, std::unique_ptr<Comm> comm = nullptr);
   ~GpuSolver();
 
   // reference-facing operations (device buffers in/out)
@@ -162,6 +163,10 @@ class GpuSolver {
   void set_force_table(const double* table_host, int n_rows);
   int step(int* iters_out);  // one Newmark step on device
   std::vector<double> coarse_operator_host() const { return fcc_host_; }
+  // full state on every rank (sharded runs: owners' values summed across ranks)
+  void gather_state(double* dst_dev);
+  int rank() const { return comm_ ? comm_->rank() : 0; }
+  int world() const { return comm_ ? comm_->size() : 1; }
 
   cudaStream_t stream() const { return st_; }
   void set_stream(cudaStream_t s);
@@ -173,7 +178,7 @@ class GpuSolver {
   double setup_s = 0;
   Timers T;
   KProf KP;
-  long long device_bytes() const { return DBuf<double>::g_bytes; }
+  long long device_bytes() const { return DBuf<double>::g_bytes.load(); }
   // algorithmic bytes: unique symmetric entries of all S_s / Q_s
   double bytes_S() const;
   double bytes_Q() const;
@@ -187,13 +192,18 @@ class GpuSolver {
   int step_index = 0;
   // probes (device history) filled per step
   std::vector<int> probe_dofs;
-  DBuf<int> d_probe_dofs;
+  DBuf<int> d_probe_dofs, d_probe_own;  // own: sharded runs, probe dof owned by this rank
   DBuf<double> probe_hist;  // [step][probe][2]: mean, std
   int probe_cap = 0;
   void record_probes(int step);
   double last_rel = 0.0;  // final true residual of the last PCG solve
 
  private:
+  std::unique_ptr<Comm> comm_;  // null on a single GPU
+  void allreduce(double* buf, size_t n) {
+    if (comm_) comm_->allreduce_sum(buf, n, st_);
+  }
+  DBuf<double> own_mask_;  // sharded: 1 on dofs this rank owns (Geometry::owner_of_dof), per term
   void build_device_inputs(const Stencils& st);
   void setup_interior_and_schur();
   void setup_nn2();

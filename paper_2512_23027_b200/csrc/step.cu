@@ -94,8 +94,10 @@ void GpuSolver::apply_block(int op, const double* x, double* y) {
 // -------------------------------------------------------- local operators --
 // reduced dof of local node (il, jl) of subdomain s; callers only ask for
 // non-Dirichlet nodes (lid_to_p != -1)
+__device__ __forceinline__ int block_origin(int s, int n, int p) { return (s * n + p - 1) / p; }
 __device__ __forceinline__ int lid_dof(const LocalArgs& A, int s, int il, int jl) {
-  const int gi = (s % A.px) * A.mx + il, gj = (s / A.px) * A.my + jl;
+  const int sg = A.s0 + s;  // global subdomain id
+  const int gi = block_origin(sg % A.px, A.nx, A.px) + il, gj = block_origin(sg / A.px, A.ny, A.py) + jl;
   return (gj - 1) * (A.nx - 1) + gi - 1;
 }
 __device__ __forceinline__ long long interior_index(const LocalArgs& A, int s, int il, int jl, int term) {
@@ -260,8 +262,8 @@ __global__ void predictor_kernel(const double* __restrict__ u, const double* __r
 __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, double* __restrict__ a,
                               const double* __restrict__ ug, const double* __restrict__ yI,
                               const double* __restrict__ wI, const int* __restrict__ iface_of_dof, int n, int nt,
-                              int n_iface, int nx, int mx, int my, int px, int H, int B, double dt, double zeta,
-                              double gamma) {
+                              int n_iface, int nx, int ny, int px, int py, int H, int B, int s0, int ns,
+                              double dt, double zeta, double gamma) {
   const long long N = (long long)n * nt;
   const double zdd = zeta * dt * dt, c1 = (1.0 - 2.0 * zeta) / (2.0 * zeta);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
@@ -272,8 +274,12 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
       un = ug[(long long)k * n_iface + q];
     } else {
       const int gi = d % (nx - 1) + 1, gj = d / (nx - 1) + 1;
-      const int sx = gi / mx, sy = gj / my, il = gi - sx * mx, jl = gj - sy * my;
-      const long long idx = ((long long)(sy * px + sx) * H + (jl - 1)) * B + (long long)(il - 1) * nt + k;
+      // interior node: cell gi lies in the same block (partition.cpp:70-76)
+      const int sx = gi * px / nx, sy = gj * py / ny;
+      const int il = gi - block_origin(sx, nx, px), jl = gj - block_origin(sy, ny, py);
+      const int sl = sy * px + sx - s0;
+      if (sl < 0 || sl >= ns) continue;  // sharded: interior of another rank's subdomain
+      const long long idx = ((long long)sl * H + (jl - 1)) * B + (long long)(il - 1) * nt + k;
       un = yI[idx] - wI[idx];
     }
     const double uo = u[t], vo = v[t], ao = a[t];
@@ -284,9 +290,13 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
   }
 }
 
-__global__ void probe_kernel(const double* __restrict__ u, const int* __restrict__ pd, int np, int n, int nt,
-                             double* __restrict__ out) {
+__global__ void probe_kernel(const double* __restrict__ u, const int* __restrict__ pd, const int* __restrict__ own,
+                             int np, int n, int nt, double* __restrict__ out) {
   for (int p = threadIdx.x; p < np; p += blockDim.x) {
+    if (own && !own[p]) {  // sharded: the owning rank contributes this probe
+      out[2 * p] = out[2 * p + 1] = 0.0;
+      continue;
+    }
     double var = 0.0;
     for (int j = 1; j < nt; ++j) {
       const double c = u[(long long)j * n + pd[p]];
@@ -393,7 +403,7 @@ const double* GpuSolver::force_at(double t, int row, double* fval) {
 
 LocalArgs GpuSolver::local_args() const {
   return LocalArgs{Kl.p, Ml.p, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, lid_to_p.p, Sp.d_xoff.p, ng_d.p, G.nl, NIN,
-                   NT, G.mx, G.my, G.px, P.nx, G.H, B, P.mass_scale, P.stiff_scale};
+                   NT, G.mx, G.my, G.px, P.nx, G.py, P.ny, G.H, B, G.s0, P.mass_scale, P.stiff_scale};
 }
 
 // src/sg.cpp:358-376: u, v in block 0, a = M^-1 (f0 - a0 M v - a1 K v - K u).
@@ -427,9 +437,30 @@ void GpuSolver::init_state(const double* u0_nodal, const double* v0_nodal, doubl
 
 void GpuSolver::record_probes(int k) {
   if (probe_dofs.empty() || k >= probe_cap) return;
-  probe_kernel<<<1, 128, 0, st_>>>(u.p, d_probe_dofs.p, (int)probe_dofs.size(), n, NT,
-                                   probe_hist.p + (size_t)k * probe_dofs.size() * 2);
+  double* row = probe_hist.p + (size_t)k * probe_dofs.size() * 2;
+  probe_kernel<<<1, 128, 0, st_>>>(u.p, d_probe_dofs.p, comm_ ? d_probe_own.p : nullptr, (int)probe_dofs.size(), n,
+                                   NT, row);
   SGW_LAUNCHED();
+  allreduce(row, probe_dofs.size() * 2);
+}
+
+__global__ void mask_state_kernel(double* __restrict__ x, const double* __restrict__ mask, int n, long long N) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+    x[i] *= mask[i % n];
+}
+
+void GpuSolver::gather_state(double* dst) {
+  SGW_CUDA(cudaMemcpyAsync(dst, u.p, NSTATE * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  if (!comm_) return;
+  if (own_mask_.n != (size_t)n) {
+    std::vector<double> m(n);
+    for (int d = 0; d < n; ++d) m[d] = G.owner_of_dof(d) == comm_->rank() ? 1.0 : 0.0;
+    own_mask_.upload(m);
+  }
+  mask_state_kernel<<<std::min(cdiv((long long)NSTATE, 256), 4096), 256, 0, st_>>>(dst, own_mask_.p, n,
+                                                                                   (long long)NSTATE);
+  SGW_LAUNCHED();
+  allreduce(dst, NSTATE);
 }
 
 int GpuSolver::step(int* iters_out) {
@@ -451,6 +482,7 @@ int GpuSolver::step(int* iters_out) {
                                                                    iface_lid_.p, li_y.p, nullptr, NS);
   SGW_LAUNCHED();
   scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
+  allreduce(vb.p, NG);
   cudaEventRecord(ev_[3], st_);
   bool conv = false;
   const int it = pcg(vb.p, vx.p, &conv, nullptr);
@@ -463,7 +495,7 @@ int GpuSolver::step(int* iters_out) {
   SGW_LAUNCHED();
   sweep(wI.p);  // A_II^-1 A_IG u_G
   update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
-                                       G.mx, G.my, G.px, G.H, B, P.dt, P.zeta, P.gamma);
+                                       P.ny, G.px, G.py, G.H, B, G.s0, NS, P.dt, P.zeta, P.gamma);
   SGW_LAUNCHED();
   t_now = t_now + P.dt;
   ++step_index;

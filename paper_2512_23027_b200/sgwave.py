@@ -93,6 +93,10 @@ def load_library():
     L.sgw_triple_products.argtypes = [ip, ip, ip, C.POINTER(ip), C.POINTER(ip), C.POINTER(ip), vp, vp, vp, vp,
                                       C.c_longlong]
     L.sgw_nearest_node.argtypes = [ip, ip, dp, dp]
+    L.sgw_nccl_unique_id.argtypes = [vp]
+    L.sgw_local_group_new.argtypes = [ip, C.POINTER(vp)]
+    L.sgw_local_group_free.argtypes = [vp]
+    L.sgw_create_local_group.argtypes = [C.POINTER(_Problem), ip, ip, vp, C.POINTER(vp)]
     _LIB = L
     return L
 
@@ -246,12 +250,73 @@ class SchurSystem:
         return out.reshape(n, n).T.copy()
 
 
+def shard_plan(n_sub: int, world_size: int) -> list[range]:
+    """Subdomains owned by each rank: contiguous row-major ranges
+    [n_sub r / W, n_sub (r+1) / W) (Geometry::first_sub in csrc/host.hpp)."""
+    if not 1 <= world_size <= n_sub:
+        raise SgInvalidArgument(SGW_EINVAL, "need 1 <= world_size <= number of subdomains")
+    return [range(n_sub * r // world_size, n_sub * (r + 1) // world_size) for r in range(world_size)]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it, the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().sgw_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+class LocalGroup:
+    """W sharded solvers in one process on one device, each driven by its own
+    thread (the exchange is host-synchronised; see include/sgw.h).  Every
+    call is collective: use map() so all ranks make it concurrently."""
+
+    def __init__(self, world_size):
+        self.world_size = world_size
+        self._g = C.c_void_p()
+        _check(load_library().sgw_local_group_new(world_size, C.byref(self._g)))
+
+    def map(self, fn, timeout=600.0):
+        """[fn(rank) for rank in range(W)], each call on its own thread."""
+        import threading
+        out, err = [None] * self.world_size, []
+
+        def body(r):
+            try:
+                out[r] = fn(r)
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                err.append(e)
+        th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.world_size)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout)
+        if any(t.is_alive() for t in th):
+            raise SgError(SGW_ENCCL, "local group: a rank did not finish (collective mismatch?)")
+        if err:
+            raise err[0]
+        return out
+
+    def solvers(self, *args, **kw):
+        return self.map(lambda r: SgSolver(*args, rank=r, world_size=self.world_size, local_group=self, **kw))
+
+    def close(self):
+        if getattr(self, "_g", None):
+            load_library().sgw_local_group_free(self._g)
+            self._g = None
+
+    __del__ = close
+
+
 class SgSolver:
     """B200 SgSolver (src/sg.cpp).  Setup (interior factorizations, local
     Schur complements, NN2 data) runs on the GPU in the constructor."""
 
     def __init__(self, nx, ny, px, py, coeff, tensor, density=1.0, alpha0=0.5445, alpha1=0.0174,
-                 params: NewmarkParams | None = None, options: SgOptions | None = None):
+                 params: NewmarkParams | None = None, options: SgOptions | None = None, *, rank=0, world_size=1,
+                 nccl_id: bytes | None = None, local_group: "LocalGroup | None" = None):
+        """world_size > 1 shards the subdomains over ranks (include/sgw.h): one
+        process per GPU with the rank-0 `nccl_id` (nccl_unique_id()), or, for
+        tests on one device, one thread per rank sharing a LocalGroup."""
         L = load_library()
         self.params = params or NewmarkParams()
         self.options = options or SgOptions()
@@ -266,11 +331,20 @@ class SgSolver:
         prob = _Problem(nx, ny, px, py, self._coeff.shape[0], _p(self._coeff), int(tensor.n_output), len(tv),
                         _p(ti), _p(tj), _p(tk), _p(tv), density, alpha0, alpha1, self.params.gamma,
                         self.params.zeta, self.params.dt, self.options.tol, self.options.max_iter,
-                        self.options.device, 0, 1, None)
+                        self.options.device, rank, world_size, None)
         if self._coeff.shape[0] != tensor.n_input:
             raise SgInvalidArgument(SGW_EINVAL, "SgSolver: coefficient terms do not match tensor input size")
+        self.rank, self.world_size = rank, world_size
         h = C.c_void_p()
-        _check(L.sgw_create(C.byref(prob), C.byref(h)))
+        if local_group is not None:
+            _check(L.sgw_create_local_group(C.byref(prob), world_size, rank, local_group._g, C.byref(h)))
+        else:
+            if world_size > 1:
+                if nccl_id is None or len(nccl_id) != 128:
+                    raise SgInvalidArgument(SGW_EINVAL, "world_size > 1 needs the 128-byte NCCL id of rank 0")
+                self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
+                prob.nccl_id = C.cast(self._nccl_id, C.c_void_p)
+            _check(L.sgw_create(C.byref(prob), C.byref(h)))
         self._h = h
         s = np.zeros(8, np.int64)
         _check(L.sgw_sizes(self._h, _p(s)))

@@ -41,7 +41,8 @@ def test_apply_block_matches_oracle(gpu, op):
     assert relerr(a, b) <= 1e-12
 
 
-@pytest.mark.parametrize("cfg", [(8, 2, 1, 1, 1, 1), (12, 2, 2, 2, 2, 2), (16, 4, 4, 2, 4, 2), (24, 3, 2, 3, 2, 3)])
+@pytest.mark.parametrize("cfg", [(8, 2, 1, 1, 1, 1), (12, 2, 2, 2, 2, 2), (16, 4, 4, 2, 4, 2), (24, 3, 2, 3, 2, 3),
+                                 (22, 4, 3, 2, 2, 2), (13, 5, 2, 1, 2, 2)])
 def test_schur_and_nn2_match_oracle(gpu, cfg):
     nx, px, py, L, pin, pout = cfg
     g, c = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 1e-3)
@@ -142,6 +143,54 @@ def test_interior_sweep_every_cluster_size(gpu, monkeypatch, cs):
     hc = c.run(u0, 0 * u0, 6, store_full=True)
     assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
+@pytest.mark.parametrize("cs", ["1", "4"])
+def test_ragged_partition_trajectory(gpu, monkeypatch, cs):
+    # partition_structured's floor-division ownership (partition.cpp:70-76)
+    # with px, py not dividing nx: blocks of two widths in a padded frame
+    monkeypatch.setenv("SGW_SWEEP_CS", cs)
+    nx = 26
+    g, c = pair(nx, 4, 3, 0.3, 0.5, 2, 3, 2, 2e-3)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 8, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 8, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world,case", [(2, (24, 24, 3, 2)), (3, (26, 20, 4, 3)), (4, (16, 16, 2, 2))])
+def test_sharded_ranks_match_single_gpu(gpu, world, case):
+    # the multi-GPU decomposition (include/sgw.h): ranks own contiguous
+    # subdomain ranges and sum their partials after every subdomain scatter.
+    # Here the ranks are threads on one device (LocalGroup), exercising the
+    # same sharded code path the NCCL communicator drives across GPUs.
+    nx, ny, px, py = case
+    coeff = O.lognormal_coeff(nx, ny, 0.3, 0.5, 0.5, 2, 3)
+    t = O.triple_products(2, 3, 2)
+    probes = [O.nearest_node(nx, ny, 0.5, 0.5), O.nearest_node(nx, ny, 0.2, 0.8), O.nearest_node(nx, ny, 0.9, 0.1)]
+    kw = dict(params=sg.NewmarkParams(dt=2e-3), options=sg.SgOptions(tol=1e-10, store_full=True, probe_nodes=probes))
+    one = sg.SgSolver(nx, ny, px, py, coeff, t, **kw)
+    grp = sg.LocalGroup(world)
+    ranks = grp.solvers(nx, ny, px, py, coeff, t, **kw)
+    x = rand(one.n_global, 5)
+    for y in grp.map(lambda r: ranks[r].schur().matvec(x)):
+        assert relerr(y, one.schur().matvec(x)) <= 1e-12
+    for z in grp.map(lambda r: ranks[r].schur().apply_nn2(x)):
+        assert relerr(z, one.schur().apply_nn2(x)) <= 1e-10
+    if one.n_corner:
+        for f in grp.map(lambda r: ranks[r].schur().coarse_operator()):
+            assert relerr(f, one.schur().coarse_operator()) <= 1e-12
+    u0 = np.zeros((nx + 1) * (ny + 1))
+    force = sg.ForceSpec(node=O.nearest_node(nx, ny, 0.5, 0.5))
+    h1 = one.run(u0, u0, 8, force)
+    for h in grp.map(lambda r: ranks[r].run(u0, u0, 8, force)):
+        assert np.all(np.abs(h.iterations - h1.iterations) <= 1)
+        assert np.linalg.norm(h.full_state - h1.full_state) / np.linalg.norm(h1.full_state) <= 1e-10
+        assert np.abs(h.probe_mean - h1.probe_mean).max() <= 1e-9 * np.abs(h1.probe_mean).max()
+    grp.close()
 
 
 def test_zero_data_stays_zero(gpu):

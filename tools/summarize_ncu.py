@@ -28,7 +28,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "lts__t_bytes.sum",
         "l1tex__t_bytes.sum"]
 # bench kernel class of each CUDA kernel name prefix
-CLASS = {"symv_tiles_kernel": "symv_S", "gemv_n_sub_kernel": "interior_sweep", "gemv_t_sub_kernel": "interior_sweep",
+CLASS = {"symv_tiles_kernel": "symv_S", "sweep_kernel": "interior_sweep", "pcg_fused_kernel": "pcg_fused",
          "sg_apply_global_kernel": "sg_operator"}
 
 
@@ -82,13 +82,14 @@ def full_captures(tag, config):
             per_launch.append((kname, tobytes("dram__bytes_read.sum") + tobytes("dram__bytes_write.sum")))
         with open(os.path.join(PROF, f"{tag}_ncu_{name}.txt"), "w") as f:
             f.write(f"# ncu --set full --clock-control none, {os.path.basename(rep)}\n\n" + "\n\n".join(lines) + "\n")
+        fresh = {}
         for kname, b in per_launch:
-            cls = CLASS.get(kname)
+            cls = CLASS.get(kname.replace("void ", "").split("<")[0])
             if cls:
-                summary.setdefault(config, {}).setdefault(cls, {})
-                summary[config][cls].setdefault("dram_bytes_per_launch_samples", []).append(b)
-                s = summary[config][cls]["dram_bytes_per_launch_samples"]
-                summary[config][cls]["dram_bytes_per_launch"] = sum(s) / len(s)
+                fresh.setdefault(cls, []).append(b)
+        for cls, s in fresh.items():  # replaces older samples of the same kernel class
+            summary.setdefault(config, {})[cls] = {"dram_bytes_per_launch_samples": s,
+                                                   "dram_bytes_per_launch": sum(s) / len(s), "source": f"{tag}_ncu_{name}.txt"}
         print(open(os.path.join(PROF, f"{tag}_ncu_{name}.txt")).read())
     json.dump(summary, open(summary_path, "w"), indent=1)
 
