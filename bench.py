@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
+                    help="N>1: shard the subdomains over the ranks (one problem, NCCL sums) or run N replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     c = CONFIGS[args.config]
@@ -186,9 +188,15 @@ def main():
     coeff = sg.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
     tensor = sg.triple_products(c["L"], c["p_in"], c["p_out"])
     node = sg.nearest_node(nx, nx, 0.5, 0.5)
+    shard = world > 1 and args.mode == "shard"
+    kw = {}
+    if shard:  # rank r owns subdomains shard_plan(n_sub, N)[r]; the NCCL id travels over torch.distributed
+        ids = [sg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        kw = dict(rank=rank, world_size=world, nccl_id=ids[0])
     t0 = time.perf_counter()
     solver = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, tensor, alpha0=ALPHA0, alpha1=ALPHA1,
-                         params=sg.NewmarkParams(dt=c["dt"]), options=sg.SgOptions(tol=TOL, device=local))
+                         params=sg.NewmarkParams(dt=c["dt"]), options=sg.SgOptions(tol=TOL, device=local), **kw)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     solver.set_stream(stream.cuda_stream)
@@ -227,6 +235,8 @@ def main():
         n = torch.tensor([float(iters)], device="cuda")
         torch.distributed.all_reduce(n)
         ms, pcg_ms, iters_all = float(t[0]), float(t[1]), int(n[0])
+        if shard:  # one problem: every rank runs the same iterations
+            iters_all = iters
     else:
         iters_all = iters
     value = gdof * iters_all / (pcg_ms / 1e3) / 1e9
@@ -256,11 +266,13 @@ def main():
     iter_ms = pcg_ms / max(iters, 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic KLE/PCE inputs of the config; seeds have no effect on the SG solve)",
         "config": {"workload": workload_desc(args.config, c), "GDOF": gdof / 1e9,
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "parallelism": "single GPU" if world == 1 else (
+                       f"{world} GPUs, subdomains sharded {[len(r) for r in sg.shard_plan(c['px'] ** 2, world)]}, "
+                       "interface sums by ncclAllReduce" if shard else f"{world} independent replicas"),
                    "l2": "inputs larger than L2: S+Q tiles stream ~2.7 GB per PCG iteration (L2 126 MB)"},
         "s_per_newmark_step": ms / args.steps / 1e3,
         "pcg_iterations": iters_all, "mean_iterations_per_step": iters / args.steps,
@@ -295,7 +307,7 @@ def main():
             t = torch.tensor([wall], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             wall = float(t[0])
-        e_iters = int(h.iterations.sum()) * world
+        e_iters = int(h.iterations.sum()) * (1 if shard else world)
         line["e2e"] = {"value": gdof * e_iters / wall / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": 8 * (nx + 1) ** 2 + 2 * 8 * (nx + 1) ** 2 / args.steps,
                        "d2h_bytes_per_step": 8 * (h.iterations.mean() + 2) + 16,
