@@ -1,6 +1,6 @@
 // Per-Newmark-step kernels: stochastic-Galerkin stencil operator applies
 // (global apply_block_*, local force, A_GI / A_IG couplings), the batched
-// block-tridiagonal Dirichlet sweeps and the fused Newmark predictor/update.
+// and the fused Newmark predictor/update (the Dirichlet sweeps are in sweep.cu).
 //
 // Reference: src/sg.cpp:252-356 (local_force, step_rhs_and_solve),
 // src/sg.cpp:358-423 (run), src/sg.cpp:425-447 (apply_block_*),
@@ -197,51 +197,6 @@ __global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict_
     } else {
       outI[interior_index(A, s, il, jl, k)] = acc;
     }
-  }
-}
-
-// ------------------------------------------------------ Dirichlet sweeps ---
-// t = b - A x over column-major B x B blocks (A may be null: t = b); batched.
-__global__ void __launch_bounds__(256) gemv_n_sub_kernel(const double* __restrict__ A, long long sA,
-                                                         const double* __restrict__ x, long long sx,
-                                                         const double* __restrict__ b, long long sb,
-                                                         double* __restrict__ out, long long so, int Bn, int lower) {
-  __shared__ double red[8][33];
-  const int s = blockIdx.y;
-  const int rl = threadIdx.x & 31, cg = threadIdx.x >> 5;
-  const int r = blockIdx.x * 32 + rl;
-  double acc = 0.0;
-  if (A && r < Bn) {
-    const double* As = A + s * sA;
-    const double* xs = x + s * sx;
-    const int cmax = lower ? r + 1 : Bn;
-    for (int c = cg; c < cmax; c += 8) acc += As[(long long)c * Bn + r] * xs[c];
-  }
-  red[cg][rl] = acc;
-  __syncthreads();
-  if (cg == 0 && r < Bn) {
-    double tot = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) tot += red[q][rl];
-    out[s * so + r] = b ? b[s * sb + r] - tot : tot;
-  }
-}
-
-// out = b - A^T x ; warp per output column (A may be null: out = b).
-// lower: A lower triangular, so (A^T x)[c] = sum_{r >= c} A[c*B + r] x[r].
-__global__ void gemv_t_sub_kernel(const double* __restrict__ A, long long sA, const double* __restrict__ x,
-                                  long long sx, const double* __restrict__ b, long long sb, double* __restrict__ out,
-                                  long long so, int Bn, int lower, int negate) {
-  const int s = blockIdx.y, lane = threadIdx.x & 31;
-  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < Bn; c += gridDim.x * (blockDim.x >> 5)) {
-    double acc = 0.0;
-    if (A) {
-      const double* col = A + s * sA + (long long)c * Bn;
-      const double* xs = x + s * sx;
-      for (int r = (lower ? c : 0) + lane; r < Bn; r += 32) acc += col[r] * xs[r];
-      acc = warp_sum(acc);
-    }
-    if (lane == 0) out[s * so + c] = negate ? (b ? b[s * sb + c] : 0.0) - acc : acc;
   }
 }
 

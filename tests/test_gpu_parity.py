@@ -145,6 +145,22 @@ def test_interior_sweep_every_cluster_size(gpu, monkeypatch, cs):
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
 
 
+@pytest.mark.parametrize("cs", ["2", "4"])
+def test_sweep_multi_tile_blocks_reproducible(gpu, monkeypatch, cs):
+    # interior blocks of several 64x64 tiles (B = 47 x 6 = 282: 5 tile rows),
+    # split over a cluster: oracle parity and bitwise-identical reruns (a race
+    # between the ranks' shared-memory pushes would show up as run-to-run noise)
+    monkeypatch.setenv("SGW_SWEEP_CS", cs)
+    nx = 96
+    g, c = pair(nx, 2, 2, 0.3, 0.5, 2, 2, 2, 1e-3)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    runs = [g.run(z, z, 4, sg.ForceSpec(node=node)).full_state for _ in range(3)]
+    hc = c.run(z, z, 4, force_node=node, store_full=True)
+    assert np.linalg.norm(runs[0] - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+    assert all(np.array_equal(runs[0], r) for r in runs[1:])
+
+
 @pytest.mark.parametrize("cs", ["1", "4"])
 def test_ragged_partition_trajectory(gpu, monkeypatch, cs):
     # partition_structured's floor-division ownership (partition.cpp:70-76)
