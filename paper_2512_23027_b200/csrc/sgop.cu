@@ -1,0 +1,508 @@
+// Fused stochastic-Galerkin operator apply (src/sg.cpp:425-447):
+//   y_k = alpha sum_e M^e x_k  +  beta sum_{(i,j)} c_ijk sum_e K_i^e x_j  (+ gamma sum_e M^e x2_k)
+// on a batch of structured node grids, e over the P1 stencil (5 points for K,
+// 7 for M).  The kernel is generated and compiled at setup (NVRTC, sm_100a)
+// for the solver's triple-product tensor, so every (i, j) pair and every
+// c_ijk becomes straight-line code with the PCE terms in named registers:
+//
+//   * CTA = a tile of 32 x R nodes of one grid; G threads per node split the
+//     input terms j (balanced by pair count).  A thread keeps the 5-point
+//     neighbourhoods of its j's in registers for the whole tile and
+//     accumulates all (P+1) outputs.
+//   * K_i stencils (3 stored components per node) stream through a ring of
+//     shared-memory stages, a chunk of input terms i per stage, with
+//     cp.async (16-byte, zero-filled outside the grid); x tiles and M are
+//     staged per tile (double-buffered across tiles).  Per node and i: 5
+//     shared loads, then 5 FMAs per (i, j) pair and 1 per c_ijk.
+//   * The G partial outputs of a node are summed in shared memory in fixed
+//     group order (bitwise reproducible); coalesced stores.
+// K / M live in a padded layout [item][i][c][row][pitch] (pitch even, zero
+// padding); x / y in the caller's layout (any pitch, term and item strides).
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "solver.cuh"
+
+namespace sgw {
+
+namespace {
+const char* kDeviceTemplate = R"CUDA(
+typedef long long ll;
+struct SgOpArgs {
+  const double* K; const double* M;  // tiled stencils (sgop_tile_stencils)
+  const double* xt;                  // tiled input (sgop_pack_x): [tile][NT][R+2][34]
+  const double* x; const double* x2; double* y;
+  ll xterm, xitem, yterm, yitem;
+  int W, H, xpitch, ypitch, tiles_x, tiles_y, items;
+  double alpha, beta, gamma;
+};
+#define XW 34
+#define RUP16(v) (((v) + 15) / 16 * 16)
+#define XBUF RUP16(NT * (R + 2) * XW)
+/* per tile and input term: diag [R][32], E [R][33] (from column -1), N [R+1][32] (from row -1) */
+#define KOE (32 * R)
+#define KON (32 * R + 33 * R)
+#define KPI ((97 * R + 32 + 1) / 2 * 2)
+/* M per tile: diag, E, N as K, then NE [R+1][33] (from row -1, column -1) */
+#define MON (32 * R + 33 * R)
+#define MONE (97 * R + 32)
+#define MPI ((130 * R + 65 + 1) / 2 * 2)
+#define MBUF RUP16(MPI)
+#define KSTG RUP16(IC * KPI)
+#define NODES (32 * R)
+#define NC (R * G)                 /* warps; warp 0 also feeds the pipeline */
+#define NTHR (32 * NC)
+
+extern __shared__ __align__(1024) double sm[];
+#define XS (sm)
+#define MS (sm + 2 * XBUF)
+#define KS (sm + 2 * XBUF + 2 * MBUF)
+#define REDSEP (sm + 2 * XBUF + 2 * MBUF + S * KSTG)
+#define BARS ((unsigned long long*)(REDSEP + (RED_ALIAS ? 0 : (G - 1) * NT * NODES)))
+#define KFULL(i) (BARS + (i))
+#define KEMPTY(i) (BARS + S + (i))
+#define XFULL(i) (BARS + 2 * S + (i))
+#define XEMPTY(i) (BARS + 2 * S + 2 + (i))
+__constant__ double gcoef[NCOEF];
+
+__device__ __forceinline__ unsigned su(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp8(double* s, const double* g, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(su(s)), "l"(g), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void bulk(double* s, const double* g, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(su(s)), "l"(g), "r"(bytes), "r"(su(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned n) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" :: "r"(su(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" :: "r"(su(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {  // release: prior reads done
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(su(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W_%=;\n}"
+               :: "r"(su(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" :: "n"(NC * 32) : "memory"); }
+
+__device__ __forceinline__ void tile_coords(const SgOpArgs& A, int t, int& tx, int& ty, int& it) {
+  const int tile = blockIdx.x + t * gridDim.x;
+  tx = tile % A.tiles_x, ty = (tile / A.tiles_x) % A.tiles_y, it = tile / (A.tiles_x * A.tiles_y);
+}
+
+// x tile and M block of tile t into buffer t & 1 (two bulk copies, lane 0).
+__device__ __forceinline__ void load_xm(const SgOpArgs& A, int t, int lane) {
+  if (lane != 0) return;
+  if (t >= 2) mbar_wait(XEMPTY(t & 1), (unsigned)((t >> 1) - 1) & 1u);
+  const ll tile = blockIdx.x + t * gridDim.x;
+  mbar_expect_tx(XFULL(t & 1), (unsigned)((XBUF + MPI) * 8));
+  bulk(XS + (t & 1) * XBUF, A.xt + tile * XBUF, XBUF * 8, XFULL(t & 1));
+  bulk(MS + (t & 1) * MBUF, A.M + tile * MPI, MPI * 8, XFULL(t & 1));
+}
+
+// K chunk q (stage q % S) of this CTA: IC input terms of its tile q / NCHUNK.
+// K is stored tile by tile ([tile][i][KPI]): one contiguous bulk copy, issued
+// by lane 0 of warp 0 once every warp has released the stage's previous use.
+__device__ __forceinline__ const double* k_chunk(const SgOpArgs& A, int q, unsigned& bytes) {
+  const int t = q / NCHUNK, ch = q % NCHUNK;
+  bytes = (unsigned)(min(IC, NIN - ch * IC) * KPI * 8);
+  return A.K + ((ll)(blockIdx.x + t * gridDim.x) * NIN + (ll)ch * IC) * KPI;
+}
+__device__ __forceinline__ void issue_k(const SgOpArgs& A, int q, int nst, int lane) {
+  if (lane != 0) return;
+  if (q + PF < nst) {  // L2 prefetch PF chunks beyond the ring: HBM latency under load is ~4 us
+    unsigned b;
+    const double* src = k_chunk(A, q + PF, b);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(b) : "memory");
+  }
+  if (q >= nst) return;
+  if (q >= S) mbar_wait(KEMPTY(q % S), (unsigned)((q / S) - 1) & 1u);
+  unsigned bytes;
+  const double* src = k_chunk(A, q, bytes);
+  mbar_expect_tx(KFULL(q % S), bytes);
+  bulk(KS + (q % S) * KSTG, src, bytes, KFULL(q % S));
+}
+
+// shared-memory reads of the current tile: x (center at [ly+1][lane+1]);
+// K of input term ii: own diag / E / N, west neighbour's E, south neighbour's N;
+// M likewise plus own NE and the south-west neighbour's NE
+#define XV(j, dy, dx) xb[((j) * (R + 2) + ly + 1 + (dy)) * XW + lane + 1 + (dx)]
+#define K_D(ii) kb[(ii) * KPI + ly * 32 + lane]
+#define K_E(ii) kb[(ii) * KPI + KOE + ly * 33 + lane + 1]
+#define K_W(ii) kb[(ii) * KPI + KOE + ly * 33 + lane]
+#define K_N(ii) kb[(ii) * KPI + KON + (ly + 1) * 32 + lane]
+#define K_S(ii) kb[(ii) * KPI + KON + ly * 32 + lane]
+// warp 0 feeds the ring S - 2 chunks ahead (and the next tile's x / M at
+// mid-tile), then every warp waits for its chunk
+#define STAGE_IN(ch)                                                   \
+  if (warp == 0) {                                                     \
+    issue_k(A, s + S - 2, nst, lane);                                  \
+    if ((ch) == NCHUNK / 2 && t + 1 < mytiles) load_xm(A, t + 1, lane); \
+    __syncwarp();                                                      \
+  }                                                                    \
+  mbar_wait(KFULL(s % S), (unsigned)(s / S) & 1u);                     \
+  kb = KS + (s % S) * KSTG;
+#define STAGE_OUT()                                                    \
+  __syncwarp();                                                        \
+  if (lane == 0) mbar_arrive(KEMPTY(s % S));                           \
+  ++s;
+
+@GROUPS@
+
+extern "C" __global__ void __launch_bounds__(NTHR, 1) sgop_kernel(const SgOpArgs A) {
+  const int ntiles = A.tiles_x * A.tiles_y * A.items;
+  if ((int)blockIdx.x >= ntiles) return;
+  const int mytiles = (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nst = mytiles * NCHUNK;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(KFULL(i), 1), mbar_init(KEMPTY(i), NC);
+    for (int i = 0; i < 2; ++i) mbar_init(XFULL(i), 1), mbar_init(XEMPTY(i), NC);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0)
+      for (int q = 0; q < PF; ++q)
+        if (q < nst) {
+          unsigned b;
+          const double* src = k_chunk(A, q, b);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(b) : "memory");
+        }
+    for (int q = 0; q < S - 2; ++q) issue_k(A, q, nst, lane);
+    load_xm(A, 0, lane);
+    __syncwarp();
+  }
+  const int ly = warp / G, gq = warp % G;
+  @DISPATCH@
+}
+)CUDA";
+
+std::string dlit(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  std::string s(b);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
+}
+}  // namespace
+
+struct SgOpJit {
+  int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255;
+  bool red_alias = true;  // partial sums reuse the tile's x buffer (after the mass step)
+  size_t smem = 0;
+  std::vector<double> coef;  // c_ijk in generated order (__constant__ gcoef)
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  ~SgOpJit() {
+    if (lib) cudaLibraryUnload(lib);
+  }
+};
+
+// shared memory: x tiles (2), M tiles (2), K ring (S stages), partial-sum buffer
+static long long sgop_smem_doubles(const SgOpJit& J) {
+  const long long xw = 34;
+  auto up = [](long long v) { return (v + 15) / 16 * 16; };
+  const long long kpi = (97LL * J.R + 33) / 2 * 2, mpi = (130LL * J.R + 66) / 2 * 2;
+  return 2 * up(J.NT * (J.R + 2) * xw) + 2 * up(mpi) + J.S * up((long long)J.IC * kpi) +
+         (J.red_alias ? 0 : (long long)(J.G - 1) * J.NT * 32 * J.R) + 2 * J.S + 4;  // + barriers
+}
+
+// CUDA source of the operator specialised for (NT, NIN, T); fills J's shape.
+std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
+  J->NT = NT, J->NIN = NIN;
+  // <= 7 input terms (35 neighbourhood values) per thread; threads per CTA
+  // bounded by the register file (estimate: x and y live values + 40) and
+  // the shared memory by the tile height R
+  // <= 10 input terms per thread; the tile height R from the register file
+  // (estimate: x and y live values + 60); then as many K stages as the
+  // shared memory holds (bytes in flight set the achievable HBM rate)
+  J->G = (NT + 9) / 10;
+  if (const char* e = std::getenv("SGW_SGOP_G")) J->G = std::max(1, std::atoi(e));  // tuning hook
+  if (J->G > 6) return std::string();  // larger PCE bases: the generic kernel (step.cu)
+  const int jg = (NT + J->G - 1) / J->G, est = 2 * (5 * jg + NT) + 80;
+  J->IC = NIN >= 48 ? 12 : NIN >= 24 ? 4 : 2;
+  if (const char* e = std::getenv("SGW_SGOP_IC")) J->IC = std::max(1, std::atoi(e));  // tuning hook
+  J->NCHUNK = (NIN + J->IC - 1) / J->IC;
+  J->R = std::max(1, std::min(16, 65536 / est / (32 * J->G)));
+  if (const char* e = std::getenv("SGW_SGOP_R")) J->R = std::max(1, std::atoi(e));  // tuning hook
+  const long long budget = 220 * 1024 / 8;
+  for (;; --J->R) {
+    J->red_alias = (long long)(J->G - 1) * NT * 32 * J->R <= (long long)NT * (J->R + 2) * 34;
+    J->S = 3;
+    if (sgop_smem_doubles(*J) <= budget || J->R == 1) break;
+  }
+  while (J->S < 12 && J->S <= J->NCHUNK) {
+    ++J->S;
+    if (sgop_smem_doubles(*J) > budget) {
+      --J->S;
+      break;
+    }
+  }
+  if (const char* e = std::getenv("SGW_SGOP_S")) J->S = std::max(3, std::atoi(e));  // tuning hook
+  J->regs = std::min(255, (65536 / (32 * J->R * J->G)) & ~7);
+  const int R = J->R, G = J->G, IC = J->IC;
+  // full (i, j) -> [(k, c)] expansion of the j <= k tensor (pce.hpp:24-40)
+  std::map<std::pair<int, int>, std::vector<std::pair<int, double>>> pairs;
+  for (size_t e = 0; e < T.v.size(); ++e) {
+    pairs[{T.i[e], T.j[e]}].push_back({T.k[e], T.v[e]});
+    if (T.j[e] != T.k[e]) pairs[{T.i[e], T.k[e]}].push_back({T.j[e], T.v[e]});
+  }
+  // j groups balanced by work (5 FMAs per pair + 1 per coefficient)
+  std::vector<long long> wj(NT, 0);
+  for (auto& p : pairs) wj[p.first.second] += 5 + (long long)p.second.size();
+  std::vector<int> order(NT), grp(NT, 0);
+  for (int j = 0; j < NT; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return wj[a] > wj[b]; });
+  std::vector<long long> load(G, 0);
+  for (int j : order) {
+    const int g = int(std::min_element(load.begin(), load.end()) - load.begin());
+    grp[j] = g;
+    load[g] += wj[j] + 7;
+  }
+  // timing experiment only (SGW_SGOP_DBG=1): stream and synchronise, skip the stencil math
+  const bool dbg_nomath = std::getenv("SGW_SGOP_DBG") && std::atoi(std::getenv("SGW_SGOP_DBG")) >= 1;
+  // generated per-group tile loops
+  std::string groups, dispatch = "switch (gq) {\n";
+  for (int g = 0; g < G; ++g) {
+    std::vector<int> js;
+    for (int j = 0; j < NT; ++j)
+      if (grp[j] == g) js.push_back(j);
+    std::string c;
+    c += "__device__ __forceinline__ void group" + std::to_string(g) +
+         "(const SgOpArgs& A, int ly, int lane, int warp, int mytiles, int nst) {\n";
+    c += "  int s = 0;\n  for (int t = 0; t < mytiles; ++t) {\n";
+    c += "    const int tile = blockIdx.x + t * gridDim.x;\n";
+    c += "    const int tx = tile % A.tiles_x, ty = (tile / A.tiles_x) % A.tiles_y, it = tile / (A.tiles_x * A.tiles_y);\n";
+    c += "    double* xb = XS + (t & 1) * XBUF;\n    const double* mb = MS + (t & 1) * MBUF;\n";
+    c += "    const double* kb;\n    (void)tx, (void)ty;\n";
+    for (int ch = 0; ch < J->NCHUNK; ++ch) {
+      if (ch == 0)  // x / M of this tile
+        c += "    mbar_wait(XFULL(t & 1), (unsigned)(t >> 1) & 1u);\n";
+      c += "    STAGE_IN(" + std::to_string(ch) + ");\n";
+      if (ch == 0) {
+        for (int j : js) {
+          const std::string J0 = std::to_string(j);
+          c += "    const double x" + J0 + "c = XV(" + J0 + ", 0, 0), x" + J0 + "e = XV(" + J0 + ", 0, 1), x" + J0 +
+               "w = XV(" + J0 + ", 0, -1), x" + J0 + "n = XV(" + J0 + ", 1, 0), x" + J0 + "s = XV(" + J0 +
+               ", -1, 0);\n";
+        }
+        for (int k = 0; k < NT; ++k) c += "    double y" + std::to_string(k) + " = 0.0;\n";
+      }
+      for (int i = ch * IC; i < std::min(NIN, (ch + 1) * IC); ++i) {
+        std::string body;
+        for (int j : js) {
+          auto it = pairs.find({i, j});
+          if (it == pairs.end()) continue;
+          const std::string J0 = std::to_string(j);
+          body += "      { const double v = fma(kd, x" + J0 + "c, ke * x" + J0 + "e) + fma(kw, x" + J0 +
+                  "w, fma(kn, x" + J0 + "n, ks * x" + J0 + "s));\n";
+          for (auto& kc : it->second) {
+            body += "        y" + std::to_string(kc.first) + " = fma(gcoef[" + std::to_string(J->coef.size()) +
+                    "], v, y" + std::to_string(kc.first) + ");\n";
+            J->coef.push_back(kc.second);
+          }
+          body += "      }\n";
+        }
+        if (body.empty() || dbg_nomath) continue;
+        const std::string ii = std::to_string(i - ch * IC);
+        c += "    {\n      const double kd = K_D(" + ii + "), ke = K_E(" + ii + "), kw = K_W(" + ii + "), kn = K_N(" + ii +
+             "), ks = K_S(" + ii + ");\n" + body + "    }\n";
+      }
+      c += "    STAGE_OUT();\n";
+    }
+    // mass on own terms, then the fixed-order sum of the G partials
+    c += "    const double md = mb[ly * 32 + lane], me = mb[KOE + ly * 33 + lane + 1], mw = mb[KOE + ly * 33 + lane], "
+         "mn = mb[MON + (ly + 1) * 32 + lane], ms_ = mb[MON + ly * 32 + lane], mne = mb[MONE + (ly + 1) * 33 + lane + 1], "
+         "msw = mb[MONE + ly * 33 + lane];\n";
+    c += "    const int gx = tx * 32 + lane, gy = ty * R + ly;\n";
+    c += "    const bool valid = gx < A.W && gy < A.H;\n";
+    for (int k : js) {
+      const std::string K0 = std::to_string(k);
+      c += "    double m" + K0 + " = fma(md, x" + K0 + "c, fma(me, x" + K0 + "e, fma(mw, x" + K0 + "w, fma(mn, x" + K0 +
+           "n, fma(ms_, x" + K0 + "s, fma(mne, XV(" + K0 + ", 1, 1), msw * XV(" + K0 + ", -1, -1)))))));\n";
+    }
+    for (int k : js) c += "    double q" + std::to_string(k) + " = 0.0;\n";
+    c += "    if (A.x2 && valid) {\n      const double* x2 = A.x2 + it * A.xitem + (ll)gy * A.xpitch + gx;\n";
+    c += "      const bool hw = gx > 0, he = gx + 1 < A.W, hs = gy > 0, hn = gy + 1 < A.H;\n";
+    for (int k : js) {
+      const std::string K0 = std::to_string(k);
+      c += "      { const double* p = x2 + " + K0 + " * A.xterm;\n";
+      c += "        double q = md * p[0];\n        if (he) q = fma(me, p[1], q);\n        if (hw) q = fma(mw, p[-1], q);\n";
+      c += "        if (hn) q = fma(mn, p[A.xpitch], q);\n        if (hs) q = fma(ms_, p[-A.xpitch], q);\n";
+      c += "        if (hn && he) q = fma(mne, p[A.xpitch + 1], q);\n        if (hs && hw) q = fma(msw, p[-A.xpitch - 1], q);\n";
+      c += "        q" + K0 + " = q; }\n";
+    }
+    c += "    }\n";
+    c += J->red_alias ? "    consumers_sync();  // everyone is done with xb (mass step) / red (previous tile)\n    double* red = xb;\n"
+                      : "    consumers_sync();  // red of the previous tile is read\n    double* red = REDSEP;\n";
+    if (G > 1) {
+      for (int k = 0; k < NT; ++k) {
+        if (grp[k] == g) continue;
+        const int slot = g < grp[k] ? g : g - 1;
+        c += "    red[(" + std::to_string(slot) + " * NT + " + std::to_string(k) + ") * NODES + ly * 32 + lane] = y" +
+             std::to_string(k) + ";\n";
+      }
+    }
+    c += "    consumers_sync();\n    if (valid) {\n      double* yo = A.y + it * A.yitem + (ll)gy * A.ypitch + gx;\n";
+    for (int k : js) {
+      const std::string K0 = std::to_string(k);
+      std::string sum;
+      for (int w = 0; w < G; ++w) {
+        std::string term = w == g ? "y" + K0
+                                  : "red[(" + std::to_string(w < g ? w : w - 1) + " * NT + " + K0 +
+                                        ") * NODES + ly * 32 + lane]";
+        sum = sum.empty() ? term : "(" + sum + " + " + term + ")";
+      }
+      c += "      yo[" + K0 + " * A.yterm] = fma(A.beta, " + sum + ", fma(A.alpha, m" + K0 + ", A.gamma * q" + K0 + "));\n";
+    }
+    c += "    }\n    __syncwarp();\n    if (lane == 0) mbar_arrive(XEMPTY(t & 1));  // x / M (and red) buffer free\n  }\n}\n";
+    groups += c;
+    dispatch += "    case " + std::to_string(g) + ": group" + std::to_string(g) + "(A, ly, lane, warp, mytiles, nst); break;\n";
+  }
+  dispatch += "  }";
+  int pf = 0;  // measured: L2 prefetch beyond the ring does not help here
+  if (const char* e = std::getenv("SGW_SGOP_PF")) pf = std::max(0, std::atoi(e));  // tuning hook
+  std::string src = "#define PF " + std::to_string(pf) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
+                    "\n#define NT " + std::to_string(NT) + "\n#define NIN " + std::to_string(NIN) +
+                    "\n#define R " + std::to_string(R) + "\n#define G " + std::to_string(G) + "\n#define IC " +
+                    std::to_string(IC) + "\n#define S " + std::to_string(J->S) + "\n#define NCHUNK " +
+                    std::to_string(J->NCHUNK) + "\n" + kDeviceTemplate;
+  src.replace(src.find("@GROUPS@"), 8, groups);
+  src.replace(src.find("@DISPATCH@"), 10, dispatch);
+  if (const char* dump = std::getenv("SGW_SGOP_DUMP")) {
+    if (FILE* f = std::fopen(dump, "w")) {
+      std::fputs(src.c_str(), f);
+      std::fclose(f);
+    }
+  }
+  return src;
+}
+
+std::shared_ptr<SgOpJit> build_sgop(int NT, int NIN, const TensorHost& T) {
+  auto J = std::make_shared<SgOpJit>();
+  const std::string src = sgop_source(NT, NIN, T, J.get());
+  if (src.empty()) return nullptr;
+  const int R = J->R, G = J->G, IC = J->IC;
+  // compile for sm_100a
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "sgop.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    throw Error(4, "nvrtcCreateProgram failed");
+  const std::string regs = "--maxrregcount=" + std::to_string(J->regs);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true", regs.c_str()};
+  const nvrtcResult rc = nvrtcCompileProgram(prog, 5, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    nvrtcDestroyProgram(&prog);
+    throw Error(4, "SG operator JIT compile failed: " + log.substr(0, 2000));
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::string cubin(n, '\0');
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  SGW_CUDA(cudaLibraryLoadData(&J->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+  SGW_CUDA(cudaLibraryGetKernel(&J->kern, J->lib, "sgop_kernel"));
+  (void)R, (void)G, (void)IC;
+  J->smem = size_t(sgop_smem_doubles(*J)) * 8;
+  if (!J->coef.empty()) {  // c_ijk into the module's constant bank
+    void* dptr = nullptr;
+    size_t bytes = 0;
+    SGW_CUDA(cudaLibraryGetGlobal(&dptr, &bytes, J->lib, "gcoef"));
+    if (bytes < J->coef.size() * sizeof(double)) throw Error(4, "SG operator: coefficient table size mismatch");
+    SGW_CUDA(cudaMemcpy(dptr, J->coef.data(), J->coef.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  SGW_CUDA(cudaFuncSetAttribute((const void*)J->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)J->smem));
+  return J;
+}
+
+int sgop_rows(const SgOpJit& J) { return J.R; }
+
+// x in the caller's layout -> [tile][NT][R+2][34] (the tile, one halo node
+// around it; zeros outside the grid), each tile's block 128-byte aligned
+__global__ void sgop_pack_x_kernel(const double* __restrict__ x, double* __restrict__ xt, long long xterm,
+                                   long long xitem, int xpitch, int W, int H, int R, int NT, int tiles_x, int tiles_y,
+                                   long long ntiles, long long xbuf) {
+  const long long per = (long long)NT * (R + 2) * 34;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ntiles * per;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long tile = e / per;
+    const int w = int(e % per), j = w / ((R + 2) * 34), rr = (w / 34) % (R + 2), cc = w % 34;
+    const int tx = int(tile % tiles_x), ty = int((tile / tiles_x) % tiles_y), it = int(tile / ((long long)tiles_x * tiles_y));
+    const int gy = ty * R - 1 + rr, gx = tx * 32 - 1 + cc;
+    double v = 0.0;
+    if (gy >= 0 && gy < H && gx >= 0 && gx < W) v = __ldg(x + it * xitem + j * xterm + (long long)gy * xpitch + gx);
+    xt[tile * xbuf + w] = v;
+  }
+}
+
+long long sgop_xt_doubles(const SgOpJit& J, const SgOpArgs& a) {
+  const long long xbuf = ((long long)J.NT * (J.R + 2) * 34 + 15) / 16 * 16;
+  return (long long)a.tiles_x * a.tiles_y * a.items * xbuf;
+}
+
+void sgop_tile_stencils(const SgOpJit& J, const double* K, const double* M, int W, int H, int items, int nin,
+                        std::vector<double>& kt, std::vector<double>& mt, SgOpArgs& a) {
+  const int R = J.R, tx_n = (W + 31) / 32, ty_n = (H + R - 1) / R;
+  const long long kpi = (97LL * R + 33) / 2 * 2, mpi = (130LL * R + 66) / 2 * 2, plane = (long long)W * H;
+  const long long ntiles = (long long)tx_n * ty_n * items;
+  kt.assign(ntiles * nin * kpi, 0.0);
+  mt.assign(ntiles * mpi, 0.0);
+  auto at = [&](const double* P, long long pl, int r, int c) {
+    return (r >= 0 && r < H && c >= 0 && c < W) ? P[pl * plane + (long long)r * W + c] : 0.0;
+  };
+  for (long long tile = 0; tile < ntiles; ++tile) {
+    const int tx = int(tile % tx_n), ty = int((tile / tx_n) % ty_n), it = int(tile / ((long long)tx_n * ty_n));
+    const int r0 = ty * R, c0 = tx * 32;
+    for (int i = 0; i < nin; ++i) {
+      double* d = &kt[(tile * nin + i) * kpi];
+      const long long pl = ((long long)it * nin + i) * 3;
+      for (int rr = 0; rr < R; ++rr)
+        for (int cc = 0; cc < 32; ++cc) d[rr * 32 + cc] = at(K, pl, r0 + rr, c0 + cc);
+      for (int rr = 0; rr < R; ++rr)
+        for (int cc = 0; cc < 33; ++cc) d[32 * R + rr * 33 + cc] = at(K, pl + 1, r0 + rr, c0 - 1 + cc);
+      for (int rr = 0; rr <= R; ++rr)
+        for (int cc = 0; cc < 32; ++cc) d[65 * R + rr * 32 + cc] = at(K, pl + 2, r0 - 1 + rr, c0 + cc);
+    }
+    double* m = &mt[tile * mpi];
+    const long long pm = (long long)it * 4;
+    for (int rr = 0; rr < R; ++rr)
+      for (int cc = 0; cc < 32; ++cc) m[rr * 32 + cc] = at(M, pm, r0 + rr, c0 + cc);
+    for (int rr = 0; rr < R; ++rr)
+      for (int cc = 0; cc < 33; ++cc) m[32 * R + rr * 33 + cc] = at(M, pm + 1, r0 + rr, c0 - 1 + cc);
+    for (int rr = 0; rr <= R; ++rr)
+      for (int cc = 0; cc < 32; ++cc) m[65 * R + rr * 32 + cc] = at(M, pm + 2, r0 - 1 + rr, c0 + cc);
+    for (int rr = 0; rr <= R; ++rr)
+      for (int cc = 0; cc < 33; ++cc) m[97 * R + 32 + rr * 33 + cc] = at(M, pm + 3, r0 - 1 + rr, c0 - 1 + cc);
+  }
+  a.W = W, a.H = H, a.tiles_x = tx_n, a.tiles_y = ty_n, a.items = items;
+}
+
+void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st) {
+  const int tiles = a.tiles_x * a.tiles_y * a.items;
+  {
+    const long long xbuf = ((long long)J.NT * (J.R + 2) * 34 + 15) / 16 * 16;
+    const long long tot = (long long)tiles * J.NT * (J.R + 2) * 34;
+    sgop_pack_x_kernel<<<(unsigned)std::min<long long>((tot + 255) / 256, 8 * kNumSMs * 4), 256, 0, st>>>(
+        a.x, const_cast<double*>(a.xt), a.xterm, a.xitem, a.xpitch, a.W, a.H, J.R, J.NT, a.tiles_x, a.tiles_y, tiles,
+        xbuf);
+    SGW_LAUNCHED();
+  }
+  const int grid = std::max(1, std::min(tiles, kNumSMs));
+  void* args[] = {const_cast<SgOpArgs*>(&a)};
+  SGW_CUDA(cudaLaunchKernel((const void*)J.kern, dim3(grid), dim3(32 * J.R * J.G), args, J.smem, st));
+  SGW_LAUNCHED();
+}
+
+}  // namespace sgw

@@ -28,6 +28,27 @@ namespace sgw {
 
 struct SweepLayout;
 
+// Arguments of the JIT-compiled SG operator (sgop.cu); identical layout to the
+// device-side struct in the generated source.
+struct SgOpArgs {
+  const double *K, *M;  // tiled stencils (sgop_tile_stencils)
+  const double* xt;     // tiled input scratch (sgop_xt_doubles), packed by launch_sgop
+  const double *x, *x2;
+  double* y;
+  long long xterm, xitem, yterm, yitem;
+  int W, H, xpitch, ypitch, tiles_x, tiles_y, items;
+  double alpha, beta, gamma;
+};
+struct SgOpJit;
+std::shared_ptr<SgOpJit> build_sgop(int NT, int NIN, const TensorHost& T);
+void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st);
+int sgop_rows(const SgOpJit& J);
+long long sgop_xt_doubles(const SgOpJit& J, const SgOpArgs& a);
+// Tile-major copies of grid stencils K [item][i][3][H][W], M [item][4][H][W]
+// (row-major, pitch W) in the operator's tile order; sets a.tiles_x/tiles_y.
+void sgop_tile_stencils(const SgOpJit& J, const double* K, const double* M, int W, int H, int items, int nin,
+                        std::vector<double>& kt, std::vector<double>& mt, SgOpArgs& a);
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -229,6 +250,10 @@ class GpuSolver {
   DBuf<double> gk_v, gp_v;
   // stencils
   DBuf<double> Kg, Mg, Kl, Ml;
+  // tiled global stencils and the JIT SG operator (sgop.cu)
+  DBuf<double> Kp_, Mp_, Xt_;
+  SgOpArgs sgop_args_{};  // global-grid operator: stencils, shapes and TMA maps
+  std::shared_ptr<SgOpJit> sgop_;
   // geometry maps
   DBuf<int> lid_to_p;           // [s * nl + lid]
   DBuf<int> iface_pos;          // per subdomain local p -> global iface pos, flat with ip_off

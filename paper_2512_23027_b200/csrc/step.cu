@@ -79,15 +79,24 @@ __global__ void sg_apply_global_kernel(const double* __restrict__ Kg, const doub
   }
 }
 
+// op 0 (mass only, the initial-acceleration CG) reads no K: the simple kernel;
+// ops 1 / 2 stream every K_i: the JIT-specialised fused operator (sgop.cu).
 void GpuSolver::apply_block(int op, const double* x, double* y) {
   const double cm = op == 0 ? 1.0 : op == 1 ? 0.0 : P.mass_scale;
   const double ck = op == 0 ? 0.0 : op == 1 ? 1.0 : P.stiff_scale;
-  const long long total = (long long)NSTATE;
   cudaEvent_t e0;
   KP.begin(K_SGOP, st_, &e0);
-  sg_apply_global_kernel<<<std::min(cdiv(total, 256), 8 * kNumSMs * 16), 256, 0, st_>>>(
-      Kg.p, Mg.p, n, P.nx - 1, P.ny - 1, NT, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, x, y, cm, ck);
-  SGW_LAUNCHED();
+  if (op == 0 || !sgop_) {
+    const long long total = (long long)NSTATE;
+    sg_apply_global_kernel<<<std::min(cdiv(total, 256), 8 * kNumSMs * 16), 256, 0, st_>>>(
+        Kg.p, Mg.p, n, P.nx - 1, P.ny - 1, NT, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, x, y, cm, ck);
+    SGW_LAUNCHED();
+  } else {
+    SgOpArgs a = sgop_args_;
+    a.x = x, a.x2 = nullptr, a.y = y;
+    a.alpha = cm, a.beta = ck, a.gamma = 0.0;
+    launch_sgop(*sgop_, a, st_);
+  }
   KP.end(st_);
 }
 

@@ -125,7 +125,11 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   double* stage = reinterpret_cast<double*>(smraw);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw + (size_t)S * kTileD * 8);
   unsigned long long* empty = full + 8;
-  double* vv = reinterpret_cast<double*>(empty + 8);  // y_k (forward) / s_k (backward), zero padded to VL
+  // ticket: stream position a stage currently holds.  Warps consume different
+  // positions, so a fast warp may reach a stage a full ring ahead of the tile
+  // it holds; a parity wait alone would then match the previous phase.
+  volatile int* ticket = reinterpret_cast<volatile int*>(empty + 8);
+  double* vv = reinterpret_cast<double*>(empty + 12);  // y_k (forward) / s_k (backward), zero padded to VL
   double* tv = vv + VL;                                 // t_k (forward) / x_k (backward)
   double* bv = tv + VL;                                 // right-hand side block: b_{k+1} / y_k
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   // b_0, read before the first cluster barrier: afterwards peers store y_0 over it
   for (int c = tid; c < B; c += kSwThreads) tv[c] = __ldcg(xs + c);
   if (tid == 0) {
+    for (int i = 0; i < 8; ++i) ticket[i] = -1;
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
         if (lane == 0) {
           const int4 d = __ldg(tt + __ldg(&sch[p].x));
           const unsigned bytes = unsigned((d.z >> 16) * (d.z & 0xffff)) * 8u;
+          ticket[st] = int(pos);  // stage st now belongs to position pos (its previous tile is released)
           mbar_expect_tx(&full[st], bytes);
           tma_bulk_load(stage + (size_t)st * kTileD, base + d.x, bytes, &full[st]);
         }
@@ -236,6 +242,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
 #pragma unroll
         for (int r = 0; r < kTile; ++r) acc[r] = 0.0;
         c0 = c1 = c2 = c3 = 0.0;
+      }
+      while (ticket[st] != int(gp)) {
       }
       mbar_wait(&full[st], unsigned(gp / S) & 1u);
       if (!trans) {  // row sums: acc[r] += T[r][2l..2l+1] . vec[64J + 2l..]
@@ -470,7 +478,7 @@ void destroy_sweep_layout(SweepLayout* p) { delete p; }
 
 size_t GpuSolver::sweep_smem_bytes() const {
   const SweepLayout& L = *sweep_layout_;
-  return (size_t)L.stages * kTileD * 8 + 16 * 8 + 3 * (size_t)L.VL * 8;
+  return (size_t)L.stages * kTileD * 8 + 16 * 8 + 4 * 8 + 3 * (size_t)L.VL * 8;
 }
 
 void GpuSolver::sweep(double* x) {

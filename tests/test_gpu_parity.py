@@ -32,9 +32,13 @@ def relerr(a, b):
 
 
 @pytest.mark.parametrize("op", ["mass", "stiffness", "transient"])
-def test_apply_block_matches_oracle(gpu, op):
-    # sg.cpp:425-447 vs the oracle; test_sg.cpp:51-73 tolerance 1e-12
-    g, c = pair(12, 2, 2, 0.3, 0.5, 2, 4, 2, 1e-3)
+@pytest.mark.parametrize("cfg", [(12, 2, 4, 2), (40, 3, 2, 3), (70, 3, 3, 3), (20, 4, 2, 3)])
+def test_apply_block_matches_oracle(gpu, op, cfg):
+    # sg.cpp:425-447 vs the oracle; test_sg.cpp:51-73 tolerance 1e-12.  The
+    # JIT-specialised operator at 1, 2 and 3 threads per node (P+1 = 6, 20, 35),
+    # grids that are not multiples of the 32 x R tile.
+    nx, L, pin, pout = cfg
+    g, c = pair(nx, 2, 2, 0.3, 0.5, L, pin, pout, 1e-3)
     x = rand(g.n_terms * g.n_dofs, 1)
     a = getattr(g, f"apply_block_{op}")(x)
     b = c.apply_block(x, op)
