@@ -285,6 +285,31 @@ void GpuSolver::build_maps() {
   ng_d.upload(ng_);
   nr_d.upload(nr_);
   nc_d.upload(nc_);
+  // node lists of the per-step coupling kernels: interface nodes, and interior
+  // nodes with an interface neighbour (7-point pattern incl. NE / SW)
+  {
+    std::vector<int> il, al;
+    const int w = G.mx + 1;
+    for (int s = 0; s < ns; ++s) {
+      const auto& sd = G.sub[s];
+      for (int lid : sd.iface_lid) il.push_back(s * G.nl + lid);
+      for (int lid = 0; lid < G.nl; ++lid) {
+        if (sd.lid_to_p[lid] != -2) continue;
+        const int i0 = lid % w, j0 = lid / w;
+        bool adj = false;
+        for (int dj = -1; dj <= 1 && !adj; ++dj)
+          for (int di = -1; di <= 1 && !adj; ++di) {
+            const int i2 = i0 + di, j2 = j0 + dj;
+            if ((di == 1 && dj == -1) || (di == -1 && dj == 1)) continue;  // no NW / SE couplings
+            if (i2 < 0 || j2 < 0 || i2 >= w || j2 >= G.my + 1) continue;
+            adj = sd.lid_to_p[j2 * w + i2] >= 0;
+          }
+        if (adj) al.push_back(s * G.nl + lid);
+      }
+    }
+    ilist_.upload(il), alist_.upload(al);
+    n_ilist_ = (long long)il.size(), n_alist_ = (long long)al.size();
+  }
   // inverse maps, ascending s (fixed reduction order of src/dd.cpp:151-155)
   std::vector<int> icnt(G.n_iface, 0), is(4 * G.n_iface, 0), ip(4 * G.n_iface, 0);
   std::vector<int> ccnt(G.n_corner, 0), cs(4 * std::max(1, G.n_corner), 0), cc(4 * std::max(1, G.n_corner), 0);
@@ -457,6 +482,7 @@ void GpuSolver::build_device_inputs(const Stencils& stc) {
     a.xpitch = a.ypitch = P.nx - 1;
     Xt_.alloc(sgop_xt_doubles(*sgop_, a));
     a.xt = Xt_.p;
+    yglob_.alloc(NSTATE);
   }
 }
 

@@ -251,7 +251,10 @@ class GpuSolver {
   // stencils
   DBuf<double> Kg, Mg, Kl, Ml;
   // tiled global stencils and the JIT SG operator (sgop.cu)
-  DBuf<double> Kp_, Mp_, Xt_;
+  DBuf<double> Kp_, Mp_, Xt_, yglob_;
+  // (s * nl + lid) lists: interface nodes, interior nodes next to the interface
+  DBuf<int> ilist_, alist_;
+  long long n_ilist_ = 0, n_alist_ = 0;
   SgOpArgs sgop_args_{};  // global-grid operator: stencils, shapes and TMA maps
   std::shared_ptr<SgOpJit> sgop_;
   // geometry maps

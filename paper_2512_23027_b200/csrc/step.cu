@@ -120,10 +120,18 @@ __device__ __forceinline__ long long interior_index(const LocalArgs& A, int s, i
 __global__ void local_force_kernel(LocalArgs A, int n, const double* __restrict__ um, const double* __restrict__ uc,
                                    double a0, double a1, const double* __restrict__ fnext, int fdof, double fval,
                                    const double* __restrict__ iface_w, const int* __restrict__ ip_off,
-                                   double* __restrict__ yI, double* __restrict__ fG, int ns) {
-  const long long total = (long long)ns * A.nl * A.nt;
+                                   double* __restrict__ yI, double* __restrict__ fG, int ns,
+                                   const int* __restrict__ list, long long nlist) {
+  // all local nodes, or only the (s * nl + lid) entries of `list`
+  const long long total = list ? nlist * A.nt : (long long)ns * A.nl * A.nt;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
+    int lid, k, s;
+    if (list) {
+      const int e = list[t / A.nt];
+      s = e / A.nl, lid = e % A.nl, k = int(t % A.nt);
+    } else {
+      lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
+    }
     const int cls = A.lid_to_p[(long long)s * A.nl + lid];
     if (cls == -1) continue;  // Dirichlet node
     const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
@@ -174,10 +182,16 @@ __global__ void local_force_kernel(LocalArgs A, int n, const double* __restrict_
 __global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict__ yI, const double* __restrict__ fG,
                                 const double* __restrict__ uLI, const int* __restrict__ ip_off,
                                 const int* __restrict__ iface_lid, double* __restrict__ outLI,
-                                double* __restrict__ outI, int ns) {
-  const long long total = (long long)ns * A.nl * A.nt;
+                                double* __restrict__ outI, int ns, const int* __restrict__ list, long long nlist) {
+  const long long total = list ? nlist * A.nt : (long long)ns * A.nl * A.nt;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
+    int lid, k, s;
+    if (list) {
+      const int e = list[t / A.nt];
+      s = e / A.nl, lid = e % A.nl, k = int(t % A.nt);
+    } else {
+      lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
+    }
     const int cls = A.lid_to_p[(long long)s * A.nl + lid];
     if (mode == 0 ? cls < 0 : cls != -2) continue;
     const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
@@ -427,6 +441,28 @@ void GpuSolver::gather_state(double* dst) {
   allreduce(dst, NSTATE);
 }
 
+// Interior rows of the local force from the global operator: the stencil of a
+// subdomain-interior node only touches that subdomain's elements, so its local
+// row equals the global row (f_ext added on term 0, weight 1).
+__global__ void interior_from_global_kernel(LocalArgs A, int n, const double* __restrict__ yg,
+                                            const double* __restrict__ fnext, int fdof, double fval,
+                                            double* __restrict__ yI, int ns) {
+  const long long total = (long long)ns * A.H * A.B;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int row = int(t % A.B), jl = int((t / A.B) % A.H) + 1, s = int(t / ((long long)A.B * A.H));
+    const int il = row / A.nt + 1, k = row % A.nt;
+    const int lid = jl * (A.mx + 1) + il;
+    if (A.lid_to_p[(long long)s * A.nl + lid] != -2) continue;  // unit row of a ragged block
+    const int d = lid_dof(A, s, il, jl);
+    double f = yg[(long long)k * n + d];
+    if (k == 0) {
+      if (fnext) f += fnext[d];
+      else if (d == fdof) f += fval;
+    }
+    yI[t] = f;
+  }
+}
+
 int GpuSolver::step(int* iters_out) {
   const long long N = (long long)NSTATE;
   const int grid = std::min(cdiv(N, 256), 8 * kNumSMs * 8);
@@ -437,13 +473,35 @@ int GpuSolver::step(int* iters_out) {
   const double* fvec = force_at(t_now + P.dt, step_index + 1, &fval);
   const LocalArgs A = local_args();
   const long long tl = (long long)NS * G.nl * NT;
-  local_force_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(
-      A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, force_kind_ == 1 ? force_dof_ : -1, fval, iface_w.p, ip_off.p,
-      yI.p, fG.p, NS);
+  const int fdof = force_kind_ == 1 ? force_dof_ : -1;
+  const long long ti = (long long)n_ilist_ * NT, ta = (long long)n_alist_ * NT;
+  if (sgop_) {
+    // interior rows: f = M um + a0 M uc + a1 sum c K uc on the global grid (JIT
+    // operator), copied into the block rows; interface rows: local stencils
+    SgOpArgs sa = sgop_args_;
+    sa.x = uc.p, sa.x2 = um.p, sa.y = yglob_.p;
+    sa.alpha = P.alpha0, sa.beta = P.alpha1, sa.gamma = 1.0;
+    {
+      cudaEvent_t e0;
+      KP.begin(K_SGOP, st_, &e0);
+      launch_sgop(*sgop_, sa, st_);
+      KP.end(st_);
+    }
+    const long long tI = (long long)NS * G.H * B;
+    interior_from_global_kernel<<<std::min(cdiv(tI, 256), 65535), 256, 0, st_>>>(A, n, yglob_.p, fvec, fdof, fval,
+                                                                                   yI.p, NS);
+    SGW_LAUNCHED();
+    local_force_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+        A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, yI.p, fG.p, NS, ilist_.p,
+        n_ilist_);
+  } else {
+    local_force_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(
+        A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, yI.p, fG.p, NS, nullptr, 0);
+  }
   SGW_LAUNCHED();
   sweep(yI.p);  // y = A_II^-1 f_I
-  coupling_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(A, 0, yI.p, fG.p, nullptr, ip_off.p,
-                                                                   iface_lid_.p, li_y.p, nullptr, NS);
+  coupling_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+      A, 0, yI.p, fG.p, nullptr, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
   SGW_LAUNCHED();
   scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
   allreduce(vb.p, NG);
@@ -454,9 +512,13 @@ int GpuSolver::step(int* iters_out) {
     throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
   cudaEventRecord(ev_[4], st_);
   gather_li(vx.p, li_x.p, false);
-  coupling_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(A, 1, nullptr, nullptr, li_x.p, ip_off.p,
-                                                                   iface_lid_.p, nullptr, wI.p, NS);
-  SGW_LAUNCHED();
+  // A_IG u_G is non-zero only on interior nodes next to the interface
+  SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
+  if (n_alist_ > 0) {
+    coupling_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
+        A, 1, nullptr, nullptr, li_x.p, ip_off.p, iface_lid_.p, nullptr, wI.p, NS, alist_.p, n_alist_);
+    SGW_LAUNCHED();
+  }
   sweep(wI.p);  // A_II^-1 A_IG u_G
   update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
                                        P.ny, G.px, G.py, G.H, B, G.s0, NS, P.dt, P.zeta, P.gamma);

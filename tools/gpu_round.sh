@@ -17,4 +17,8 @@ timeout 900 ncu --set full --clock-control none --import-source on --profile-fro
 echo "sweep rc=$?" >> gpurun_out/plain.log
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -k regex:pcg_fused -c 1 -o gpurun_out/prof_pcg $CMD > gpurun_out/ncu_pcg.log 2>&1
-echo "pcg rc=$?" >> gpurun_out/plain.log
+echo "rc=$?" >> gpurun_out/plain.log
+timeout 600 python tools/sgop_bench.py C2 5 > gpurun_out/sgop_plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgop_kernel -s 2 -c 1 \
+    -o gpurun_out/prof_sgop python tools/sgop_bench.py C2 5 > gpurun_out/ncu_sgop.log 2>&1
+echo "rc=$?" >> gpurun_out/plain.log
