@@ -389,8 +389,25 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   const Stencils stc = build_stencils(P, G, true);
   build_device_inputs(stc);
   build_maps();
-  setup_interior_and_schur();
-  setup_nn2();
+  // setup in batches of subdomains sized so the dense temporaries (A_II block
+  // factor, L^-1 blocks, S_s, the rolling L^-1 A_IG) stay within ~24 GB
+  B = G.W * NT;
+  amax_ = 0;
+  for (int s = 0; s < NS; ++s) amax_ = std::max(amax_, NT * ng_[s]);
+  plan_nn2();
+  build_sweep_layout();
+  {
+    const double per = 8.0 * (3.0 * G.H * double(B) * B + double(amax_) * amax_ + 2.0 * double(B) * amax_);
+    int nb = std::max(1, std::min(NS, int(24e9 / per)));
+    if (const char* e = std::getenv("SGW_SETUP_BATCH")) nb = std::max(1, std::atoi(e));  // test hook
+    std::vector<double> fcc((size_t)NC * NC, 0.0);
+    for (int b0 = 0; b0 < NS; b0 += nb) {
+      const int cnt = std::min(nb, NS - b0);
+      setup_interior_and_schur(b0, cnt);
+      nn2_batch(b0, cnt, fcc);
+    }
+    finish_nn2(fcc);
+  }
 
   // work vectors
   for (DBuf<double>* b : {&u, &v, &a, &um, &uc, &unext}) b->alloc(NSTATE), b->zero(st_);
@@ -487,10 +504,14 @@ void GpuSolver::build_device_inputs(const Stencils& stc) {
 }
 
 // -------------------------------------------------- interior and Schur -----
-void GpuSolver::setup_interior_and_schur() {
-  const int H = G.H, W = G.W, ns = NS;
-  B = W * NT;
-  SetupArgs A{Kl.p, Ml.p, gp_ptr.p, gp_i.p, gp_v.p, lid_to_p.p, ng_d.p, G.nl, NIN, NT, G.mx, G.my, W, H, B,
+// Subdomains [b0, b0 + nb): dense per-batch temporaries (block Cholesky of A_II,
+// L^-1 blocks, the local Schur S_s), then the factor tiles go to Fcomp and S_s
+// to Sdense_ (batch-local) for nn2_batch.  Batched cuSOLVER / cuBLAS calls per
+// grid row k over the batch.
+void GpuSolver::setup_interior_and_schur(int b0, int nb) {
+  const int H = G.H, W = G.W, ns = nb, amax = amax_;
+  SetupArgs A{Kl.p + (size_t)b0 * NIN * 3 * G.nl, Ml.p + (size_t)b0 * 4 * G.nl, gp_ptr.p, gp_i.p, gp_v.p,
+              lid_to_p.p + (size_t)b0 * G.nl, ng_d.p + b0, G.nl, NIN, NT, G.mx, G.my, W, H, B,
               P.mass_scale, P.stiff_scale};
   const size_t BB = size_t(B) * B;
   DBuf<double> D;
@@ -503,49 +524,57 @@ void GpuSolver::setup_interior_and_schur() {
     assemble_ii_kernel<<<std::min(cdiv(tot, 256), 65535), 256, 0, st_>>>(A, D.p, Lsub.p, ns);
     SGW_LAUNCHED();
   }
+  Linv.alloc(size_t(ns) * H * BB);
+  set_identity_kernel<<<std::min(cdiv((long long)ns * H * BB, 256), 65535), 256, 0, st_>>>(Linv.p, B, ns * H);
+  SGW_LAUNCHED();
+  // pointer tables [k][s] for the batched calls
+  std::vector<double*> hD(size_t(H) * ns), hL(size_t(H) * ns), hI(size_t(H) * ns);
+  for (int k = 0; k < H; ++k)
+    for (int q = 0; q < ns; ++q) {
+      hD[size_t(k) * ns + q] = D.p + (size_t(q) * H + k) * BB;
+      hL[size_t(k) * ns + q] = k < H - 1 ? Lsub.p + (size_t(q) * (H - 1) + k) * BB : nullptr;
+      hI[size_t(k) * ns + q] = Linv.p + (size_t(q) * H + k) * BB;
+    }
+  DBuf<double*> pD, pL, pI;
+  pD.upload(hD), pL.upload(hL), pI.upload(hI);
   // block Cholesky over grid rows (src/sg.cpp:218-225 restated block-wise)
-  DBuf<double> work;
   DBuf<int> info;
   info.alloc(size_t(ns) * H);
   info.zero(st_);
-  int lw = 0;
-  SGW_SOLVER(cusolverDnDpotrf_bufferSize(sol_, CUBLAS_FILL_MODE_LOWER, B, D.p, B, &lw));
-  work.alloc(std::max(lw, 1));
   const double one = 1.0, mone = -1.0;
   for (int k = 0; k < H; ++k) {
     if (k > 0)
       SGW_BLAS(cublasDgemmStridedBatched(blas_, CUBLAS_OP_N, CUBLAS_OP_T, B, B, B, &mone, Lsub.p + (k - 1) * BB, B,
                                          (long long)(H - 1) * BB, Lsub.p + (k - 1) * BB, B, (long long)(H - 1) * BB,
                                          &one, D.p + k * BB, B, (long long)H * BB, ns));
-    for (int s = 0; s < ns; ++s) {
-      double* Dk = D.p + (size_t(s) * H + k) * BB;
-      SGW_SOLVER(cusolverDnDpotrf(sol_, CUBLAS_FILL_MODE_LOWER, B, Dk, B, work.p, (int)work.n, info.p + s * H + k));
-      if (k < H - 1)
-        SGW_BLAS(cublasDtrsm(blas_, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, B, B,
-                             &one, Dk, B, Lsub.p + (size_t(s) * (H - 1) + k) * BB, B));
-    }
+    SGW_SOLVER(cusolverDnDpotrfBatched(sol_, CUBLAS_FILL_MODE_LOWER, B, pD.p + size_t(k) * ns, B, info.p + size_t(k) * ns,
+                                       ns));
+    if (k < H - 1)
+      SGW_BLAS(cublasDtrsmBatched(blas_, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, B,
+                                  B, &one, pD.p + size_t(k) * ns, B, pL.p + size_t(k) * ns, B, ns));
   }
   {
     std::vector<int> h(info.n);
     SGW_CUDA(cudaMemcpyAsync(h.data(), info.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
     SGW_CUDA(cudaStreamSynchronize(st_));
-    for (int s = 0; s < ns; ++s)
-      for (int k = 0; k < H; ++k)
-        if (h[s * H + k] != 0)
-          throw Error(2, "stochastic interior factorization failed (subdomain " + std::to_string(s) + ")");
+    for (int k = 0; k < H; ++k)
+      for (int q = 0; q < ns; ++q)
+        if (h[size_t(k) * ns + q] != 0)
+          throw Error(2, "stochastic interior factorization failed (subdomain " + std::to_string(G.s0 + b0 + q) + ")");
   }
   // S_s = A_GG - Y^T Y, Y = L^-1 A_IG by rolling block forward substitution
-  int amax = 0;
-  for (int s = 0; s < ns; ++s) amax = std::max(amax, NT * ng_[s]);
   Sdense_.alloc(size_t(ns) * amax * amax);
   Sdense_.zero(st_);
-  amax_ = amax;
-  assemble_gg_kernel<<<dim3(cdiv(amax, 128), ns), 128, 0, st_>>>(A, ip_off.p, iface_lid_.p, Sdense_.p, amax, ns);
+  assemble_gg_kernel<<<dim3(cdiv(amax, 128), ns), 128, 0, st_>>>(A, ip_off.p + b0, iface_lid_.p, Sdense_.p, amax, ns);
   SGW_LAUNCHED();
   DBuf<double> R, Y;
   R.alloc(size_t(ns) * B * amax);
   Y.alloc(size_t(ns) * B * amax);
   const long long sRY = (long long)B * amax, sS = (long long)amax * amax;
+  std::vector<double*> hR(ns), hY(ns);
+  for (int q = 0; q < ns; ++q) hR[q] = R.p + q * sRY, hY[q] = Y.p + q * sRY;
+  DBuf<double*> pR, pY;
+  pR.upload(hR), pY.upload(hY);
   for (int k = 0; k < H; ++k) {
     R.zero(st_);
     assemble_rhs_kernel<<<cdiv((long long)ns * B, 256), 256, 0, st_>>>(A, k, R.p, amax, ns);
@@ -553,38 +582,32 @@ void GpuSolver::setup_interior_and_schur() {
     if (k > 0)
       SGW_BLAS(cublasDgemmStridedBatched(blas_, CUBLAS_OP_N, CUBLAS_OP_N, B, amax, B, &mone, Lsub.p + (k - 1) * BB, B,
                                          (long long)(H - 1) * BB, Y.p, B, sRY, &one, R.p, B, sRY, ns));
-    for (int s = 0; s < ns; ++s)
-      SGW_BLAS(cublasDtrsm(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B, amax,
-                           &one, D.p + (size_t(s) * H + k) * BB, B, R.p + s * sRY, B));
+    SGW_BLAS(cublasDtrsmBatched(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B,
+                                amax, &one, pD.p + size_t(k) * ns, B, pR.p, B, ns));
     SGW_BLAS(cublasDgemmStridedBatched(blas_, CUBLAS_OP_T, CUBLAS_OP_N, amax, amax, B, &mone, R.p, B, sRY, R.p, B, sRY,
                                        &one, Sdense_.p, amax, sS, ns));
     std::swap(R.p, Y.p);
+    std::swap(pR.p, pY.p);
   }
   R.reset();
   Y.reset();
   // Linv_kk = L_kk^-1 (exact zeros above the diagonal) for the per-step sweeps
-  Linv.alloc(size_t(ns) * H * BB);
-  set_identity_kernel<<<std::min(cdiv((long long)ns * H * BB, 256), 65535), 256, 0, st_>>>(Linv.p, B, ns * H);
-  SGW_LAUNCHED();
-  for (int s = 0; s < ns; ++s)
-    for (int k = 0; k < H; ++k)
-      SGW_BLAS(cublasDtrsm(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B, B,
-                           &one, D.p + (size_t(s) * H + k) * BB, B, Linv.p + (size_t(s) * H + k) * BB, B));
-  SGW_CUDA(cudaStreamSynchronize(st_));
+  for (int k = 0; k < H; ++k)
+    SGW_BLAS(cublasDtrsmBatched(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B, B,
+                                &one, pD.p + size_t(k) * ns, B, pI.p + size_t(k) * ns, B, ns));
   D.reset();
-  build_compact_factor();
+  compact_factor_batch(b0, nb);
 }
 
 // ------------------------------------------------------------ NN2 data -----
 // src/dd.cpp:98-140: S_rr, S_rc, S_cc; Q = S_rr^-1 (explicit), Psi = Q S_rc,
 // F_cc = sum_s B_s^T (S_cc - S_rc^T Psi) B_s assembled in ascending s.
-void GpuSolver::setup_nn2() {
-  const int ns = NS, nt = NT, amax = amax_;
+void GpuSolver::plan_nn2() {
+  const int ns = NS, nt = NT;
   std::vector<int> dimsS(ns), dimsQ(ns);
   for (int s = 0; s < ns; ++s) dimsS[s] = nt * ng_[s], dimsQ[s] = nt * nr_[s];
   Sp.plan(dimsS);
   Qp.plan(dimsQ);
-  for (int s = 0; s < ns; ++s) pack_tiles_range(Sp, s, Sdense_.p + size_t(s) * amax * amax, amax, st_);
   roff_ = Qp.xoff;
   d_roff.upload(roff_);
   psioff_.assign(ns + 1, 0);
@@ -612,13 +635,18 @@ void GpuSolver::setup_nn2() {
   c_f.alloc(std::max<long long>(1, coff_[ns])), c_d.alloc(std::max<long long>(1, coff_[ns]));
   dcoarse.alloc(std::max(1, NC)), ucoarse.alloc(std::max(1, NC));
   ucoarse.zero(st_);
-  // per subdomain: extract, invert, Psi, local coarse block
+}
+
+// Subdomains [b0, b0 + nb) with S_s in Sdense_ (batch-local): S tiles, and per
+// subdomain extract, invert, Psi, local coarse block (accumulated into fcc).
+void GpuSolver::nn2_batch(int b0, int nb, std::vector<double>& fcc) {
+  const int nt = NT, amax = amax_;
+  for (int q = 0; q < nb; ++q) pack_tiles_range(Sp, b0 + q, Sdense_.p + size_t(q) * amax * amax, amax, st_);
   DBuf<double> Srr, Src, Scc, work;
   DBuf<int> ri, ci, info;
   info.alloc(1);
-  std::vector<double> fcc((size_t)NC * NC, 0.0);
   const double one = 1.0, zero = 0.0, mone = -1.0;
-  for (int s = 0; s < ns; ++s) {
+  for (int s = b0; s < b0 + nb; ++s) {
     const auto& sd = G.sub[s];
     const int a = nt * ng_[s], rs = nt * nr_[s], cs = nt * nc_[s];
     std::vector<int> hr, hc;
@@ -629,7 +657,7 @@ void GpuSolver::setup_nn2() {
     (void)a;
     ri.upload(hr);
     ci.upload(hc);
-    const double* Ss = Sdense_.p + size_t(s) * amax * amax;
+    const double* Ss = Sdense_.p + size_t(s - b0) * amax * amax;
     if (rs > 0) {
       Srr.alloc((size_t)rs * rs);
       extract_kernel<<<cdiv((long long)rs * rs, 256), 256, 0, st_>>>(Ss, amax, ri.p, rs, ri.p, rs, Srr.p);
@@ -661,6 +689,13 @@ void GpuSolver::setup_nn2() {
         }
     }
   }
+  Sdense_.reset();
+}
+
+void GpuSolver::finish_nn2(std::vector<double>& fcc) {
+  DBuf<double> work;
+  DBuf<int> info;
+  info.alloc(1);
   if (NC > 0 && comm_) {  // F_cc = sum over all ranks' subdomains (dd.cpp:128-137)
     Finv.upload(fcc);
     allreduce(Finv.p, fcc.size());
@@ -672,7 +707,6 @@ void GpuSolver::setup_nn2() {
     Finv.upload(fcc);
     spd_inverse(sol_, st_, Finv.p, NC, work, info, "coarse F_cc");
   }
-  Sdense_.reset();
   SGW_CUDA(cudaStreamSynchronize(st_));
 }
 

@@ -226,8 +226,10 @@ class GpuSolver {
   }
   DBuf<double> own_mask_;  // sharded: 1 on dofs this rank owns (Geometry::owner_of_dof), per term
   void build_device_inputs(const Stencils& st);
-  void setup_interior_and_schur();
-  void setup_nn2();
+  void setup_interior_and_schur(int b0, int nb);
+  void plan_nn2();
+  void nn2_batch(int b0, int nb, std::vector<double>& fcc);
+  void finish_nn2(std::vector<double>& fcc);
   void build_maps();
   void sweep(double* x);  // x <- A_II^-1 x (block-row layout, all subdomains)
   void gather_li(const double* glob, double* li, bool weighted);
@@ -287,7 +289,8 @@ class GpuSolver {
   DBuf<int> sw_off, sw_cs, sw_cuts, sw_ncut;
   int sweep_cs_ = 1;
   SweepLayout* sweep_layout_ = nullptr;
-  void build_compact_factor();
+  void build_sweep_layout();
+  void compact_factor_batch(int b0, int nb);
   size_t sweep_smem_bytes() const;
   // persistent cooperative PCG (pcg_fused.cu)
   void setup_fused_pcg();

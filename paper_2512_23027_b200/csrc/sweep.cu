@@ -50,6 +50,7 @@ struct SweepLayout {
   const int* nsched;     // [rank * T_N + type]
   long long sub_off, blk, per_sub;  // SUB tiles inside a block row; block-row stride; per subdomain
   int B, H, nb, VL, stages;
+  int n_inv, n_all;  // tile-table sizes (host side: compaction)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -355,7 +356,7 @@ __global__ void compact_factor_kernel(const double* __restrict__ Linv_d, const d
   }
 }
 
-void GpuSolver::build_compact_factor() {
+void GpuSolver::build_sweep_layout() {
   const int H = G.H, nb = (B + kTile - 1) / kTile;
   if (B > kPre * kSwWarps * 32) throw Error(1, "interior block too large for the sweep kernel");
   // L_{k+1,k}: row r is zero left of c0(r) = (node(r) - 1)(P+1)
@@ -448,15 +449,25 @@ void GpuSolver::build_compact_factor() {
   L.sub_off = sub_off, L.blk = blk, L.per_sub = (long long)H * blk;
   L.B = B, L.H = H, L.nb = nb, L.VL = nb * kTile;
   L.stages = 5;
+  L.n_inv = n_inv, L.n_all = (int)tabs.size();
   delete sweep_layout_;
   sweep_layout_ = new SweepLayout(L);
   Fcomp.alloc(size_t(NS) * L.per_sub);
+  const size_t smem = sweep_smem_bytes();
+  for (auto fn : {(const void*)sweep_kernel<1>, (const void*)sweep_kernel<2>, (const void*)sweep_kernel<4>,
+                  (const void*)sweep_kernel<8>})
+    SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+// factor blocks of subdomains [b0, b0 + nb) (batch-local Linv / Lsub) -> tiles
+void GpuSolver::compact_factor_batch(int b0, int nb) {
+  const SweepLayout& L = *sweep_layout_;
   DBuf<unsigned long long> drop;
   drop.alloc(1);
   drop.zero(st_);
-  TileTabs T{reinterpret_cast<const int4*>(sw_off.p), n_inv, (int)tabs.size()};
-  compact_factor_kernel<<<8 * kNumSMs * 4, 256, 0, st_>>>(Linv.p, Lsub.p, Fcomp.p, T, sw_cs.p, sub_off, blk, B, H, NS,
-                                                           drop.p);
+  TileTabs T{L.tiles[0], L.n_inv, L.n_all};
+  compact_factor_kernel<<<8 * kNumSMs * 4, 256, 0, st_>>>(Linv.p, Lsub.p, Fcomp.p + (size_t)b0 * L.per_sub, T, sw_cs.p,
+                                                           L.sub_off, L.blk, L.B, L.H, nb, drop.p);
   SGW_LAUNCHED();
   unsigned long long h = 0;
   SGW_CUDA(cudaMemcpyAsync(&h, drop.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
@@ -468,10 +479,6 @@ void GpuSolver::build_compact_factor() {
   }
   Linv.reset();
   Lsub.reset();
-  const size_t smem = sweep_smem_bytes();
-  for (auto fn : {(const void*)sweep_kernel<1>, (const void*)sweep_kernel<2>, (const void*)sweep_kernel<4>,
-                  (const void*)sweep_kernel<8>})
-    SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
 void destroy_sweep_layout(SweepLayout* p) { delete p; }

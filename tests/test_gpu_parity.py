@@ -149,6 +149,23 @@ def test_interior_sweep_every_cluster_size(gpu, monkeypatch, cs):
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
 
 
+@pytest.mark.parametrize("batch", ["1", "5"])
+def test_setup_in_subdomain_batches(gpu, monkeypatch, batch):
+    # the setup processes subdomains in batches (memory bound at C3+); any batch
+    # size gives the oracle's operators and trajectory
+    monkeypatch.setenv("SGW_SETUP_BATCH", batch)
+    nx = 24
+    g, c = pair(nx, 4, 3, 0.3, 0.5, 2, 3, 2, 2e-3)
+    x = rand(g.n_global, 17)
+    assert relerr(g.schur().matvec(x), c.schur_matvec(x)) <= 1e-10
+    assert relerr(g.schur().apply_nn2(x), c.apply_nn2(x)) <= 1e-10
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 5)
+    hc = c.run(u0, 0 * u0, 5, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
 @pytest.mark.parametrize("cs", ["2", "4"])
 def test_sweep_multi_tile_blocks_reproducible(gpu, monkeypatch, cs):
     # interior blocks of several 64x64 tiles (B = 47 x 6 = 282: 5 tile rows),
