@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-shard", action="store_true",
+                    help="test hook: the sharded code path (NCCL communicator) even on one rank")
     ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
                     help="N>1: shard the subdomains over the ranks (one problem, NCCL sums) or run N replicas")
     args = ap.parse_args()
@@ -178,7 +180,7 @@ def main():
     import paper_2512_23027_b200 as sg
 
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.force_shard:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
@@ -188,7 +190,7 @@ def main():
     coeff = sg.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
     tensor = sg.triple_products(c["L"], c["p_in"], c["p_out"])
     node = sg.nearest_node(nx, nx, 0.5, 0.5)
-    shard = world > 1 and args.mode == "shard"
+    shard = (world > 1 and args.mode == "shard") or args.force_shard
     kw = {}
     if shard:  # rank r owns subdomains shard_plan(n_sub, N)[r]; the NCCL id travels over torch.distributed
         ids = [sg.nccl_unique_id() if rank == 0 else None]
@@ -323,7 +325,7 @@ def main():
                                 "s_per_newmark_step": r["s_per_step"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 

@@ -75,7 +75,8 @@ typedef struct sgw_problem {
    * call it with the same arguments.  Results (state, probes, PCG output)
    * are identical on all ranks.
    * nccl_id: 128-byte ncclUniqueId from sgw_nccl_unique_id on rank 0,
-   * broadcast by the caller (e.g. torch.distributed).                      */
+   * broadcast by the caller (e.g. torch.distributed).  A non-NULL id with
+   * world_size 1 runs the sharded code path on a 1-rank communicator.      */
   int rank, world_size;
   const void* nccl_id;
 } sgw_problem;

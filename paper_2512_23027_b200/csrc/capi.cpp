@@ -100,10 +100,8 @@ int sgw_create(const sgw_problem* p, sgw_solver** out) {
     if (!out) throw Error(SGW_EINVAL, "null argument");
     Problem P = problem_from(p);
     std::unique_ptr<Comm> comm;
-    if (P.world > 1) {
-      if (!p->nccl_id) throw Error(SGW_EINVAL, "world_size > 1 needs the NCCL unique id of rank 0");
-      comm = make_nccl_comm(p->nccl_id, P.rank, P.world, P.device);
-    }
+    if (P.world > 1 && !p->nccl_id) throw Error(SGW_EINVAL, "world_size > 1 needs the NCCL unique id of rank 0");
+    if (p->nccl_id) comm = make_nccl_comm(p->nccl_id, P.rank, P.world, P.device);  // also a 1-rank communicator
     auto s = std::make_unique<sgw_solver>();
     s->g = std::make_unique<GpuSolver>(std::move(P), std::move(comm));
     *out = s.release();

@@ -339,9 +339,9 @@ class SgSolver:
         if local_group is not None:
             _check(L.sgw_create_local_group(C.byref(prob), world_size, rank, local_group._g, C.byref(h)))
         else:
-            if world_size > 1:
-                if nccl_id is None or len(nccl_id) != 128:
-                    raise SgInvalidArgument(SGW_EINVAL, "world_size > 1 needs the 128-byte NCCL id of rank 0")
+            if world_size > 1 and (nccl_id is None or len(nccl_id) != 128):
+                raise SgInvalidArgument(SGW_EINVAL, "world_size > 1 needs the 128-byte NCCL id of rank 0")
+            if nccl_id is not None:
                 self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
                 prob.nccl_id = C.cast(self._nccl_id, C.c_void_p)
             _check(L.sgw_create(C.byref(prob), C.byref(h)))

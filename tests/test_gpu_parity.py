@@ -230,6 +230,24 @@ def test_sharded_ranks_match_single_gpu(gpu, world, case):
     grp.close()
 
 
+def test_nccl_one_rank_communicator(gpu):
+    # the NCCL transport of the sharded path (ncclCommInitRank + ncclAllReduce on
+    # the solver stream, host-driven PCG) on a 1-rank communicator
+    nx = 24
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, 2, 3)
+    t = O.triple_products(2, 3, 2)
+    kw = dict(params=sg.NewmarkParams(dt=2e-3), options=sg.SgOptions(tol=1e-10, store_full=True))
+    one = sg.SgSolver(nx, nx, 3, 2, coeff, t, **kw)
+    nc = sg.SgSolver(nx, nx, 3, 2, coeff, t, rank=0, world_size=1, nccl_id=sg.nccl_unique_id(), **kw)
+    x = rand(one.n_global, 3)
+    assert relerr(nc.schur().matvec(x), one.schur().matvec(x)) <= 1e-14
+    assert relerr(nc.schur().apply_nn2(x), one.schur().apply_nn2(x)) <= 1e-12
+    u0 = O.gaussian_pulse(nx, nx)
+    h1, h2 = one.run(u0, 0 * u0, 6), nc.run(u0, 0 * u0, 6)
+    assert np.all(np.abs(h1.iterations - h2.iterations) <= 1)
+    assert np.linalg.norm(h2.full_state - h1.full_state) / np.linalg.norm(h1.full_state) <= 1e-10
+
+
 def test_zero_data_stays_zero(gpu):
     g, _ = pair(8, 2, 2, 0.2, 1.0, 2, 1, 2, 0.05)
     z = np.zeros(81)
