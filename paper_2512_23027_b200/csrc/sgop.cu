@@ -225,10 +225,15 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   // <= 10 input terms per thread; the tile height R from the register file
   // (estimate: x and y live values + 60); then as many K stages as the
   // shared memory holds (bytes in flight set the achievable HBM rate)
-  J->G = (NT + 9) / 10;
-  if (const char* e = std::getenv("SGW_SGOP_G")) J->G = std::max(1, std::atoi(e));  // tuning hook
-  if (J->G > 6) return std::string();  // larger PCE bases: the generic kernel (step.cu)
-  const int jg = (NT + J->G - 1) / J->G, est = 2 * (5 * jg + NT) + 80;
+  // Threads of a node: GJ groups of input terms j (registers: 5 neighbourhood
+  // values per j) times GI interleaved groups of input terms i (shorter code
+  // per thread; with G = 4 every SM sub-partition runs a single code stream).
+  int GJ = (NT + 9) / 10, GI = 1;  // measured at C2: GI = 2 does not help
+  if (const char* e = std::getenv("SGW_SGOP_G")) GJ = std::max(1, std::atoi(e));   // tuning hooks
+  if (const char* e = std::getenv("SGW_SGOP_GI")) GI = std::max(1, std::atoi(e));
+  if (GJ > 6) return std::string();  // larger PCE bases: the generic kernel (step.cu)
+  J->G = GJ * GI;
+  const int jg = (NT + GJ - 1) / GJ, est = 2 * (5 * jg + NT) + 80;
   J->IC = NIN >= 48 ? 12 : NIN >= 24 ? 4 : 2;
   if (const char* e = std::getenv("SGW_SGOP_IC")) J->IC = std::max(1, std::atoi(e));  // tuning hook
   J->NCHUNK = (NIN + J->IC - 1) / J->IC;
@@ -262,10 +267,10 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   std::vector<int> order(NT), grp(NT, 0);
   for (int j = 0; j < NT; ++j) order[j] = j;
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return wj[a] > wj[b]; });
-  std::vector<long long> load(G, 0);
+  std::vector<long long> load(GJ, 0);
   for (int j : order) {
     const int g = int(std::min_element(load.begin(), load.end()) - load.begin());
-    grp[j] = g;
+    grp[j] = g;  // j group; the owner of output k = j is group grp[k] (i group 0)
     load[g] += wj[j] + 7;
   }
   // timing experiment only (SGW_SGOP_DBG=1): stream and synchronise, skip the stencil math
@@ -273,9 +278,11 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   // generated per-group tile loops
   std::string groups, dispatch = "switch (gq) {\n";
   for (int g = 0; g < G; ++g) {
+    const int jgrp = g % GJ, igrp = g / GJ;
+    const bool owner = igrp == 0;  // owns the outputs k of its j group
     std::vector<int> js;
     for (int j = 0; j < NT; ++j)
-      if (grp[j] == g) js.push_back(j);
+      if (grp[j] == jgrp) js.push_back(j);
     std::string c;
     c += "__device__ __forceinline__ void group" + std::to_string(g) +
          "(const SgOpArgs& A, int ly, int lane, int warp, int mytiles, int nst) {\n";
@@ -298,6 +305,7 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
         for (int k = 0; k < NT; ++k) c += "    double y" + std::to_string(k) + " = 0.0;\n";
       }
       for (int i = ch * IC; i < std::min(NIN, (ch + 1) * IC); ++i) {
+        if (i % GI != igrp) continue;
         std::string body;
         for (int j : js) {
           auto it = pairs.find({i, j});
@@ -319,7 +327,8 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
       }
       c += "    STAGE_OUT();\n";
     }
-    // mass on own terms, then the fixed-order sum of the G partials
+    // mass on own terms (owner groups), then the fixed-order sum of the G partials
+    if (owner) {
     c += "    const double md = mb[ly * 32 + lane], me = mb[KOE + ly * 33 + lane + 1], mw = mb[KOE + ly * 33 + lane], "
          "mn = mb[MON + (ly + 1) * 32 + lane], ms_ = mb[MON + ly * 32 + lane], mne = mb[MONE + (ly + 1) * 33 + lane + 1], "
          "msw = mb[MONE + ly * 33 + lane];\n";
@@ -342,18 +351,24 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
       c += "        q" + K0 + " = q; }\n";
     }
     c += "    }\n";
+    } else {
+      c += "    const int gx = tx * 32 + lane, gy = ty * R + ly;\n    (void)gx, (void)gy, (void)it;\n";
+    }
     c += J->red_alias ? "    consumers_sync();  // everyone is done with xb (mass step) / red (previous tile)\n    double* red = xb;\n"
                       : "    consumers_sync();  // red of the previous tile is read\n    double* red = REDSEP;\n";
     if (G > 1) {
       for (int k = 0; k < NT; ++k) {
-        if (grp[k] == g) continue;
-        const int slot = g < grp[k] ? g : g - 1;
+        const int own = grp[k];  // owner group of output k
+        if (own == g) continue;
+        const int slot = g < own ? g : g - 1;
         c += "    red[(" + std::to_string(slot) + " * NT + " + std::to_string(k) + ") * NODES + ly * 32 + lane] = y" +
              std::to_string(k) + ";\n";
       }
     }
-    c += "    consumers_sync();\n    if (valid) {\n      double* yo = A.y + it * A.yitem + (ll)gy * A.ypitch + gx;\n";
+    c += "    consumers_sync();\n";
+    if (owner) c += "    if (valid) {\n      double* yo = A.y + it * A.yitem + (ll)gy * A.ypitch + gx;\n";
     for (int k : js) {
+      if (!owner) break;
       const std::string K0 = std::to_string(k);
       std::string sum;
       for (int w = 0; w < G; ++w) {
@@ -364,7 +379,8 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
       }
       c += "      yo[" + K0 + " * A.yterm] = fma(A.beta, " + sum + ", fma(A.alpha, m" + K0 + ", A.gamma * q" + K0 + "));\n";
     }
-    c += "    }\n    __syncwarp();\n    if (lane == 0) mbar_arrive(XEMPTY(t & 1));  // x / M (and red) buffer free\n  }\n}\n";
+    if (owner) c += "    }\n";
+    c += "    __syncwarp();\n    if (lane == 0) mbar_arrive(XEMPTY(t & 1));  // x / M (and red) buffer free\n  }\n}\n";
     groups += c;
     dispatch += "    case " + std::to_string(g) + ": group" + std::to_string(g) + "(A, ly, lane, warp, mytiles, nst); break;\n";
   }
