@@ -248,6 +248,36 @@ def test_nccl_one_rank_communicator(gpu):
     assert np.linalg.norm(h2.full_state - h1.full_state) / np.linalg.norm(h1.full_state) <= 1e-10
 
 
+def test_nonconvergence_raises(gpu):
+    # sg.cpp:413-416: a step whose interface solve does not converge throws
+    coeff = O.lognormal_coeff(16, 16, 0.3, 0.5, 0.5, 2, 2)
+    g = sg.SgSolver(16, 16, 4, 4, coeff, O.triple_products(2, 2, 2), params=sg.NewmarkParams(dt=1e-3),
+                    options=sg.SgOptions(tol=1e-14, max_iter=1))
+    u0 = O.gaussian_pulse(16, 16)
+    with pytest.raises(sg.SgError) as e:
+        g.run(u0, 0 * u0, 2)
+    assert not isinstance(e.value, ValueError)
+
+
+@pytest.mark.parametrize("cfg", [(4, 2, 2, 1, 1, 0), (6, 3, 2, 1, 2, 0), (8, 1, 4, 2, 2, 1)])
+def test_smallest_meshes_and_single_term(gpu, cfg):
+    # edge cases: one interior node per subdomain (4x4 on 2x2), P+1 = 1
+    # (deterministic limit), strips without cross points (no coarse space)
+    nx, px, py, L, pin, pout = cfg
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, L, pin)
+    t = O.triple_products(L, pin, pout)
+    g = sg.SgSolver(nx, nx, px, py, coeff, t, params=sg.NewmarkParams(dt=1e-2),
+                    options=sg.SgOptions(tol=1e-10, store_full=True))
+    c = O.SgSolver(nx, nx, px, py, coeff, t, dt=1e-2, tol=1e-10)
+    x = rand(g.n_terms * g.n_dofs, 4)
+    assert relerr(g.apply_block_transient(x), c.apply_block(x, "transient")) <= 1e-12
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 4)
+    hc = c.run(u0, 0 * u0, 4, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
 def test_zero_data_stays_zero(gpu):
     g, _ = pair(8, 2, 2, 0.2, 1.0, 2, 1, 2, 0.05)
     z = np.zeros(81)
