@@ -198,6 +198,7 @@ std::string dlit(double v) {
 struct SgOpJit {
   int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255;
   bool red_alias = true;  // partial sums reuse the tile's x buffer (after the mass step)
+  bool jouter = false;    // k-resident code shape (see sgop_source)
   size_t smem = 0;
   std::vector<double> coef;  // c_ijk in generated order (__constant__ gcoef)
   cudaLibrary_t lib = nullptr;
@@ -228,14 +229,24 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   // Threads of a node: GJ groups of input terms j (registers: 5 neighbourhood
   // values per j) times GI interleaved groups of input terms i (shorter code
   // per thread; with G = 4 every SM sub-partition runs a single code stream).
-  int GJ = (NT + 9) / 10, GI = 1;  // measured at C2: GI = 2 does not help
+  // Two code shapes.  "x-resident" (default): a thread keeps the 5-point
+  // neighbourhoods of its j's in registers for the whole tile and streams
+  // K_i.  "k-resident" (SGW_SGOP_MODE=jout): threads keep the stencils of a
+  // chunk of IC input terms in registers and read each x_j neighbourhood
+  // once per chunk from shared memory (fewer registers, more shared-memory
+  // traffic; measured 12% slower at C2).
+  J->jouter = false;
+  if (const char* e = std::getenv("SGW_SGOP_MODE")) J->jouter = std::string(e) == "jout";  // tuning hook
+  int GJ = J->jouter ? 2 : (NT + 9) / 10, GI = 1;
   if (const char* e = std::getenv("SGW_SGOP_G")) GJ = std::max(1, std::atoi(e));   // tuning hooks
   if (const char* e = std::getenv("SGW_SGOP_GI")) GI = std::max(1, std::atoi(e));
+  if (J->jouter) GI = 1;
   if (GJ > 6) return std::string();  // larger PCE bases: the generic kernel (step.cu)
   J->G = GJ * GI;
-  const int jg = (NT + GJ - 1) / GJ, est = 2 * (5 * jg + NT) + 80;
-  J->IC = NIN >= 48 ? 12 : NIN >= 24 ? 4 : 2;
+  J->IC = J->jouter ? 4 : NIN >= 48 ? 12 : NIN >= 24 ? 4 : 2;
   if (const char* e = std::getenv("SGW_SGOP_IC")) J->IC = std::max(1, std::atoi(e));  // tuning hook
+  const int jg = (NT + GJ - 1) / GJ;
+  const int est = J->jouter ? 2 * (5 * J->IC + NT + 5) + 60 : 2 * (5 * jg + NT) + 80;
   J->NCHUNK = (NIN + J->IC - 1) / J->IC;
   J->R = std::max(1, std::min(16, 65536 / est / (32 * J->G)));
   if (const char* e = std::getenv("SGW_SGOP_R")) J->R = std::max(1, std::atoi(e));  // tuning hook
@@ -295,14 +306,47 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
       if (ch == 0)  // x / M of this tile
         c += "    mbar_wait(XFULL(t & 1), (unsigned)(t >> 1) & 1u);\n";
       c += "    STAGE_IN(" + std::to_string(ch) + ");\n";
-      if (ch == 0) {
+      if (ch == 0 && !J->jouter) {
         for (int j : js) {
           const std::string J0 = std::to_string(j);
           c += "    const double x" + J0 + "c = XV(" + J0 + ", 0, 0), x" + J0 + "e = XV(" + J0 + ", 0, 1), x" + J0 +
                "w = XV(" + J0 + ", 0, -1), x" + J0 + "n = XV(" + J0 + ", 1, 0), x" + J0 + "s = XV(" + J0 +
                ", -1, 0);\n";
         }
+      }
+      if (ch == 0)
         for (int k = 0; k < NT; ++k) c += "    double y" + std::to_string(k) + " = 0.0;\n";
+      if (J->jouter) {  // stencils of the chunk in registers, x_j from shared memory
+        const int i0 = ch * IC, i1 = std::min(NIN, (ch + 1) * IC);
+        c += "    {\n";
+        for (int i = i0; i < i1 && !dbg_nomath; ++i) {
+          const std::string I0 = std::to_string(i - i0);
+          c += "    const double k" + I0 + "d = K_D(" + I0 + "), k" + I0 + "e = K_E(" + I0 + "), k" + I0 + "w = K_W(" +
+               I0 + "), k" + I0 + "n = K_N(" + I0 + "), k" + I0 + "s = K_S(" + I0 + ");\n";
+        }
+        for (int j : js) {
+          if (dbg_nomath) break;
+          std::string body;
+          for (int i = i0; i < i1; ++i) {
+            auto it = pairs.find({i, j});
+            if (it == pairs.end()) continue;
+            const std::string I0 = std::to_string(i - i0);
+            body += "      { const double v = fma(k" + I0 + "d, xc, k" + I0 + "e * xe) + fma(k" + I0 + "w, xw, fma(k" + I0 +
+                    "n, xn, k" + I0 + "s * xs));\n";
+            for (auto& kc : it->second) {
+              body += "        y" + std::to_string(kc.first) + " = fma(gcoef[" + std::to_string(J->coef.size()) +
+                      "], v, y" + std::to_string(kc.first) + ");\n";
+              J->coef.push_back(kc.second);
+            }
+            body += "      }\n";
+          }
+          if (body.empty()) continue;
+          const std::string J0 = std::to_string(j);
+          c += "    {\n      const double xc = XV(" + J0 + ", 0, 0), xe = XV(" + J0 + ", 0, 1), xw = XV(" + J0 +
+               ", 0, -1), xn = XV(" + J0 + ", 1, 0), xs = XV(" + J0 + ", -1, 0);\n" + body + "    }\n";
+        }
+        c += "    }\n    STAGE_OUT();\n";
+        continue;
       }
       for (int i = ch * IC; i < std::min(NIN, (ch + 1) * IC); ++i) {
         if (i % GI != igrp) continue;
@@ -336,8 +380,13 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
     c += "    const bool valid = gx < A.W && gy < A.H;\n";
     for (int k : js) {
       const std::string K0 = std::to_string(k);
-      c += "    double m" + K0 + " = fma(md, x" + K0 + "c, fma(me, x" + K0 + "e, fma(mw, x" + K0 + "w, fma(mn, x" + K0 +
-           "n, fma(ms_, x" + K0 + "s, fma(mne, XV(" + K0 + ", 1, 1), msw * XV(" + K0 + ", -1, -1)))))));\n";
+      if (J->jouter)
+        c += "    double m" + K0 + " = fma(md, XV(" + K0 + ", 0, 0), fma(me, XV(" + K0 + ", 0, 1), fma(mw, XV(" + K0 +
+             ", 0, -1), fma(mn, XV(" + K0 + ", 1, 0), fma(ms_, XV(" + K0 + ", -1, 0), fma(mne, XV(" + K0 +
+             ", 1, 1), msw * XV(" + K0 + ", -1, -1)))))));\n";
+      else
+        c += "    double m" + K0 + " = fma(md, x" + K0 + "c, fma(me, x" + K0 + "e, fma(mw, x" + K0 + "w, fma(mn, x" + K0 +
+             "n, fma(ms_, x" + K0 + "s, fma(mne, XV(" + K0 + ", 1, 1), msw * XV(" + K0 + ", -1, -1)))))));\n";
     }
     for (int k : js) c += "    double q" + std::to_string(k) + " = 0.0;\n";
     c += "    if (A.x2 && valid) {\n      const double* x2 = A.x2 + it * A.xitem + (ll)gy * A.xpitch + gx;\n";
