@@ -100,6 +100,8 @@ typedef struct sgw_history {
   double* probe_mean;    /* n_probes x (n_steps + 1)                    */
   double* probe_std;     /* n_probes x (n_steps + 1)                    */
   double* full_state;    /* (n_steps + 1) x (P+1) n_dofs, term-major    */
+  double* probe_coeffs;  /* n_probes x (P+1) x (n_steps + 1): every chaos
+                            coefficient at the probes (SgHistory::probe_coeffs) */
 } sgw_history;
 
 const char* sgw_last_error(void);

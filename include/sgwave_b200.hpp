@@ -13,6 +13,9 @@
 // std::runtime_error, as the reference does.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <functional>
 #include <stdexcept>
 #include <string>
@@ -50,6 +53,7 @@ struct PcgReport {  // pcg.hpp:11-18
 struct SgHistory {  // sg.hpp:21-31
   std::vector<double> times;
   std::vector<Vec> probe_mean, probe_std;  // [probe][step]
+  std::vector<std::vector<Vec>> probe_coeffs;  // [probe][term][step]
   std::vector<Vec> full_state;             // [step] flattened (P+1) n_dofs, if requested
   std::vector<PcgReport> reports;
   double mean_iterations() const {
@@ -223,14 +227,20 @@ class SgSolver {  // sg.hpp:43-98
     std::vector<int> its(n_steps);
     Vec res(n_steps), pm(size_t(np) * (n_steps + 1)), ps(pm.size());
     Vec full(opt_.store_full ? size_t(n_steps + 1) * n_terms_ * n_dofs_ : 0);
+    Vec pc(size_t(np) * n_terms_ * (n_steps + 1));
     sgw_history h{its.data(), res.data(), np, opt_.probe_nodes.data(), pm.data(), ps.data(),
-                  full.empty() ? nullptr : full.data()};
+                  full.empty() ? nullptr : full.data(), pc.empty() ? nullptr : pc.data()};
     detail::check(sgw_run(h_, u0_nodal.data(), v0_nodal.data(), n_steps, &f, &h));
     SgHistory out;
     out.times = times;
     for (int p = 0; p < np; ++p) {
       out.probe_mean.emplace_back(pm.begin() + size_t(p) * (n_steps + 1), pm.begin() + size_t(p + 1) * (n_steps + 1));
       out.probe_std.emplace_back(ps.begin() + size_t(p) * (n_steps + 1), ps.begin() + size_t(p + 1) * (n_steps + 1));
+      out.probe_coeffs.emplace_back();
+      for (int j = 0; j < n_terms_; ++j) {
+        const size_t o = (size_t(p) * n_terms_ + j) * (n_steps + 1);
+        out.probe_coeffs.back().emplace_back(pc.begin() + o, pc.begin() + o + n_steps + 1);
+      }
     }
     const size_t N = size_t(n_terms_) * n_dofs_;
     for (size_t k = 0; !full.empty() && k <= (size_t)n_steps; ++k)
@@ -256,5 +266,73 @@ class SgSolver {  // sg.hpp:43-98
   long long n_dofs_ = 0, n_global_ = 0, n_coarse_ = 0;
   int n_terms_ = 0;
 };
+
+// ------------------------------------------------------------- outputs ---
+// The solve-sg data files (experiments.cpp:393-434, docs/outputs.md:19-30) in
+// the reference's CsvWriter format (%.17g, io.cpp:15-44).  Returns file names.
+inline std::string format_double(double v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+inline std::vector<std::string> write_sg_outputs(const std::string& dir, const SgHistory& h, int nx, int ny,
+                                                 double dt, const std::vector<double>& snapshot_times = {}) {
+  std::vector<std::string> names;
+  auto write = [&](const std::string& name, const std::string& text) {
+    FILE* f = std::fopen((dir + "/" + name).c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write " + dir + "/" + name);
+    std::fwrite(text.data(), 1, text.size(), f);
+    std::fclose(f);
+    names.push_back(name);
+  };
+  auto row = [](std::initializer_list<double> a, const Vec* more = nullptr) {
+    std::string r;
+    for (double v : a) r += (r.empty() ? "" : ",") + format_double(v);
+    if (more)
+      for (double v : *more) r += "," + format_double(v);
+    return r + "\n";
+  };
+  for (size_t p = 0; p < h.probe_mean.size(); ++p) {
+    const size_t nt = p < h.probe_coeffs.size() ? h.probe_coeffs[p].size() : 0;
+    std::string t = "t,mean,std";
+    for (size_t j = 0; j < nt; ++j) t += ",u" + std::to_string(j);
+    t += "\n";
+    for (size_t s = 0; s < h.times.size(); ++s) {
+      Vec c(nt);
+      for (size_t j = 0; j < nt; ++j) c[j] = h.probe_coeffs[p][j][s];
+      t += row({h.times[s], h.probe_mean[p][s], h.probe_std[p][s]}, &c);
+    }
+    write("probe_" + std::to_string(p) + ".csv", t);
+  }
+  if (!h.reports.empty()) {
+    std::string t = "step,iterations,final_residual\n";
+    for (size_t s = 0; s < h.reports.size(); ++s)
+      t += row({double(s + 1), double(h.reports[s].iterations),
+                h.reports[s].residual_history.empty() ? 0.0 : h.reports[s].residual_history.back()});
+    write("iterations.csv", t);
+  }
+  if (!snapshot_times.empty() && !h.full_state.empty()) {
+    const long long n = (long long)(nx - 1) * (ny - 1), nodes = (long long)(nx + 1) * (ny + 1);
+    for (size_t k = 0; k < snapshot_times.size(); ++k) {
+      const int step = std::min<int>((int)h.full_state.size() - 1, (int)std::llround(snapshot_times[k] / dt));
+      const Vec& u = h.full_state[step];
+      const int nt = int(u.size() / n);
+      std::string t = "node_id,x,y,mean,std\n";
+      for (long long i = 0; i < nodes; ++i) {
+        const int gi = int(i % (nx + 1)), gj = int(i / (nx + 1));
+        double mean = 0.0, sd = 0.0;
+        if (gi > 0 && gi < nx && gj > 0 && gj < ny) {  // moments (sg.cpp:17-26), Dirichlet nodes 0
+          const long long d = (long long)(gj - 1) * (nx - 1) + gi - 1;
+          double var = 0.0;
+          for (int j = 1; j < nt; ++j) var += u[j * n + d] * u[j * n + d];
+          mean = u[d], sd = std::sqrt(var);
+        }
+        t += row({double(i), double(gi) / nx, double(gj) / ny, mean, sd});
+      }
+      write("snapshot_" + std::to_string(k) + ".csv", t);
+    }
+  }
+  return names;
+}
 
 }  // namespace sgwave::b200

@@ -21,7 +21,9 @@ from .sgwave import (  # noqa: F401
     lognormal_coeff,
     nccl_unique_id,
     nearest_node,
+    moments,
     ricker,
     shard_plan,
     triple_products,
+    write_sg_outputs,
 )

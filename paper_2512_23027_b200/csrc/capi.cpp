@@ -268,7 +268,7 @@ int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, cons
       std::vector<int> own(np);
       for (int q = 0; q < np; ++q) own[q] = g.G.owner_of_dof(g.probe_dofs[q]) == g.rank();
       g.d_probe_own.upload(own);
-      g.probe_hist.alloc((size_t)(n_steps + 1) * np * 2);
+      g.probe_hist.alloc((size_t)(n_steps + 1) * np * (2 + g.NT));
     }
     set_force(g, force, n_steps + 1);
     DBuf<double> du, dv;
@@ -293,14 +293,18 @@ int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, cons
       }
     }
     if (np) {
-      std::vector<double> ph((size_t)(n_steps + 1) * np * 2);
+      const size_t w = 2 + g.NT, S1 = n_steps + 1;
+      std::vector<double> ph(S1 * np * w);
       SGW_CUDA(cudaMemcpyAsync(ph.data(), g.probe_hist.p, ph.size() * sizeof(double), cudaMemcpyDeviceToHost,
                                g.stream()));
       SGW_CUDA(cudaStreamSynchronize(g.stream()));
       for (int p = 0; p < np; ++p)
-        for (int k = 0; k <= n_steps; ++k) {
-          if (h->probe_mean) h->probe_mean[(size_t)p * (n_steps + 1) + k] = ph[((size_t)k * np + p) * 2];
-          if (h->probe_std) h->probe_std[(size_t)p * (n_steps + 1) + k] = ph[((size_t)k * np + p) * 2 + 1];
+        for (size_t k = 0; k < S1; ++k) {
+          const double* o = &ph[(k * np + p) * w];
+          if (h->probe_mean) h->probe_mean[p * S1 + k] = o[0];
+          if (h->probe_std) h->probe_std[p * S1 + k] = o[1];
+          if (h->probe_coeffs)
+            for (int j = 0; j < g.NT; ++j) h->probe_coeffs[(p * g.NT + j) * S1 + k] = o[2 + j];
         }
     }
   });

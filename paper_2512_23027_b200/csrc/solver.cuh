@@ -214,7 +214,7 @@ class GpuSolver {
   // probes (device history) filled per step
   std::vector<int> probe_dofs;
   DBuf<int> d_probe_dofs, d_probe_own;  // own: sharded runs, probe dof owned by this rank
-  DBuf<double> probe_hist;  // [step][probe][2]: mean, std
+  DBuf<double> probe_hist;  // [step][probe][2 + P+1]: mean, std, u_0 .. u_P
   int probe_cap = 0;
   void record_probes(int step);
   double last_rel = 0.0;  // final true residual of the last PCG solve

@@ -270,9 +270,11 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
 
 __global__ void probe_kernel(const double* __restrict__ u, const int* __restrict__ pd, const int* __restrict__ own,
                              int np, int n, int nt, double* __restrict__ out) {
+  // per probe: mean, std, then every chaos coefficient u_0 .. u_P (sg.cpp:391-405)
   for (int p = threadIdx.x; p < np; p += blockDim.x) {
+    double* o = out + (long long)p * (2 + nt);
     if (own && !own[p]) {  // sharded: the owning rank contributes this probe
-      out[2 * p] = out[2 * p + 1] = 0.0;
+      for (int j = 0; j < 2 + nt; ++j) o[j] = 0.0;
       continue;
     }
     double var = 0.0;
@@ -280,8 +282,9 @@ __global__ void probe_kernel(const double* __restrict__ u, const int* __restrict
       const double c = u[(long long)j * n + pd[p]];
       var += c * c;
     }
-    out[2 * p] = u[pd[p]];
-    out[2 * p + 1] = sqrt(var);
+    o[0] = u[pd[p]];
+    o[1] = sqrt(var);
+    for (int j = 0; j < nt; ++j) o[2 + j] = u[(long long)j * n + pd[p]];
   }
 }
 
@@ -415,11 +418,12 @@ void GpuSolver::init_state(const double* u0_nodal, const double* v0_nodal, doubl
 
 void GpuSolver::record_probes(int k) {
   if (probe_dofs.empty() || k >= probe_cap) return;
-  double* row = probe_hist.p + (size_t)k * probe_dofs.size() * 2;
+  const size_t w = probe_dofs.size() * (2 + NT);
+  double* row = probe_hist.p + (size_t)k * w;
   probe_kernel<<<1, 128, 0, st_>>>(u.p, d_probe_dofs.p, comm_ ? d_probe_own.p : nullptr, (int)probe_dofs.size(), n,
                                    NT, row);
   SGW_LAUNCHED();
-  allreduce(row, probe_dofs.size() * 2);
+  allreduce(row, w);
 }
 
 __global__ void mask_state_kernel(double* __restrict__ x, const double* __restrict__ mask, int n, long long N) {

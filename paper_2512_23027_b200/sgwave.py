@@ -58,7 +58,7 @@ class _Force(C.Structure):
 class _History(C.Structure):
     _fields_ = [("iterations", C.c_void_p), ("residual", C.c_void_p), ("n_probes", C.c_int),
                 ("probe_nodes", C.c_void_p), ("probe_mean", C.c_void_p), ("probe_std", C.c_void_p),
-                ("full_state", C.c_void_p)]
+                ("full_state", C.c_void_p), ("probe_coeffs", C.c_void_p)]
 
 
 def load_library():
@@ -212,9 +212,69 @@ class SgHistory:  # include/sgwave/sg.hpp:23-31
     probe_mean: np.ndarray
     probe_std: np.ndarray
     full_state: np.ndarray | None
+    probe_coeffs: np.ndarray | None = None  # n_probes x (P+1) x (n_steps+1)
 
     def mean_iterations(self):
         return float(self.iterations.mean()) if len(self.iterations) else 0.0
+
+
+def _g17(v) -> str:
+    return "%.17g" % v  # io.cpp:15-19 format_double
+
+
+def _write_csv(path, header, rows):
+    with open(path, "w", newline="") as f:
+        f.write(header + "\n")
+        for r in rows:
+            f.write(",".join(_g17(v) for v in r) + "\n")
+
+
+def moments(flat_state, n_dofs):
+    """sg.cpp:17-26: mean = u_0, std = sqrt(sum_{j>=1} u_j^2) per dof."""
+    u = np.asarray(flat_state, np.float64)
+    nt = u.size // n_dofs
+    var = np.zeros(n_dofs)
+    for j in range(1, nt):
+        var += u[j * n_dofs:(j + 1) * n_dofs] ** 2
+    return u[:n_dofs].copy(), np.sqrt(var)
+
+
+def write_sg_outputs(out_dir, hist: SgHistory, nx, ny, dt, snapshot_times=()):
+    """The `solve-sg` data files (experiments.cpp:393-434, docs/outputs.md:19-30),
+    values in %.17g like CsvWriter (io.cpp:15-44):
+      probe_<k>.csv     t,mean,std,u0..uP       (needs hist.probe_coeffs)
+      iterations.csv    step,iterations,final_residual
+      snapshot_<k>.csv  node_id,x,y,mean,std    (needs hist.full_state)
+    Returns the written file names."""
+    os.makedirs(out_dir, exist_ok=True)
+    names = []
+    pc = hist.probe_coeffs
+    nt = 0 if pc is None or pc.size == 0 else pc.shape[1]
+    for p in range(hist.probe_mean.shape[0]):
+        header = "t,mean,std" + "".join(f",u{j}" for j in range(nt))
+        rows = [[hist.times[s], hist.probe_mean[p, s], hist.probe_std[p, s]] + [pc[p, j, s] for j in range(nt)]
+                for s in range(len(hist.times))]
+        names.append(f"probe_{p}.csv")
+        _write_csv(os.path.join(out_dir, names[-1]), header, rows)
+    if len(hist.iterations):
+        _write_csv(os.path.join(out_dir, "iterations.csv"), "step,iterations,final_residual",
+                   [[s + 1, int(hist.iterations[s]), hist.residual[s]] for s in range(len(hist.iterations))])
+        names.append("iterations.csv")
+    if len(snapshot_times) and hist.full_state is not None:
+        n = (nx - 1) * (ny - 1)
+        nodes = (nx + 1) * (ny + 1)
+        gi, gj = np.arange(nodes) % (nx + 1), np.arange(nodes) // (nx + 1)
+        interior = (gi > 0) & (gi < nx) & (gj > 0) & (gj < ny)
+        dof = np.where(interior, (gj - 1) * (nx - 1) + gi - 1, -1)
+        for k, ts in enumerate(snapshot_times):
+            step = min(len(hist.full_state) - 1, int(np.floor(ts / dt + 0.5)))  # std::llround
+            mean, sd = moments(hist.full_state[step], n)
+            mean_n = np.where(interior, mean[np.maximum(dof, 0)], 0.0)
+            sd_n = np.where(interior, sd[np.maximum(dof, 0)], 0.0)
+            rows = [[i, gi[i] / nx, gj[i] / ny, mean_n[i], sd_n[i]] for i in range(nodes)]
+            names.append(f"snapshot_{k}.csv")
+            _write_csv(os.path.join(out_dir, names[-1]), "node_id,x,y,mean,std", rows)
+    return names
 
 
 class SchurSystem:
@@ -399,12 +459,13 @@ class SgSolver:
         res = np.zeros(n_steps)
         pm = np.zeros((len(probes), n_steps + 1))
         ps = np.zeros_like(pm)
+        pc = np.zeros((len(probes), self.n_terms, n_steps + 1))
         full = np.zeros((n_steps + 1, self.n_terms * self.n_dofs)) if self.options.store_full else None
-        hist = _History(_p(its), _p(res), len(probes), _p(probes), _p(pm), _p(ps), _p(full))
+        hist = _History(_p(its), _p(res), len(probes), _p(probes), _p(pm), _p(ps), _p(full), _p(pc))
         f = (force or ForceSpec())._c()
         _check(load_library().sgw_run(self._h, _p(u0), _p(v0), n_steps, C.byref(f), C.byref(hist)))
         times = np.cumsum(np.r_[0.0, np.full(n_steps, self.params.dt)])
-        return SgHistory(times, its, res, pm, ps, full)
+        return SgHistory(times, its, res, pm, ps, full, pc)
 
     # device-resident stepping (benchmarks)
     def init_state(self, u0_nodal, v0_nodal, force: ForceSpec | None = None):

@@ -7,6 +7,8 @@
 //   test_host_mirror gpu : operator and trajectory parity with the oracle
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <cstring>
 #include <string>
 
@@ -91,6 +93,24 @@ static void cpu_tests() {
   CHECK(throws<std::invalid_argument>([&] { b::SgSolver s({c.nx, c.nx}, {2, 2}, f, bad, 1.0, 0.5, 0.01, p, {}); }));
   b::NewmarkParams p0;  // dt = 0
   CHECK(throws<std::invalid_argument>([&] { b::SgSolver s({c.nx, c.nx}, {2, 2}, f, t, 1.0, 0.5, 0.01, p0, {}); }));
+  // output writers on a synthetic history: CsvWriter format (%.17g), step numbering from 1
+  b::SgHistory h;
+  h.times = {0.0, 0.1, 0.2};
+  h.probe_mean = {{1.0, 0.5, 1.0 / 3.0}};
+  h.probe_std = {{0.0, 0.25, 2.0}};
+  h.probe_coeffs = {{{1.0, 0.5, 1.0 / 3.0}, {0.0, 0.25, -2.0}}};
+  h.reports = {b::PcgReport{3, true, {1.0, 1e-11}}, b::PcgReport{4, true, {1.0, 2.5e-11}}};
+  CHECK(std::system("mkdir -p build/outputs_cpu") == 0);
+  const auto names = b::write_sg_outputs("build/outputs_cpu", h, 4, 4, 0.1);
+  CHECK(names.size() == 2);
+  std::ifstream pf("build/outputs_cpu/probe_0.csv"), itf("build/outputs_cpu/iterations.csv");
+  std::string l0, l1, l2, l3, i0, i1;
+  std::getline(pf, l0), std::getline(pf, l1), std::getline(pf, l2), std::getline(pf, l3);
+  std::getline(itf, i0), std::getline(itf, i1);
+  CHECK(l0 == "t,mean,std,u0,u1");
+  CHECK(l1 == "0,1,0,1,0");
+  CHECK(l3 == "0.20000000000000001,0.33333333333333331,2,0.33333333333333331,-2");
+  CHECK(i0 == "step,iterations,final_residual" && i1 == "1,3,9.9999999999999994e-12");
 }
 
 static void gpu_tests() {
@@ -163,6 +183,18 @@ static void gpu_tests() {
   CHECK(gflat.size() == oflat.size() && rel(gflat, oflat) <= 1e-8);
   CHECK(h.probe_mean.size() == 1 && rel(h.probe_mean[0], pm) <= 1e-8);
   CHECK(h.mean_iterations() > 0.0);
+  // probe chaos coefficients = the state at the probe dof (sg.cpp:391-405)
+  const int pd = (probe / (c.nx + 1) - 1) * (c.nx - 1) + probe % (c.nx + 1) - 1;
+  bool coeff_ok = h.probe_coeffs.size() == 1 && (int)h.probe_coeffs[0].size() == s.n_terms();
+  for (int j = 0; j < s.n_terms() && coeff_ok; ++j)
+    for (int k = 0; k <= steps && coeff_ok; ++k)
+      coeff_ok = h.probe_coeffs[0][j][k] == h.full_state[k][size_t(j) * s.n_dofs() + pd];
+  CHECK(coeff_ok);
+  // solve-sg outputs (experiments.cpp:393-434)
+  const std::string dir = "build/outputs_gpu";
+  CHECK(std::system(("mkdir -p " + dir).c_str()) == 0);
+  const auto names = b::write_sg_outputs(dir, h, c.nx, c.nx, c.dt, {0.004, 0.1});
+  CHECK(names.size() == 4);  // probe_0, iterations, snapshot_0, snapshot_1
   orc_solver_destroy(oh);
 }
 
