@@ -448,7 +448,9 @@ void GpuSolver::build_sweep_layout() {
   L.nsched = sw_ncut.p;
   L.sub_off = sub_off, L.blk = blk, L.per_sub = (long long)H * blk;
   L.B = B, L.H = H, L.nb = nb, L.VL = nb * kTile;
-  L.stages = 5;
+  // ring depth: 6 x 32 KB stages when the shared memory (227 KB) allows (+1% at C2), else 5
+  L.stages = (6LL * kTileD + 3LL * nb * kTile + 20) * 8 <= 227 * 1024 ? 6 : 5;
+  if (const char* e = std::getenv("SGW_SWEEP_STAGES")) L.stages = std::max(2, std::min(8, std::atoi(e)));  // tuning hook
   L.n_inv = n_inv, L.n_all = (int)tabs.size();
   delete sweep_layout_;
   sweep_layout_ = new SweepLayout(L);
