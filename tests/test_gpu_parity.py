@@ -316,3 +316,36 @@ def test_constrained_probe_rejected(gpu):
                     options=sg.SgOptions(probe_nodes=[0]))
     with pytest.raises(ValueError):
         g.run(np.zeros(81), np.zeros(81), 1)
+
+
+@pytest.mark.timeout(1200)
+def test_c2_full_size_parity_and_properties(gpu):
+    # BASELINE configs[1] (C2) at full size: 256x256, 8x8 subdomains, P+1 = 20,
+    # n_in = 84.  Three Newmark steps against the oracle (iterations +-1,
+    # trajectory 1e-8), and size-independent properties of the operators:
+    # symmetry of S and NN2 (test_dd.cpp:77-96), linearity of the SG operator.
+    import bench
+    c = bench.CONFIGS["C2"]
+    nx = c["nx"]
+    coeff = O.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
+    t = O.triple_products(c["L"], c["p_in"], c["p_out"])
+    g = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, t, alpha0=bench.ALPHA0, alpha1=bench.ALPHA1,
+                    params=sg.NewmarkParams(dt=c["dt"]), options=sg.SgOptions(tol=bench.TOL, store_full=True))
+    x, y = rand(g.n_global, 41), rand(g.n_global, 42)
+    S = g.schur()
+    a, b = y @ S.matvec(x), x @ S.matvec(y)
+    assert abs(a - b) <= 1e-11 * abs(b)
+    a, b = y @ S.apply_nn2(x), x @ S.apply_nn2(y)
+    assert abs(a - b) <= 1e-11 * abs(b)
+    u, w = rand(g.n_terms * g.n_dofs, 43), rand(g.n_terms * g.n_dofs, 44)
+    lhs = g.apply_block_transient(2.0 * u - 3.0 * w)
+    rhs = 2.0 * g.apply_block_transient(u) - 3.0 * g.apply_block_transient(w)
+    assert relerr(lhs, rhs) <= 1e-13
+    cpu = O.SgSolver(nx, nx, c["px"], c["px"], coeff, t, alpha0=bench.ALPHA0, alpha1=bench.ALPHA1, dt=c["dt"],
+                     tol=bench.TOL)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 3, sg.ForceSpec(node=node, f0=bench.F0, t0=bench.T0))
+    hc = cpu.run(z, z, 3, force_node=node, f0=bench.F0, t0=bench.T0, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-8
