@@ -41,6 +41,7 @@ class NcclComm final : public Comm {
   }
   int rank() const override { return rank_; }
   int size() const override { return world_; }
+  bool capturable() const override { return true; }
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
     if (n == 0) return;
     SGW_NCCL(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, comm_, st));
@@ -93,6 +94,7 @@ class ThreadComm final : public Comm {
   }
   int rank() const override { return rank_; }
   int size() const override { return g_->world; }
+  bool capturable() const override { return false; }
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
     if (n == 0) return;
     if (n > cap_) {

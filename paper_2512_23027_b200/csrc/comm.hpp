@@ -26,6 +26,7 @@ class Comm {
   virtual int rank() const = 0;
   virtual int size() const = 0;
   virtual void allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;  // in place, device buffer
+  virtual bool capturable() const = 0;  // may be recorded into a CUDA graph (stream-ordered, no host sync)
 };
 
 void nccl_unique_id(void* out128);

@@ -378,6 +378,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   SGW_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   own_stream_ = true;
   for (auto& e : ev_) SGW_CUDA(cudaEventCreate(&e));
+  SGW_CUDA(cudaMallocHost(&h_scal_, 8 * sizeof(double)));
   if (cublasCreate(&blas_) != CUBLAS_STATUS_SUCCESS) throw Error(4, "cublasCreate failed");
   if (cusolverDnCreate(&sol_) != CUSOLVER_STATUS_SUCCESS) throw Error(4, "cusolverDnCreate failed");
   cublasSetStream(blas_, st_);
@@ -432,6 +433,9 @@ GpuSolver::~GpuSolver() {
   if (blas_) cublasDestroy(blas_);
   if (sol_) cusolverDnDestroy(sol_);
   for (auto& e : ev_) cudaEventDestroy(e);
+  if (graph_mv_) cudaGraphExecDestroy(graph_mv_);
+  if (graph_pc_) cudaGraphExecDestroy(graph_pc_);
+  if (h_scal_) cudaFreeHost(h_scal_);
   if (own_stream_ && st_) cudaStreamDestroy(st_);
 }
 

@@ -315,6 +315,11 @@ class GpuSolver {
   std::vector<double> force_table_;
   DBuf<double> force_row_, fext_;
   cudaEvent_t ev_[8];
+  // host-driven PCG: pinned residual scalar and the two per-iteration graphs
+  double* h_scal_ = nullptr;
+  cudaGraphExec_t graph_mv_ = nullptr, graph_pc_ = nullptr;
+  const double* graph_x_ = nullptr;
+  long long graph_mv_launches_ = 0, graph_pc_launches_ = 0;
 };
 
 }  // namespace sgw
