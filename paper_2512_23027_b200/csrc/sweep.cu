@@ -389,10 +389,29 @@ void GpuSolver::build_sweep_layout() {
   const long long blk = (sub_off + off + 31) & ~31LL;  // 256-byte aligned block rows
   if (blk >= (1LL << 31)) throw Error(1, "interior block too large for the sweep layout");
   // cluster size: about one wave of CTAs over the 148 SMs
-  sweep_cs_ = NS >= 100 ? 1 : NS >= 48 ? 2 : NS >= 24 ? 4 : 8;
+  sweep_cs_ = NS >= 100 ? 1 : NS >= 48 ? 2 : NS >= 24 ? 4 : NS >= 12 ? 8 : 16;
   if (const char* e = std::getenv("SGW_SWEEP_CS")) {  // test hook: force a cluster size
     const int v = std::atoi(e);
-    if (v == 1 || v == 2 || v == 4 || v == 8) sweep_cs_ = v;
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) sweep_cs_ = v;
+  }
+  if (sweep_cs_ == 16) {  // non-portable cluster size: only if 16-CTA clusters of this size are schedulable
+    const size_t sm16 = (size_t)6 * kTileD * 8 + 16 * 8 + 4 * 8 + 3 * (size_t)nb * kTile * 8;
+    const size_t smem = sm16 <= 227 * 1024 ? sm16 : (size_t)5 * kTileD * 8 + 16 * 8 + 4 * 8 + 3 * (size_t)nb * kTile * 8;
+    int nclus = 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16), cfg.blockDim = dim3(kSwThreads), cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr, cfg.numAttrs = 1;
+    if (cudaFuncSetAttribute((const void*)sweep_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute((const void*)sweep_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&nclus, (const void*)sweep_kernel<16>, &cfg) != cudaSuccess || nclus < NS) {
+      (void)cudaGetLastError();
+      sweep_cs_ = 8;
+    }
   }
   // schedules: output blocks -> (rank, warp) bins by longest-first greedy on
   // tile counts; each rank issues its warps' tiles interleaved
@@ -457,8 +476,10 @@ void GpuSolver::build_sweep_layout() {
   Fcomp.alloc(size_t(NS) * L.per_sub);
   const size_t smem = sweep_smem_bytes();
   for (auto fn : {(const void*)sweep_kernel<1>, (const void*)sweep_kernel<2>, (const void*)sweep_kernel<4>,
-                  (const void*)sweep_kernel<8>})
+                  (const void*)sweep_kernel<8>, (const void*)sweep_kernel<16>})
     SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (sweep_cs_ == 16)
+    SGW_CUDA(cudaFuncSetAttribute((const void*)sweep_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
 // factor blocks of subdomains [b0, b0 + nb) (batch-local Linv / Lsub) -> tiles
@@ -511,7 +532,8 @@ void GpuSolver::sweep(double* x) {
     case 1: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<1>, x, F, L)); break;
     case 2: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<2>, x, F, L)); break;
     case 4: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<4>, x, F, L)); break;
-    default: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<8>, x, F, L)); break;
+    case 8: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<8>, x, F, L)); break;
+    default: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<16>, x, F, L)); break;
   }
   SGW_LAUNCHED();
   KP.end(st_);

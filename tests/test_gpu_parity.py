@@ -135,7 +135,7 @@ def test_gaussian_pulse_trajectory_matches_oracle(gpu):
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-8
 
 
-@pytest.mark.parametrize("cs", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("cs", ["1", "2", "4", "8", "16"])
 def test_interior_sweep_every_cluster_size(gpu, monkeypatch, cs):
     # the batched Dirichlet solve (one thread-block cluster of CS CTAs per
     # subdomain) must give the oracle trajectory for every cluster size
