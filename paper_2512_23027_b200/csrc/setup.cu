@@ -528,6 +528,7 @@ void GpuSolver::setup_interior_and_schur(int b0, int nb) {
     assemble_ii_kernel<<<std::min(cdiv(tot, 256), 65535), 256, 0, st_>>>(A, D.p, Lsub.p, ns);
     SGW_LAUNCHED();
   }
+  extract_band_batch(b0, nb);  // A_{k+1,k} band for the sweeps, before the factorization
   Linv.alloc(size_t(ns) * H * BB);
   set_identity_kernel<<<std::min(cdiv((long long)ns * H * BB, 256), 65535), 256, 0, st_>>>(Linv.p, B, ns * H);
   SGW_LAUNCHED();
@@ -599,8 +600,14 @@ void GpuSolver::setup_interior_and_schur(int b0, int nb) {
   for (int k = 0; k < H; ++k)
     SGW_BLAS(cublasDtrsmBatched(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B, B,
                                 &one, pD.p + size_t(k) * ns, B, pI.p + size_t(k) * ns, B, ns));
+  // D_k^-1 = L_kk^-T L_kk^-1 (block Thomas form of the sweeps) over the finished factor blocks
+  const double zero = 0.0;
+  SGW_BLAS(cublasDgemmStridedBatched(blas_, CUBLAS_OP_T, CUBLAS_OP_N, B, B, B, &one, Linv.p, B, (long long)BB, Linv.p,
+                                     B, (long long)BB, &zero, D.p, B, (long long)BB, ns * H));
+  compact_dinv_batch(b0, nb, D.p);
   D.reset();
-  compact_factor_batch(b0, nb);
+  Linv.reset();
+  Lsub.reset();
 }
 
 // ------------------------------------------------------------ NN2 data -----

@@ -9,9 +9,11 @@
 //  * S_s and Q_s = S_rr^-1: lower 64x64 tiles, row-major inside a tile,
 //    diagonal tiles stored full (TilePack).
 //  * Psi_s = S_rr^-1 S_rc: column-major r_s x c_s.  F_cc^-1: n_C x n_C.
-//  * interior factor: block-tridiagonal by interior grid rows, block B =
-//    W (P+1) (node-major, term-minor); Linv[s][k] = L_kk^-1 and
-//    Lsub[s][k] = L_{k+1,k}, column-major B x B.
+//  * interior solve: block-tridiagonal by interior grid rows, block B =
+//    W (P+1) (node-major, term-minor); per grid row the lower tiles of
+//    D_k^-1 = (L_kk L_kk^T)^-1 and the S/SW coupling band of A_{k+1,k} in
+//    both orientations (sweep.cu).  Setup copies Linv[s][k] = L_kk^-1 and
+//    Lsub[s][k] = A_{k+1,k} -> L_{k+1,k} are dense column-major B x B.
 #pragma once
 
 #include <cublas_v2.h>
@@ -286,11 +288,13 @@ class GpuSolver {
   DBuf<int> iface_lid_;  // flat (ip_off): local interface p -> local node id
   DBuf<double> Linv, Lsub;  // dense setup copies (freed after compaction)
   DBuf<double> Fcomp;       // compact interior factor (sweep.cu)
-  DBuf<int> sw_off, sw_cs, sw_cuts, sw_ncut;
-  int sweep_cs_ = 1;
+  DBuf<int> sw_off, sw_cuts, sw_ncut, sw_wcuts, sw_nw;
+  int sweep_cs_ = 1, sweep_nch_ = 0, sweep_nbm_ = 12;
+  long long sweep_lo_off_ = 0, sweep_up_off_ = 0;
   SweepLayout* sweep_layout_ = nullptr;
   void build_sweep_layout();
-  void compact_factor_batch(int b0, int nb);
+  void extract_band_batch(int b0, int nb);
+  void compact_dinv_batch(int b0, int nb, const double* dinv);
   size_t sweep_smem_bytes() const;
   // persistent cooperative PCG (pcg_fused.cu)
   void setup_fused_pcg();

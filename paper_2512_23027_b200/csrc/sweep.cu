@@ -1,30 +1,34 @@
 // Batched interior Dirichlet solve x <- A_II^-1 x for every subdomain
 // (src/sg.cpp:317 and :350: SimplicialLLT::solve, restated block-wise).
 //
-// A_II = L L^T is block lower-bidiagonal over the H interior grid rows
-// (blocks B = W (P+1), node-major / term-minor):
-//   forward   y_k = L_kk^-1 (b_k - L_{k,k-1} y_{k-1})
-//   backward  x_k = L_kk^-T (y_k - L_{k+1,k}^T x_{k+1})
-// Both products of a block row are stored as 64 x 64 tiles (row-major, width
-// padded to even, zeros outside the factor's profile):
-//   INV_k = L_kk^-1     tiles (I, J), J <= I
-//   SUB_k = L_{k+1,k}   tiles (I, J), J >= Jmin(I): row r of L_{k+1,k} is zero left of
-//                       column c0(r) = ((node(r) - 1)(P+1)), so whole tiles vanish
-// The forward sweep multiplies the tiles (row sums); the backward sweep
-// multiplies their transposes from the same storage (column sums), so the
-// factor is held once.
+// A_II is block tridiagonal over the H interior grid rows (blocks B = W (P+1),
+// node-major / term-minor).  The solve is the block Thomas algorithm on the
+// Schur complements D_k = L_kk L_kk^T of the block Cholesky factor:
+//   forward   w_0 = b_0,  z_k = D_k^-1 w_k,  w_{k+1} = b_{k+1} - A_{k+1,k} z_k
+//   backward  x_{H-1} = z_{H-1},  x_k = D_k^-1 (w_k - A_{k,k+1} x_{k+1})
+// D_k^-1 = L_kk^-T L_kk^-1 is symmetric and stored once (lower 64 x 64 tiles,
+// row-major, diagonal tiles full); the grid-row coupling A_{k+1,k} only joins a
+// node to its S and SW neighbours (setup.cu assemble_ii_kernel), so it is kept
+// as a band of 2 (P+1) columns per row, for both orientations.  Per grid row
+// the sweep streams B (B + 1) / 2 + B 2 (P+1) doubles per direction, against
+// B (B + 1) / 2 plus the dense profile of L_{k+1,k} (about as large again) for
+// a forward/backward substitution with the Cholesky factor itself.
 //
-// Kernel: one thread-block cluster of CS CTAs per subdomain.  Every output
-// block (64 rows of a forward product, 64 columns of a backward one) belongs
-// to one consumer warp of one rank, which accumulates the block's tiles in
-// registers: lane l owns tile columns 2l, 2l+1, so a forward block needs one
-// 64-to-2 butterfly reduction at its end and a backward block none.  A
-// producer warp streams the rank's tiles (32 KB each) through a ring of
-// shared-memory stages with cp.async.bulk (TMA bulk copies completing on
-// mbarriers), interleaving the warps' tiles and running ahead across block
-// rows.  Results are pushed into every rank's copy of the vector through
-// DSMEM; one split cluster barrier closes each block-row phase.  Reductions
-// run in a fixed order: results are bitwise reproducible.
+// Kernel: one thread-block cluster of CS CTAs per subdomain.  A producer warp
+// streams the rank's tiles (<= 32 KB each) through a ring of shared-memory
+// stages with cp.async.bulk (TMA bulk copies completing on mbarriers).
+//  * D^-1 phase: each consumer warp owns a contiguous run of lower tiles in
+//    row-major order.  Lane l holds tile columns 2l, 2l+1: one pass over a
+//    tile gives the row products T v_J (64 lane partials per row run, one
+//    butterfly at its end) and the column products T^T v_I (lane-local).  Both
+//    land in per-warp register accumulators indexed by output block; the
+//    warps add them into one CTA vector in warp order, which each rank pushes
+//    to the owners of the rows (DSMEM).  The owner sums the ranks in order.
+//  * band phase: each rank applies the band columns that fall in the rows it
+//    owns and pushes the partial rows to every rank; the next phase sums the
+//    ranks' partials in rank order.
+// One split cluster barrier closes every phase.  All reductions run in a fixed
+// order: results are bitwise reproducible.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -37,20 +41,31 @@ namespace cg = cooperative_groups;
 
 namespace sgw {
 
-constexpr int kSwWarps = 4;                        // consumer warps
-constexpr int kSwThreads = (kSwWarps + 1) * 32;    // + one TMA producer warp
-constexpr int kTileD = kTile * kTile;              // doubles per stage (one tile)
-constexpr int kMaxSched = 512;                     // tiles per (rank, product)
-constexpr int kPre = 12;                           // prefetched rhs values per consumer thread
-enum { T_INV = 0, T_SUB = 1, T_INVT = 2, T_SUBT = 3, T_N = 4 };
+constexpr int kSwWarps = 4;                            // consumer warps
+constexpr int kSwThreads = (kSwWarps + 1) * 32;        // + one TMA producer warp
+constexpr int kTileD = kTile * kTile;                  // doubles per stage
+constexpr int kMaxSched = 512;                         // entries per (rank, phase type)
+constexpr int kPre = 12;                               // prefetched rhs values per consumer thread
+constexpr int kMaxCS = 16;                             // cluster size limit (non-portable 16)
+constexpr int kSmemMax = 227 * 1024;
+enum { T_SYM = 0, T_BLO = 1, T_BUP = 2, T_N = 3 };
+
+constexpr int kMaxW = 256;                             // entries per (rank, phase type, warp)
 
 struct SweepLayout {
-  const int4* tiles[2];  // INV / SUB tile tables: {offset, I << 16 | J, h << 16 | wp, 0}
-  const int4* sched;     // [(rank * T_N + type) * kMaxSched + p]: {tile, warp | first << 8 | last << 9, block, 0}
-  const int* nsched;     // [rank * T_N + type]
-  long long sub_off, blk, per_sub;  // SUB tiles inside a block row; block-row stride; per subdomain
-  int B, H, nb, VL, stages;
-  int n_inv, n_all;  // tile-table sizes (host side: compaction)
+  const int4* ent;     // stream entries: D^-1 tiles {off, I << 16 | J, h << 16 | wp, bytes},
+                       // then A_{k+1,k} / A_{k,k+1} band chunks {off, q, 0, bytes}
+  const int4* sched;   // producer stream [(rank * T_N + type) * kMaxSched + p]: {off, bytes, entry, 0}
+  const int* nsched;   // [rank * T_N + type]
+  const int4* wsched;  // consumer lists [((rank * T_N + type) * kSwWarps + warp) * kMaxW + p]:
+                       // {stream position, first | last << 1, I << 16 | J (tile) or q (chunk), h << 16 | wp}
+  const int* nwsched;  // [(rank * T_N + type) * kSwWarps + warp]
+  long long blk, per_sub;  // grid-row stride; per subdomain (doubles)
+  int B, H, nb, VL, NT, Rb, bw, stages;
+  int slot_len, tpart_len;
+  int own[kMaxCS + 1];                                  // rank r owns rows [own[r], own[r+1])
+  int tlo[2][kMaxCS], thi[2][kMaxCS], toff[2][kMaxCS];  // band rows rank r contributes (LO, UP)
+  int n_sym, n_ent;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -87,42 +102,84 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kSwWarps * 32) : "memory");
 }
 
-// Streaming order: forward INV_0, SUB_0, INV_1, ..., INV_{H-1}; backward
-// INVT_{H-1}, SUBT_{H-2}, INVT_{H-2}, ..., INVT_0 (SUB_k / SUBT_k hold L_{k+1,k}).
+// Phase order (4H - 3 phases): forward SYM_0, BLO_0, SYM_1, ..., BLO_{H-2},
+// SYM_{H-1}; backward BUP_{H-2}, SYM_{H-2}, ..., BUP_0, SYM_0.
 __device__ __forceinline__ void seg_info(int seg, int H, int& type, int& k, bool& fwd) {
   const int nf = 2 * H - 1;
   fwd = seg < nf;
-  const int q = fwd ? seg : seg - nf;
-  const int j = (q + 1) >> 1;
-  const bool sub = q & 1;
-  type = fwd ? (sub ? T_SUB : T_INV) : (sub ? T_SUBT : T_INVT);
-  k = fwd ? (sub ? j - 1 : j) : H - 1 - j;
-}
-
-// 64 lane partials (rows 0..63 of a block, this lane's two columns) -> sums
-// of rows 2 lane and 2 lane + 1 in a[0], a[1]: a butterfly that halves the
-// live values at every level (62 exchanges for 64 rows).
-__device__ __forceinline__ void butterfly64(double (&a)[kTile], int lane) {
-#pragma unroll
-  for (int lvl = 0; lvl < 5; ++lvl) {
-    const int half = 32 >> lvl, m = 16 >> lvl;
-    const bool up = lane & m;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = up ? a[i] : a[i + half], keep = up ? a[i + half] : a[i];
-      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-    }
+  if (fwd) {
+    k = seg >> 1;
+    type = (seg & 1) ? T_BLO : T_SYM;
+  } else {
+    const int q = seg - nf;
+    k = H - 2 - (q >> 1);
+    type = (q & 1) ? T_SYM : T_BUP;
   }
 }
 
-template <int CS>
+// Row products of a swizzled tile (row stride W): lane accumulates rows lane
+// and lane + 32 against v_J (broadcast), four chains per row.  Rows >= h of the
+// stage hold stale (finite) data: they only reach padding rows of the output.
+template <int W>
+__device__ __forceinline__ void tile_rows(const double* __restrict__ buf, const double* __restrict__ vj, int lane,
+                                          int wp, double (&ra)[4], double (&rb)[4]) {
+  const int sw = 2 * (lane & 7);
+  const int ws = W > 0 ? W : wp;
+  const double* pa = buf + lane * ws;
+  const double* pb = pa + 32 * ws;
+#pragma unroll(W > 0 ? 16 : 4)
+  for (int c = 0; c < ws; c += 4) {
+    const double2 v0 = *reinterpret_cast<const double2*>(vj + c);
+    const double2 v1 = *reinterpret_cast<const double2*>(vj + c + 2);
+    const int o0 = (c & ~15) | ((c & 15) ^ sw), o1 = ((c + 2) & ~15) | (((c + 2) & 15) ^ sw);
+    const double2 a0 = *reinterpret_cast<const double2*>(pa + o0);
+    const double2 a1 = *reinterpret_cast<const double2*>(pa + o1);
+    const double2 b0 = *reinterpret_cast<const double2*>(pb + o0);
+    const double2 b1 = *reinterpret_cast<const double2*>(pb + o1);
+    ra[0] = fma(a0.x, v0.x, ra[0]);
+    ra[1] = fma(a0.y, v0.y, ra[1]);
+    ra[2] = fma(a1.x, v1.x, ra[2]);
+    ra[3] = fma(a1.y, v1.y, ra[3]);
+    rb[0] = fma(b0.x, v0.x, rb[0]);
+    rb[1] = fma(b0.y, v0.y, rb[1]);
+    rb[2] = fma(b1.x, v1.x, rb[2]);
+    rb[3] = fma(b1.y, v1.y, rb[3]);
+  }
+}
+
+// Column products of a full-width swizzled tile: lane holds columns 2 lane,
+// 2 lane + 1, summed over all 64 rows against v_I (rows >= h meet v_I = 0).
+__device__ __forceinline__ void tile_cols(const double* __restrict__ buf, const double* __restrict__ vi, int lane,
+                                          double (&cc)[4]) {
+  const int q = 2 * lane;
+#pragma unroll
+  for (int r = 0; r < kTile; r += 2) {
+    const double2 w = *reinterpret_cast<const double2*>(vi + r);
+    const double2 a = *reinterpret_cast<const double2*>(buf + r * kTile + (q ^ (2 * (r & 7))));
+    const double2 b = *reinterpret_cast<const double2*>(buf + (r + 1) * kTile + (q ^ (2 * ((r + 1) & 7))));
+    cc[0] = fma(a.x, w.x, cc[0]);
+    cc[1] = fma(a.y, w.x, cc[1]);
+    cc[2] = fma(b.x, w.y, cc[2]);
+    cc[3] = fma(b.y, w.y, cc[3]);
+  }
+}
+
+// cx[j] += a, cy[j] += b for a warp-uniform runtime j (registers stay put)
+template <int NBM>
+__device__ __forceinline__ void add_at(double (&cx)[NBM], double (&cy)[NBM], int j, double a, double b) {
+#pragma unroll
+  for (int q = 0; q < NBM; ++q)
+    if (q == j) cx[q] += a, cy[q] += b;
+}
+
+template <int CS, int NBM>
 __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict__ x, const double* __restrict__ F,
-                                                              SweepLayout L) {
+                                                              const SweepLayout L) {
   extern __shared__ __align__(128) unsigned char smraw[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = CS > 1 ? (int)cluster.block_rank() : 0;
   const int s = blockIdx.x / CS;
-  const int B = L.B, H = L.H, VL = L.VL, S = L.stages;
+  const int B = L.B, H = L.H, VL = L.VL, S = L.stages, nb = L.nb;
   double* stage = reinterpret_cast<double*>(smraw);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw + (size_t)S * kTileD * 8);
   unsigned long long* empty = full + 8;
@@ -130,22 +187,31 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   // positions, so a fast warp may reach a stage a full ring ahead of the tile
   // it holds; a parity wait alone would then match the previous phase.
   volatile int* ticket = reinterpret_cast<volatile int*>(empty + 8);
-  double* vv = reinterpret_cast<double*>(empty + 12);  // y_k (forward) / s_k (backward), zero padded to VL
-  double* tv = vv + VL;                                 // t_k (forward) / x_k (backward)
-  double* bv = tv + VL;                                 // right-hand side block: b_{k+1} / y_k
+  double* wv = reinterpret_cast<double*>(smraw + (size_t)S * kTileD * 8 + 256);  // D^-1 input (full vector)
+  double* red = wv + VL;                       // CTA sum of the warps' D^-1 partials
+  double* zv = CS > 1 ? red + VL : red;        // D^-1 output, owned rows
+  double* slots = zv + VL;                     // [source rank][owned row] partials (CS > 1)
+  double* tpart = CS > 1 ? slots + CS * L.slot_len : red + VL;  // band partials [rank segments]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* Fs = F + (long long)s * L.per_sub;
   double* xs = x + (long long)s * H * B;
-  const int nseg = 2 * (2 * H - 1);
+  const int nseg = 4 * H - 3;
+  const int own_lo = L.own[rank], own_hi = L.own[rank + 1];
 
-  for (int i = tid; i < 3 * VL; i += kSwThreads) vv[i] = 0.0;
-  __syncthreads();
-  // b_0, read before the first cluster barrier: afterwards peers store y_0 over it
-  for (int c = tid; c < B; c += kSwThreads) tv[c] = __ldcg(xs + c);
+  // the ring starts zeroed: rows beyond a partial tile are then always finite
+  for (int i = tid; i < S * kTileD / 2; i += kSwThreads) reinterpret_cast<double2*>(stage)[i] = make_double2(0.0, 0.0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the first bulk copy overwrites it
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) ticket[i] = -1;
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // b_0, read before the first cluster barrier (line 0 is rewritten only at the end)
+  double pre[kPre];
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) {
+    const int i = tid + u * kSwWarps * 32;
+    pre[u] = (warp < kSwWarps && i < B) ? __ldcg(xs + i) : 0.0;
   }
   __syncthreads();
   cl_arrive();  // peers push into this CTA's shared memory only after it is initialised
@@ -160,141 +226,187 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       seg_info(seg, H, type, k, fwd);
       const int4* sch = L.sched + (rank * T_N + type) * kMaxSched;
       const int n = L.nsched[rank * T_N + type];
-      const int4* tt = L.tiles[type & 1];
-      const double* base = Fs + k * L.blk + ((type & 1) ? L.sub_off : 0);
+      const double* base = Fs + k * L.blk;
       for (int p = 0; p < n; ++p, ++pos) {
         const int st = int(pos % S);
         if (pos >= S) mbar_wait(&empty[st], unsigned((pos / S) - 1) & 1u);
         if (lane == 0) {
-          const int4 d = __ldg(tt + __ldg(&sch[p].x));
-          const unsigned bytes = unsigned((d.z >> 16) * (d.z & 0xffff)) * 8u;
+          const int4 d = __ldg(sch + p);
           ticket[st] = int(pos);  // stage st now belongs to position pos (its previous tile is released)
-          mbar_expect_tx(&full[st], bytes);
-          tma_bulk_load(stage + (size_t)st * kTileD, base + d.x, bytes, &full[st]);
+          mbar_expect_tx(&full[st], unsigned(d.y));
+          tma_bulk_load(stage + (size_t)st * kTileD, base + d.x, unsigned(d.y), &full[st]);
         }
         __syncwarp();
       }
-      // one cluster barrier closes every segment; arrive early, wait one late
+      // one cluster barrier closes every phase; arrive early, wait one late
       if (seg > 0) cl_wait();
       cl_arrive();
     }
-    cl_wait();
-    cl_arrive();  // final barrier
     cl_wait();
     return;
   }
 
   // -------------------------------------------------------- consumers ---
   long long pos = 0;
-  double pre[kPre];
-#pragma unroll
-  for (int i = 0; i < kPre; ++i) pre[i] = 0.0;
   for (int seg = 0; seg < nseg; ++seg) {
     int type, k;
     bool fwd;
     seg_info(seg, H, type, k, fwd);
-    const bool sub = type & 1, trans = type >= T_INVT;
-    // prologue (vectors of the previous phase are complete: cluster barrier)
-    bool sync = false;
-    if (sub) {
-#pragma unroll
-      for (int i = 0; i < kPre; ++i) {
-        const int c = tid + i * kSwWarps * 32;
-        if (c < B) bv[c] = pre[i];
-      }
-      sync = true;
-    } else if (fwd ? k < H - 1 : k > 0) {
-      // prefetch the next phase's right-hand side: b_{k+1} (forward) / y_{k-1} (backward)
-      const double* src = xs + (long long)(fwd ? k + 1 : k - 1) * B;
-#pragma unroll
-      for (int i = 0; i < kPre; ++i) {
-        const int c = tid + i * kSwWarps * 32;
-        pre[i] = c < B ? __ldcg(src + c) : 0.0;
-      }
-    }
-    if (sync) consumers_sync();
-    // forward INV: t -> y (tv -> vv), SUB: y -> t (vv -> tv); backward from
-    // y_{H-1} in vv: INVT vv -> tv, SUBT tv -> vv.  A phase never writes the
-    // vector it (or a slower peer) reads.
-    const double* vec = (sub == fwd) ? vv : tv;
-    double* dst = (sub == fwd) ? tv : vv;
-    double* peer[CS];
-#pragma unroll
-    for (int q = 0; q < CS; ++q) peer[q] = CS > 1 ? cluster.map_shared_rank(dst, q) : dst;
-    double* ys = xs + (long long)k * B;
-
-    const int4* sch = L.sched + (rank * T_N + type) * kMaxSched;
     const int n = L.nsched[rank * T_N + type];
-    const int4* tt = L.tiles[type & 1];
-    double acc[kTile];
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    if (type == T_SYM) {
+      // input w_k (forward: b_k minus the band partials of BLO_{k-1}; backward:
+      // w_k minus those of BUP_k).  The forward stores w_k for the backward pass.
+      const int t = fwd ? 0 : 1;
+      const bool band_in = !(fwd && k == 0);
 #pragma unroll
-    for (int r = 0; r < kTile; ++r) acc[r] = 0.0;
-    for (int p = 0; p < n; ++p) {
-      const int4 e = __ldg(sch + p);
-      if ((e.y & 0xff) != warp) continue;
-      const long long gp = pos + p;
-      const int st = int(gp % S);
-      const int4 d = __ldg(tt + e.x);
-      const int I = d.y >> 16, J = d.y & 0xffff, h = d.z >> 16, wp = d.z & 0xffff;
-      const bool act = 2 * lane < wp;
-      const double* buf = stage + (size_t)st * kTileD;
-      if (e.y & 0x100) {  // first tile of the output block
-#pragma unroll
-        for (int r = 0; r < kTile; ++r) acc[r] = 0.0;
-        c0 = c1 = c2 = c3 = 0.0;
+      for (int u = 0; u < kPre; ++u) {
+        const int i = tid + u * kSwWarps * 32;
+        if (i < VL) {
+          double v = pre[u];
+          if (band_in)
+            for (int r = 0; r < CS; ++r)
+              if (i >= L.tlo[t][r] && i < L.thi[t][r]) v -= tpart[L.toff[t][r] + i - L.tlo[t][r]];
+          wv[i] = v;
+          if (fwd && k > 0 && i >= own_lo && i < own_hi && i < B) xs[(long long)k * B + i] = v;
+        }
       }
-      while (ticket[st] != int(gp)) {
-      }
-      mbar_wait(&full[st], unsigned(gp / S) & 1u);
-      if (!trans) {  // row sums: acc[r] += T[r][2l..2l+1] . vec[64J + 2l..]
-        if (act) {
-          const double2 xv = reinterpret_cast<const double2*>(vec + J * kTile)[lane];
+      // prefetch the next input: b_{k+1}, then w_{H-2} (end of the forward), w_{k-1}
+      const int nxt = fwd ? (k + 1 < H ? k + 1 : H - 2) : k - 1;
+      if (nxt >= 0) {
 #pragma unroll
-          for (int r = 0; r < kTile; ++r)
-            if (r < h) {
-              const double2 a = reinterpret_cast<const double2*>(buf + r * wp)[lane];
-              acc[r] = fma(a.x, xv.x, fma(a.y, xv.y, acc[r]));
+        for (int u = 0; u < kPre; ++u) {
+          const int i = tid + u * kSwWarps * 32;
+          pre[u] = i < B ? __ldcg(xs + (long long)nxt * B + i) : 0.0;
+        }
+      }
+      consumers_sync();
+
+      double cx[NBM], cy[NBM];
+#pragma unroll
+      for (int q = 0; q < NBM; ++q) cx[q] = cy[q] = 0.0;
+      // row sums of rows lane / lane + 32 of the current row run
+      double ra[4] = {0.0, 0.0, 0.0, 0.0}, rb[4] = {0.0, 0.0, 0.0, 0.0};
+      const int4* ws = L.wsched + (long long)((rank * T_N + type) * kSwWarps + warp) * kMaxW;
+      const int nw = L.nwsched[(rank * T_N + type) * kSwWarps + warp];
+      int4 e = __ldg(ws);
+      for (int p = 0; p < nw; ++p) {
+        const int4 en = __ldg(ws + min(p + 1, nw - 1));
+        const long long gp = pos + e.x;
+        const int st = int(gp % S);
+        const int I = e.z >> 16, J = e.z & 0xffff, wp = e.w & 0xffff;
+        const double* buf = stage + (size_t)st * kTileD;
+        if (e.y & 1) {  // first tile of a row run
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ra[c] = rb[c] = 0.0;
+        }
+        while (ticket[st] != int(gp)) {
+        }
+        mbar_wait(&full[st], unsigned(gp / S) & 1u);
+        if (wp == kTile)
+          tile_rows<kTile>(buf, wv + J * kTile, lane, wp, ra, rb);
+        else  // the corner tile of a grid row whose width is not a multiple of 64 (diagonal)
+          tile_rows<0>(buf, wv + J * kTile, lane, wp, ra, rb);
+        if (I != J) {  // column products T^T v_I from the same stage
+          double cc[4] = {0.0, 0.0, 0.0, 0.0};
+          tile_cols(buf, wv + I * kTile, lane, cc);
+          add_at(cx, cy, J, cc[0] + cc[2], cc[1] + cc[3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
+        if (e.y & 2) {  // last tile of the row run: rows (lane, lane + 32) -> (2 lane, 2 lane + 1)
+          const double va = (ra[0] + ra[1]) + (ra[2] + ra[3]), vb = (rb[0] + rb[1]) + (rb[2] + rb[3]);
+          const int s0 = (2 * lane) & 31, s1 = (2 * lane + 1) & 31;
+          const double a0 = __shfl_sync(0xffffffffu, va, s0), b0 = __shfl_sync(0xffffffffu, vb, s0);
+          const double a1 = __shfl_sync(0xffffffffu, va, s1), b1 = __shfl_sync(0xffffffffu, vb, s1);
+          add_at(cx, cy, I, lane < 16 ? a0 : b0, lane < 16 ? a1 : b1);
+        }
+        e = en;
+      }
+      // CTA sum in warp order, then to the row owners
+#pragma unroll 1
+      for (int w = 0; w < kSwWarps; ++w) {
+        if (warp == w) {
+#pragma unroll
+          for (int q = 0; q < NBM; ++q)
+            if (q < nb) {
+              double2* dq = reinterpret_cast<double2*>(red + q * kTile) + lane;
+              double2 v = make_double2(cx[q], cy[q]);
+              if (w > 0) {
+                const double2 o = *dq;
+                v.x = o.x + v.x, v.y = o.y + v.y;
+              }
+              *dq = v;
             }
         }
-      } else if (act) {  // column sums: (c0, c1) += T[r][2l..2l+1] * vec[64I + r]
-        const double* w = vec + I * kTile;
-#pragma unroll 8
-        for (int r = 0; r + 1 < h; r += 2) {
-          const double2 a = reinterpret_cast<const double2*>(buf + r * wp)[lane];
-          const double2 b = reinterpret_cast<const double2*>(buf + (r + 1) * wp)[lane];
-          const double w0 = w[r], w1 = w[r + 1];
-          c0 = fma(a.x, w0, c0);
-          c1 = fma(a.y, w0, c1);
-          c2 = fma(b.x, w1, c2);
-          c3 = fma(b.y, w1, c3);
-        }
-        if (h & 1) {
-          const double2 a = reinterpret_cast<const double2*>(buf + (h - 1) * wp)[lane];
-          c0 = fma(a.x, w[h - 1], c0);
-          c1 = fma(a.y, w[h - 1], c1);
+        consumers_sync();
+      }
+      if (CS > 1) {
+        for (int i = tid; i < VL; i += kSwWarps * 32) {
+          int r = 0;
+          while (i >= L.own[r + 1]) ++r;
+          double* dst = cluster.map_shared_rank(slots, r);
+          dst[rank * L.slot_len + i - L.own[r]] = red[i];
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
-      if (e.y & 0x200) {  // last tile of the output block: finish it
-        double v0, v1;
-        int o;
-        if (!trans) {
-          butterfly64(acc, lane);
-          v0 = acc[0], v1 = acc[1], o = I * kTile + 2 * lane;
-        } else {
-          v0 = c0 + c2, v1 = c1 + c3, o = J * kTile + 2 * lane;
+    } else {
+      // input z_k / x_{k+1}: the owned rows, summed over the ranks in order
+      if (CS > 1)
+        for (int i = own_lo + tid; i < own_hi; i += kSwWarps * 32) {
+          double v = 0.0;
+          for (int r = 0; r < CS; ++r) v += slots[r * L.slot_len + i - own_lo];
+          zv[i] = v;
         }
+      if (!fwd)  // x_{k+1} is final
+        for (int i = own_lo + tid; i < own_hi && i < B; i += kSwWarps * 32) xs[(long long)(k + 1) * B + i] = zv[i];
+      consumers_sync();
+
+      const int t = type == T_BLO ? 0 : 1, d0 = type == T_BLO ? -1 : 0;
+      const int Rb = L.Rb, bw = L.bw, NT = L.NT;
+      const int tl = L.tlo[t][rank], th = L.thi[t][rank], to = L.toff[t][rank];
+      double* dst[CS];
+#pragma unroll
+      for (int r = 0; r < CS; ++r) dst[r] = CS > 1 ? cluster.map_shared_rank(tpart, r) : tpart;
+      const int4* ws = L.wsched + (long long)((rank * T_N + type) * kSwWarps + warp) * kMaxW;
+      const int nw = L.nwsched[(rank * T_N + type) * kSwWarps + warp];
+      for (int p = 0; p < nw; ++p) {
+        const int4 e = __ldg(ws + p);
+        const long long gp = pos + e.x;
+        const int st = int(gp % S);
+        const int q = e.z;
+        const double* buf = stage + (size_t)st * kTileD;
+        while (ticket[st] != int(gp)) {
+        }
+        mbar_wait(&full[st], unsigned(gp / S) & 1u);
+        double val[2] = {0.0, 0.0};
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int oo = o + u;
-          if (oo < B) {
-            const double val = sub ? bv[oo] - (u ? v1 : v0) : (u ? v1 : v0);
-#pragma unroll
-            for (int q = 0; q < CS; ++q) peer[q][oo] = val;
-            if (!sub) ys[oo] = val;  // y_k (forward) / x_k (backward)
+          const int r = lane + 32 * u, i = q * Rb + r;
+          if (r < Rb && i < B) {
+            const int c0 = (i / NT + d0) * NT;
+            double v0 = 0.0, v1 = 0.0;
+            int c = 0;
+            for (; c + 1 < bw; c += 2) {
+              const int g0 = c0 + c, g1 = g0 + 1;
+              const double z0 = (g0 >= own_lo && g0 < own_hi) ? zv[g0] : 0.0;
+              const double z1 = (g1 >= own_lo && g1 < own_hi) ? zv[g1] : 0.0;
+              v0 = fma(buf[c * Rb + r], z0, v0);
+              v1 = fma(buf[(c + 1) * Rb + r], z1, v1);
+            }
+            if (c < bw) {
+              const int g0 = c0 + c;
+              v0 = fma(buf[c * Rb + r], (g0 >= own_lo && g0 < own_hi) ? zv[g0] : 0.0, v0);
+            }
+            val[u] = v0 + v1;
           }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = lane + 32 * u, i = q * Rb + r;
+          if (r < Rb && i >= tl && i < th)
+#pragma unroll
+            for (int rr = 0; rr < CS; ++rr) dst[rr][to + i - tl] = val[u];
         }
       }
     }
@@ -302,101 +414,168 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
     cl_arrive();  // results pushed: one cluster barrier (also a CTA barrier) ends the phase
     cl_wait();
   }
-  cl_arrive();  // final barrier: no rank exits while peers may still touch its shared memory
-  cl_wait();
+  // x_0 (the last phase was SYM_0): owned rows, ranks in order
+  for (int i = own_lo + tid; i < own_hi && i < B; i += kSwWarps * 32) {
+    double v;
+    if (CS > 1) {
+      v = 0.0;
+      for (int r = 0; r < CS; ++r) v += slots[r * L.slot_len + i - own_lo];
+    } else {
+      v = red[i];
+    }
+    xs[i] = v;
+  }
 }
 
-// --------------------------------------------------------- compaction ---
-struct TileTabs {
-  const int4* tiles;  // INV tiles then SUB tiles
-  int n_inv, n_all;
-};
-
-// Copy the dense column-major factor blocks (Linv_d: L_kk^-1, Lsub_d: L_{k+1,k})
-// into the tile layout; record the largest magnitude of L_{k+1,k} outside the
-// tiles (must be exactly zero).
-__global__ void compact_factor_kernel(const double* __restrict__ Linv_d, const double* __restrict__ Lsub_d,
-                                      double* __restrict__ F, TileTabs T, const int* __restrict__ jmin,
-                                      long long sub_off, long long blk, int B, int H, int ns,
-                                      unsigned long long* __restrict__ dropped) {
-  const long long BB = (long long)B * B;
-  const long long total = (long long)ns * H * blk;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const long long sk = e / blk;  // s * H + k
-    const int k = int(sk % H);
-    const long long w = e % blk;
-    const bool sub = w >= sub_off;
-    const long long ws = w - (sub ? sub_off : 0);
-    int lo = sub ? T.n_inv : 0, hi = sub ? T.n_all : T.n_inv;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (T.tiles[mid].x <= ws) lo = mid; else hi = mid;
-    }
-    const int4 d = T.tiles[lo];
-    const long long idx = ws - d.x;
-    const int wp = d.z & 0xffff, h = d.z >> 16;
+// ------------------------------------------------------------ storage ---
+// D_k^-1 (dense column-major, lower triangle valid) -> lower tiles, diagonal
+// tiles mirrored to full.  Element (r, c) of a tile sits at r wp + (c ^ 2 (r & 7)):
+// 16-byte column pairs swizzled by row, so that 8 lanes reading one column pair
+// of 8 consecutive rows, or 8 column pairs of one row, hit distinct banks.
+// One CTA per (subdomain, grid row, tile).
+__global__ void compact_dinv_kernel(const double* __restrict__ Dinv, double* __restrict__ F, const int4* __restrict__ ent,
+                                    int n_sym, long long blk, int B, int H) {
+  const int e = blockIdx.x % n_sym;
+  const long long sk = blockIdx.x / n_sym;  // s * H + k
+  const int4 d = ent[e];
+  const int I = d.y >> 16, J = d.y & 0xffff, h = d.z >> 16, wp = d.z & 0xffff;
+  const double* D = Dinv + sk * (long long)B * B;
+  double* out = F + sk * blk + d.x;
+  for (int idx = threadIdx.x; idx < h * wp; idx += blockDim.x) {
+    const int rl = idx / wp;
+    const int r = I * kTile + rl, c = J * kTile + ((idx % wp) ^ (2 * (rl & 7)));
     double v = 0.0;
-    if (idx < (long long)h * wp) {  // else: block-row alignment padding
-      const int r = (d.y >> 16) * kTile + int(idx / wp), c = (d.y & 0xffff) * kTile + int(idx % wp);
-      if (c < B) {
-        if (!sub) v = c <= r ? Linv_d[sk * BB + (long long)c * B + r] : 0.0;
-        else if (k < H - 1) v = Lsub_d[((sk / H) * (H - 1) + k) * BB + (long long)c * B + r];
-      }
-    }
-    F[e] = v;
+    if (r < B && c < B) v = c <= r ? D[(long long)c * B + r] : D[(long long)r * B + c];
+    out[idx] = v;
   }
-  const long long tot2 = (long long)ns * (H - 1) * BB;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot2; e += (long long)gridDim.x * blockDim.x) {
-    const long long m = e % BB;
+}
+
+// A_{k+1,k} (dense column-major B x B, rows: grid row k+1) -> the LO band
+// (row i of grid row k+1, columns (node(i) - 1)(P+1) + c) and the UP band of
+// its transpose A_{k,k+1} (row i of grid row k, columns node(i)(P+1) + c),
+// chunks of Rb rows stored column-major [c][Rb].  Also records the largest
+// |entry| of A_{k+1,k} outside the LO band (must be exactly zero).
+__global__ void extract_band_kernel(const double* __restrict__ E, double* __restrict__ F, int B, int H, int NT, int Rb,
+                                    int bw, int nch, long long blk, long long lo_off, long long up_off, int ns,
+                                    unsigned long long* __restrict__ dropped) {
+  const long long chunk = (long long)bw * Rb;
+  const long long per = 2LL * nch * chunk;  // both bands of one (s, k)
+  const long long total = (long long)ns * (H - 1) * per;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long sk = t / per;  // s * (H - 1) + k
+    const long long w = t % per;
+    const bool up = w >= nch * chunk;
+    const long long wq = up ? w - nch * chunk : w;
+    const int q = int(wq / chunk), c = int((wq % chunk) / Rb), r = int(wq % Rb);
+    const int i = q * Rb + r;
+    const double* A = E + sk * (long long)B * B;
+    double v = 0.0;
+    if (i < B) {
+      const int g = (i / NT + (up ? 0 : -1)) * NT + c;
+      if (g >= 0 && g < B) v = up ? A[(long long)i * B + g] : A[(long long)g * B + i];
+    }
+    const long long s = sk / (H - 1), k = sk % (H - 1);
+    F[(s * H + k) * blk + (up ? up_off : lo_off) + wq] = v;
+  }
+  const long long tot2 = (long long)ns * (H - 1) * B * B;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot2; t += (long long)gridDim.x * blockDim.x) {
+    const long long m = t % ((long long)B * B);
     const int c = int(m / B), r = int(m % B);
-    if (c < jmin[r / kTile] * kTile) {
-      const double a = fabs(Lsub_d[e]);
+    const int g0 = (r / NT - 1) * NT;
+    if (c < g0 || c >= g0 + bw) {
+      const double a = fabs(E[t]);
       if (a != 0.0) atomicMax(dropped, (unsigned long long)__double_as_longlong(a));
     }
   }
 }
 
+using SweepFn = void (*)(double*, const double*, const SweepLayout);
+static SweepFn sweep_fn(int cs, int nbm) {
+#define SGW_SW(C)                                                  \
+  case C:                                                          \
+    return nbm == 12 ? (SweepFn)sweep_kernel<C, 12> : (SweepFn)sweep_kernel<C, 24>;
+  switch (cs) {
+    SGW_SW(1)
+    SGW_SW(2)
+    SGW_SW(4)
+    SGW_SW(8)
+    default:
+      return nbm == 12 ? (SweepFn)sweep_kernel<16, 12> : (SweepFn)sweep_kernel<16, 24>;
+  }
+#undef SGW_SW
+}
+
+static size_t smem_bytes(int stages, int VL, int CS, int slot_len, int tpart_len) {
+  const size_t vec = 2 * (size_t)VL + (CS > 1 ? (size_t)VL + (size_t)CS * slot_len : 0) + (size_t)tpart_len;
+  return (size_t)stages * kTileD * 8 + 256 + vec * 8;
+}
+
 void GpuSolver::build_sweep_layout() {
-  const int H = G.H, nb = (B + kTile - 1) / kTile;
+  const int H = G.H, nb = (B + kTile - 1) / kTile, VL = nb * kTile;
   if (B > kPre * kSwWarps * 32) throw Error(1, "interior block too large for the sweep kernel");
-  // L_{k+1,k}: row r is zero left of c0(r) = (node(r) - 1)(P+1)
-  std::vector<int> jmin(nb, nb);
-  for (int r = 0; r < B; ++r) jmin[r / kTile] = std::min(jmin[r / kTile], std::max(0, r / NT - 1) * NT / kTile);
+  const int bw = 2 * NT;
+  int Rb = 64;
+  while (Rb > 16 && Rb * bw > kTileD) Rb /= 2;
+  if (Rb * bw > kTileD) throw Error(1, "interior band too wide for the sweep kernel");
+  const int nch = (B + Rb - 1) / Rb;
   auto hgt = [&](int I) { return std::min(kTile, B - I * kTile); };
-  auto wpad = [&](int J) { return (std::min(kTile, B - J * kTile) + 1) & ~1; };
-  std::vector<int4> tabs;
-  std::vector<std::vector<int>> blocks[T_N];  // output block -> tile ids (into its table)
-  for (auto& b : blocks) b.assign(nb, {});
+  // stored tile width: a multiple of 16 so that the swizzle (column pairs
+  // XOR 2 (row & 7)) stays inside the row and both products are conflict-free
+  auto wpad = [&](int J) { return (std::min(kTile, B - J * kTile) + 15) & ~15; };
+  std::vector<int4> ent;
   long long off = 0;
   for (int I = 0; I < nb; ++I)
     for (int J = 0; J <= I; ++J) {
-      blocks[T_INV][I].push_back((int)tabs.size());
-      blocks[T_INVT][J].push_back((int)tabs.size());
-      tabs.push_back(make_int4((int)off, I << 16 | J, hgt(I) << 16 | wpad(J), 0));
+      ent.push_back(make_int4((int)off, I << 16 | J, hgt(I) << 16 | wpad(J), hgt(I) * wpad(J) * 8));
       off += (long long)hgt(I) * wpad(J);
     }
-  const int n_inv = (int)tabs.size();
-  const long long sub_off = (off + 31) & ~31LL;  // 256-byte aligned
-  off = 0;
-  for (int I = 0; I < nb; ++I)
-    for (int J = jmin[I]; J < nb; ++J) {
-      const int id = (int)tabs.size() - n_inv;
-      blocks[T_SUB][I].push_back(id);
-      blocks[T_SUBT][J].push_back(id);
-      tabs.push_back(make_int4((int)off, I << 16 | J, hgt(I) << 16 | wpad(J), 0));
-      off += (long long)hgt(I) * wpad(J);
-    }
-  const long long blk = (sub_off + off + 31) & ~31LL;  // 256-byte aligned block rows
+  const int n_sym = (int)ent.size();
+  const long long lo_off = (off + 31) & ~31LL;  // 256-byte aligned
+  const long long up_off = (lo_off + (long long)nch * bw * Rb + 31) & ~31LL;
+  for (int band = 0; band < 2; ++band)
+    for (int q = 0; q < nch; ++q)
+      ent.push_back(make_int4(int((band ? up_off : lo_off) + (long long)q * bw * Rb), q, 0, bw * Rb * 8));
+  const long long blk = (up_off + (long long)nch * bw * Rb + 31) & ~31LL;
   if (blk >= (1LL << 31)) throw Error(1, "interior block too large for the sweep layout");
+
   // cluster size: about one wave of CTAs over the 148 SMs
-  sweep_cs_ = NS >= 100 ? 1 : NS >= 48 ? 2 : NS >= 24 ? 4 : NS >= 12 ? 8 : 16;
+  int CS = NS >= 100 ? 1 : NS >= 48 ? 2 : NS >= 24 ? 4 : NS >= 12 ? 8 : 16;
   if (const char* e = std::getenv("SGW_SWEEP_CS")) {  // test hook: force a cluster size
     const int v = std::atoi(e);
-    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) sweep_cs_ = v;
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) CS = v;
   }
-  if (sweep_cs_ == 16) {  // non-portable cluster size: only if 16-CTA clusters of this size are schedulable
-    const size_t sm16 = (size_t)6 * kTileD * 8 + 16 * 8 + 4 * 8 + 3 * (size_t)nb * kTile * 8;
-    const size_t smem = sm16 <= 227 * 1024 ? sm16 : (size_t)5 * kTileD * 8 + 16 * 8 + 4 * 8 + 3 * (size_t)nb * kTile * 8;
+  const int nbm = nb <= 12 ? 12 : 24;
+  SweepLayout L{};
+  auto plan = [&](int cs) {
+    // row ownership: contiguous 64-row blocks
+    for (int r = 0; r <= cs; ++r) L.own[r] = r == cs ? VL : kTile * (r * nb / cs);
+    L.slot_len = 0;
+    for (int r = 0; r < cs; ++r) L.slot_len = std::max(L.slot_len, L.own[r + 1] - L.own[r]);
+    // band rows each rank contributes to: rows whose column window meets its rows
+    L.tpart_len = 0;
+    for (int t = 0; t < 2; ++t) {
+      int acc = 0;
+      for (int r = 0; r < cs; ++r) {
+        int lo = B, hi = 0;
+        const int a = L.own[r], b = std::min(L.own[r + 1], B);
+        for (int i = 0; i < B && a < b; ++i) {
+          const int g = (i / NT + (t ? 0 : -1)) * NT;
+          if (g < b && g + bw > a) lo = std::min(lo, i), hi = std::max(hi, i + 1);
+        }
+        if (lo >= hi) lo = hi = 0;
+        L.tlo[t][r] = lo, L.thi[t][r] = hi, L.toff[t][r] = acc;
+        acc += hi - lo;
+      }
+      L.tpart_len = std::max(L.tpart_len, acc);
+    }
+    int st = 6;
+    while (st > 3 && smem_bytes(st, VL, cs, L.slot_len, L.tpart_len) > (size_t)kSmemMax) --st;
+    L.stages = st;
+  };
+  plan(CS);
+  if (CS == 16) {  // non-portable cluster size: only if 16-CTA clusters of this size are schedulable
+    const size_t smem = smem_bytes(L.stages, VL, 16, L.slot_len, L.tpart_len);
+    const void* fn = (const void*)sweep_fn(16, nbm);
     int nclus = 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16), cfg.blockDim = dim3(kSwThreads), cfg.dynamicSmemBytes = smem;
@@ -404,93 +583,111 @@ void GpuSolver::build_sweep_layout() {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 16, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr, cfg.numAttrs = 1;
-    if (cudaFuncSetAttribute((const void*)sweep_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute((const void*)sweep_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess ||
-        cudaOccupancyMaxActiveClusters(&nclus, (const void*)sweep_kernel<16>, &cfg) != cudaSuccess || nclus < NS) {
+    if (smem > (size_t)kSmemMax || cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg) != cudaSuccess || nclus < NS) {
       (void)cudaGetLastError();
-      sweep_cs_ = 8;
+      CS = 8;
+      plan(CS);
     }
   }
-  // schedules: output blocks -> (rank, warp) bins by longest-first greedy on
-  // tile counts; each rank issues its warps' tiles interleaved
-  const int CS = sweep_cs_, nbin = CS * kSwWarps;
+  if (smem_bytes(L.stages, VL, CS, L.slot_len, L.tpart_len) > (size_t)kSmemMax)
+    throw Error(1, "interior block too large for the sweep kernel's shared memory");
+  sweep_cs_ = CS;
+
+  // schedules.  D^-1: the lower tiles in row-major order, cut into CS x 4
+  // contiguous runs of equal work (rank-major; an off-diagonal tile costs a
+  // row and a column product, a diagonal one a row product); a rank streams its
+  // warps' tiles interleaved.  Bands: the chunks holding the rank's rows, dealt
+  // to the warps in turn.
+  const int nbin = CS * kSwWarps;
   std::vector<int4> sched((size_t)CS * T_N * kMaxSched, make_int4(0, 0, 0, 0));
   std::vector<int> nsched((size_t)CS * T_N, 0);
-  for (int t = 0; t < T_N; ++t) {
-    std::vector<int> order(nb);
-    for (int b = 0; b < nb; ++b) order[b] = b;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return blocks[t][a].size() > blocks[t][b].size(); });
-    std::vector<long long> load(nbin, 0);
-    std::vector<std::vector<int>> bins(nbin);
-    for (int b : order) {
-      if (blocks[t][b].empty()) continue;
-      const int bi = int(std::min_element(load.begin(), load.end()) - load.begin());
-      load[bi] += (long long)blocks[t][b].size();
-      bins[bi].push_back(b);
+  std::vector<int4> wsched((size_t)CS * T_N * kSwWarps * kMaxW, make_int4(0, 0, 0, 0));
+  std::vector<int> nwsched((size_t)CS * T_N * kSwWarps, 0);
+  auto push = [&](int q, int t, int w, int e, int flags, int key) {
+    int& n = nsched[q * T_N + t];
+    int& nw = nwsched[(q * T_N + t) * kSwWarps + w];
+    if (n >= kMaxSched || nw >= kMaxW) throw Error(1, "sweep: schedule too long");
+    sched[(size_t)(q * T_N + t) * kMaxSched + n] = make_int4(ent[e].x, ent[e].w, e, 0);
+    wsched[((size_t)(q * T_N + t) * kSwWarps + w) * kMaxW + nw] = make_int4(n, flags, key, ent[e].z);
+    ++n, ++nw;
+  };
+  {
+    std::vector<double> wt(n_sym);
+    double total = 0.0;
+    for (int e = 0; e < n_sym; ++e) {
+      const int I = ent[e].y >> 16, J = ent[e].y & 0xffff;
+      wt[e] = (I == J ? 1.0 : 2.0) * (ent[e].z >> 16), total += wt[e];
     }
-    for (int q = 0; q < CS; ++q) {
-      std::vector<std::vector<int4>> perw(kSwWarps);
-      for (int w = 0; w < kSwWarps; ++w)
-        for (int b : bins[q * kSwWarps + w]) {
-          const auto& tl = blocks[t][b];
-          for (size_t i = 0; i < tl.size(); ++i)
-            perw[w].push_back(make_int4(tl[i], w | int(i == 0) << 8 | int(i + 1 == tl.size()) << 9, b, 0));
-        }
-      int n = 0;
+    std::vector<std::vector<int>> bins(nbin);
+    double acc = 0.0;
+    int b = 0;
+    for (int e = 0; e < n_sym; ++e) {
+      while (b < nbin - 1 && acc + 0.5 * wt[e] > (b + 1) * total / nbin) ++b;
+      bins[b].push_back(e);
+      acc += wt[e];
+    }
+    for (int q = 0; q < CS; ++q)
       for (size_t i = 0;; ++i) {
         bool any = false;
-        for (int w = 0; w < kSwWarps; ++w)
-          if (i < perw[w].size()) {
-            if (n >= kMaxSched) throw Error(1, "sweep: schedule too long");
-            sched[(size_t)(q * T_N + t) * kMaxSched + n++] = perw[w][i];
-            any = true;
-          }
+        for (int w = 0; w < kSwWarps; ++w) {
+          const auto& tl = bins[q * kSwWarps + w];
+          if (i >= tl.size()) continue;
+          const int I = ent[tl[i]].y >> 16;
+          const bool first = i == 0 || (ent[tl[i - 1]].y >> 16) != I;
+          const bool last = i + 1 == tl.size() || (ent[tl[i + 1]].y >> 16) != I;
+          push(q, T_SYM, w, tl[i], int(first) | int(last) << 1, ent[tl[i]].y);
+          any = true;
+        }
         if (!any) break;
       }
-      nsched[q * T_N + t] = n;
-    }
   }
-  std::vector<int> raw(tabs.size() * 4), sraw(sched.size() * 4);
-  std::memcpy(raw.data(), tabs.data(), raw.size() * sizeof(int));
+  for (int t = 0; t < 2; ++t)
+    for (int q = 0; q < CS; ++q)
+      if (L.thi[t][q] > L.tlo[t][q])
+        for (int c = L.tlo[t][q] / Rb, i = 0; c <= (L.thi[t][q] - 1) / Rb; ++c, ++i)
+          push(q, T_BLO + t, i % kSwWarps, n_sym + t * nch + c, 0, c);
+  std::vector<int> raw(ent.size() * 4), sraw(sched.size() * 4), wraw(wsched.size() * 4);
+  std::memcpy(raw.data(), ent.data(), raw.size() * sizeof(int));
   std::memcpy(sraw.data(), sched.data(), sraw.size() * sizeof(int));
+  std::memcpy(wraw.data(), wsched.data(), wraw.size() * sizeof(int));
   sw_off.upload(raw);
   sw_cuts.upload(sraw);
   sw_ncut.upload(nsched);
-  sw_cs.upload(jmin);
-  SweepLayout L{};
-  L.tiles[0] = reinterpret_cast<const int4*>(sw_off.p);
-  L.tiles[1] = reinterpret_cast<const int4*>(sw_off.p) + n_inv;
+  sw_wcuts.upload(wraw);
+  sw_nw.upload(nwsched);
+  L.wsched = reinterpret_cast<const int4*>(sw_wcuts.p);
+  L.nwsched = sw_nw.p;
+  L.ent = reinterpret_cast<const int4*>(sw_off.p);
   L.sched = reinterpret_cast<const int4*>(sw_cuts.p);
   L.nsched = sw_ncut.p;
-  L.sub_off = sub_off, L.blk = blk, L.per_sub = (long long)H * blk;
-  L.B = B, L.H = H, L.nb = nb, L.VL = nb * kTile;
-  // ring depth: 6 x 32 KB stages when the shared memory (227 KB) allows (+1% at C2), else 5
-  L.stages = (6LL * kTileD + 3LL * nb * kTile + 20) * 8 <= 227 * 1024 ? 6 : 5;
-  if (const char* e = std::getenv("SGW_SWEEP_STAGES")) L.stages = std::max(2, std::min(8, std::atoi(e)));  // tuning hook
-  L.n_inv = n_inv, L.n_all = (int)tabs.size();
+  L.blk = blk, L.per_sub = (long long)H * blk;
+  L.B = B, L.H = H, L.nb = nb, L.VL = VL, L.NT = NT, L.Rb = Rb, L.bw = bw;
+  if (const char* e = std::getenv("SGW_SWEEP_STAGES"))  // tuning hook
+    L.stages = std::max(2, std::min(L.stages, std::atoi(e)));
+  L.n_sym = n_sym, L.n_ent = (int)ent.size();
   delete sweep_layout_;
   sweep_layout_ = new SweepLayout(L);
+  sweep_lo_off_ = lo_off, sweep_up_off_ = up_off, sweep_nch_ = nch, sweep_nbm_ = nbm;
   Fcomp.alloc(size_t(NS) * L.per_sub);
   const size_t smem = sweep_smem_bytes();
-  for (auto fn : {(const void*)sweep_kernel<1>, (const void*)sweep_kernel<2>, (const void*)sweep_kernel<4>,
-                  (const void*)sweep_kernel<8>, (const void*)sweep_kernel<16>})
-    SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (sweep_cs_ == 16)
-    SGW_CUDA(cudaFuncSetAttribute((const void*)sweep_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const void* fn = (const void*)sweep_fn(CS, nbm);
+  SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (CS == 16) SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
-// factor blocks of subdomains [b0, b0 + nb) (batch-local Linv / Lsub) -> tiles
-void GpuSolver::compact_factor_batch(int b0, int nb) {
+// A_{k+1,k} blocks of subdomains [b0, b0 + nb) (batch-local Lsub, before the
+// factorization overwrites them) -> the band chunks in Fcomp
+void GpuSolver::extract_band_batch(int b0, int nb) {
   const SweepLayout& L = *sweep_layout_;
+  if (L.H < 2) return;
   DBuf<unsigned long long> drop;
   drop.alloc(1);
   drop.zero(st_);
-  TileTabs T{L.tiles[0], L.n_inv, L.n_all};
-  compact_factor_kernel<<<8 * kNumSMs * 4, 256, 0, st_>>>(Linv.p, Lsub.p, Fcomp.p + (size_t)b0 * L.per_sub, T, sw_cs.p,
-                                                           L.sub_off, L.blk, L.B, L.H, nb, drop.p);
+  extract_band_kernel<<<8 * kNumSMs * 4, 256, 0, st_>>>(Lsub.p, Fcomp.p + (size_t)b0 * L.per_sub, L.B, L.H, L.NT, L.Rb,
+                                                        L.bw, sweep_nch_, L.blk, sweep_lo_off_, sweep_up_off_, nb,
+                                                        drop.p);
   SGW_LAUNCHED();
   unsigned long long h = 0;
   SGW_CUDA(cudaMemcpyAsync(&h, drop.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
@@ -498,17 +695,25 @@ void GpuSolver::compact_factor_batch(int b0, int nb) {
   if (h != 0) {
     double v;
     std::memcpy(&v, &h, sizeof(v));
-    throw Error(2, "interior factor: non-zero entry outside the block profile (" + std::to_string(v) + ")");
+    throw Error(2, "interior operator: grid-row coupling outside the S/SW band (" + std::to_string(v) + ")");
   }
-  Linv.reset();
-  Lsub.reset();
+}
+
+// D_k^-1 blocks of subdomains [b0, b0 + nb) (batch-local, dense) -> tiles
+void GpuSolver::compact_dinv_batch(int b0, int nb, const double* dinv) {
+  const SweepLayout& L = *sweep_layout_;
+  const long long nblk = (long long)nb * L.H * L.n_sym;
+  if (nblk >= (1LL << 31)) throw Error(1, "sweep: too many tiles per setup batch");
+  compact_dinv_kernel<<<(unsigned)nblk, 256, 0, st_>>>(dinv, Fcomp.p + (size_t)b0 * L.per_sub, L.ent, L.n_sym, L.blk,
+                                                       L.B, L.H);
+  SGW_LAUNCHED();
 }
 
 void destroy_sweep_layout(SweepLayout* p) { delete p; }
 
 size_t GpuSolver::sweep_smem_bytes() const {
   const SweepLayout& L = *sweep_layout_;
-  return (size_t)L.stages * kTileD * 8 + 16 * 8 + 4 * 8 + 3 * (size_t)L.VL * 8;
+  return smem_bytes(L.stages, L.VL, sweep_cs_, L.slot_len, L.tpart_len);
 }
 
 void GpuSolver::sweep(double* x) {
@@ -528,24 +733,20 @@ void GpuSolver::sweep(double* x) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const double* F = Fcomp.p;
-  switch (sweep_cs_) {
-    case 1: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<1>, x, F, L)); break;
-    case 2: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<2>, x, F, L)); break;
-    case 4: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<4>, x, F, L)); break;
-    case 8: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<8>, x, F, L)); break;
-    default: SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel<16>, x, F, L)); break;
-  }
+  SGW_CUDA(cudaLaunchKernelEx(&cfg, sweep_fn(sweep_cs_, sweep_nbm_), x, F, L));
   SGW_LAUNCHED();
   KP.end(st_);
 }
 
-// Algorithmic bytes of one forward + backward solve: every entry of the factor's
-// profile read once per direction (L_kk^-1 lower triangle; L_{k+1,k} right of c0(r)).
+// Algorithmic bytes of one forward + backward solve: D_k^-1 (unique entries)
+// once per grid row and direction except the shared last row (2H - 1 applies),
+// and the nonzero band of A_{k+1,k} once per direction (the first / last node
+// of a row has one neighbour node in the window).
 double GpuSolver::bytes_sweep() const {
   const SweepLayout& L = *sweep_layout_;
-  double inv = 0.5 * double(L.B) * (L.B + 1), sub = 0.0;
-  for (int r = 0; r < L.B; ++r) sub += double(L.B - std::max(0, r / NT - 1) * NT);
-  return 2.0 * 8.0 * double(NS) * (double(L.H) * inv + double(L.H - 1) * sub);
+  const double dinv = 0.5 * double(L.B) * (L.B + 1);
+  const double band = double(L.B) * L.bw - double(NT) * NT;
+  return 8.0 * double(NS) * (double(2 * L.H - 1) * dinv + 2.0 * double(L.H - 1) * band);
 }
 
 }  // namespace sgw
