@@ -95,6 +95,22 @@ __device__ __forceinline__ void tma_bulk_load(void* dst, const void* src, unsign
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Cross-CTA phase signals: every consumer thread of every rank arrives (release,
+// cluster scope: its own DSMEM pushes and earlier loads are ordered before)
+// on the target's barrier; the target's threads wait with acquire.
+__device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, int rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra WAITC_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 // split cluster barrier (release / acquire); legal for a cluster of one CTA
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive;" ::: "memory"); }
 __device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait;" ::: "memory"); }
@@ -187,6 +203,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   // positions, so a fast warp may reach a stage a full ring ahead of the tile
   // it holds; a parity wait alone would then match the previous phase.
   volatile int* ticket = reinterpret_cast<volatile int*>(empty + 8);
+  unsigned long long* slot_bar = empty + 12;   // partials of a D^-1 phase have arrived (CS > 1)
+  unsigned long long* tpart_bar = empty + 13;  // band partials of a band phase have arrived (CS > 1)
   double* wv = reinterpret_cast<double*>(smraw + (size_t)S * kTileD * 8 + 256);  // D^-1 input (full vector)
   double* red = wv + VL;                       // CTA sum of the warps' D^-1 partials
   double* zv = CS > 1 ? red + VL : red;        // D^-1 output, owned rows
@@ -204,6 +222,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) ticket[i] = -1;
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
+    mbar_init(slot_bar, CS * kSwWarps * 32);
+    mbar_init(tpart_bar, CS * kSwWarps * 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // b_0, read before the first cluster barrier (line 0 is rewritten only at the end)
@@ -238,16 +258,13 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
         }
         __syncwarp();
       }
-      // one cluster barrier closes every phase; arrive early, wait one late
-      if (seg > 0) cl_wait();
-      cl_arrive();
     }
-    cl_wait();
-    return;
+    return;  // the ring alone paces the stream: the producer runs ahead across phases
   }
 
   // -------------------------------------------------------- consumers ---
   long long pos = 0;
+  unsigned sph = 0, tph = 0;  // completed phases of slot_bar / tpart_bar
   for (int seg = 0; seg < nseg; ++seg) {
     int type, k;
     bool fwd;
@@ -258,6 +275,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       // w_k minus those of BUP_k).  The forward stores w_k for the backward pass.
       const int t = fwd ? 0 : 1;
       const bool band_in = !(fwd && k == 0);
+      if (CS > 1 && band_in) mbar_wait_cluster(tpart_bar, tph++ & 1u);
 #pragma unroll
       for (int u = 0; u < kPre; ++u) {
         const int i = tid + u * kSwWarps * 32;
@@ -347,9 +365,12 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
           double* dst = cluster.map_shared_rank(slots, r);
           dst[rank * L.slot_len + i - L.own[r]] = red[i];
         }
+#pragma unroll
+        for (int r = 0; r < CS; ++r) mbar_arrive_remote(slot_bar, r);
       }
     } else {
       // input z_k / x_{k+1}: the owned rows, summed over the ranks in order
+      if (CS > 1) mbar_wait_cluster(slot_bar, sph++ & 1u);
       if (CS > 1)
         for (int i = own_lo + tid; i < own_hi; i += kSwWarps * 32) {
           double v = 0.0;
@@ -409,12 +430,17 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
             for (int rr = 0; rr < CS; ++rr) dst[rr][to + i - tl] = val[u];
         }
       }
+      if (CS > 1) {
+#pragma unroll
+        for (int r = 0; r < CS; ++r) mbar_arrive_remote(tpart_bar, r);
+      } else {
+        consumers_sync();
+      }
     }
     pos += n;
-    cl_arrive();  // results pushed: one cluster barrier (also a CTA barrier) ends the phase
-    cl_wait();
   }
   // x_0 (the last phase was SYM_0): owned rows, ranks in order
+  if (CS > 1) mbar_wait_cluster(slot_bar, sph & 1u);
   for (int i = own_lo + tid; i < own_hi && i < B; i += kSwWarps * 32) {
     double v;
     if (CS > 1) {
