@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
 
   // --------------------------------------------------------- producer ---
   if (warp == kSwWarps) {
-    long long pos = 0;
+    unsigned pos = 0, st = 0, par = 1;  // par: parity of the release that frees stage st
     for (int seg = 0; seg < nseg; ++seg) {
       int type, k;
       bool fwd;
@@ -248,8 +248,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       const int n = L.nsched[rank * T_N + type];
       const double* base = Fs + k * L.blk;
       for (int p = 0; p < n; ++p, ++pos) {
-        const int st = int(pos % S);
-        if (pos >= S) mbar_wait(&empty[st], unsigned((pos / S) - 1) & 1u);
+        if (pos >= (unsigned)S) mbar_wait(&empty[st], par);
         if (lane == 0) {
           const int4 d = __ldg(sch + p);
           ticket[st] = int(pos);  // stage st now belongs to position pos (its previous tile is released)
@@ -257,14 +256,22 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
           tma_bulk_load(stage + (size_t)st * kTileD, base + d.x, unsigned(d.y), &full[st]);
         }
         __syncwarp();
+        if (++st == (unsigned)S) st = 0, par ^= 1u;
       }
     }
     return;  // the ring alone paces the stream: the producer runs ahead across phases
   }
 
   // -------------------------------------------------------- consumers ---
-  long long pos = 0;
+  unsigned pos = 0;
   unsigned sph = 0, tph = 0;  // completed phases of slot_bar / tpart_bar
+  // this warp's ring cursor: stream position cgp sits in stage cst, ring lap parity cpar
+  unsigned cgp = 0, cst = 0, cpar = 0;
+  auto seek = [&](unsigned gp) {
+    cst += gp - cgp;
+    cgp = gp;
+    while (cst >= (unsigned)S) cst -= S, cpar ^= 1u;
+  };
   for (int seg = 0; seg < nseg; ++seg) {
     int type, k;
     bool fwd;
@@ -309,8 +316,9 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       int4 e = __ldg(ws);
       for (int p = 0; p < nw; ++p) {
         const int4 en = __ldg(ws + min(p + 1, nw - 1));
-        const long long gp = pos + e.x;
-        const int st = int(gp % S);
+        const unsigned gp = pos + e.x;
+        seek(gp);
+        const int st = (int)cst;
         const int I = e.z >> 16, J = e.z & 0xffff, wp = e.w & 0xffff;
         const double* buf = stage + (size_t)st * kTileD;
         if (e.y & 1) {  // first tile of a row run
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
         }
         while (ticket[st] != int(gp)) {
         }
-        mbar_wait(&full[st], unsigned(gp / S) & 1u);
+        mbar_wait(&full[st], cpar);
         if (wp == kTile)
           tile_rows<kTile>(buf, wv + J * kTile, lane, wp, ra, rb);
         else  // the corner tile of a grid row whose width is not a multiple of 64 (diagonal)
@@ -391,13 +399,14 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       const int nw = L.nwsched[(rank * T_N + type) * kSwWarps + warp];
       for (int p = 0; p < nw; ++p) {
         const int4 e = __ldg(ws + p);
-        const long long gp = pos + e.x;
-        const int st = int(gp % S);
+        const unsigned gp = pos + e.x;
+        seek(gp);
+        const int st = (int)cst;
         const int q = e.z;
         const double* buf = stage + (size_t)st * kTileD;
         while (ticket[st] != int(gp)) {
         }
-        mbar_wait(&full[st], unsigned(gp / S) & 1u);
+        mbar_wait(&full[st], cpar);
         double val[2] = {0.0, 0.0};
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
