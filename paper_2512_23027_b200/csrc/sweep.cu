@@ -95,9 +95,10 @@ __device__ __forceinline__ void tma_bulk_load(void* dst, const void* src, unsign
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-// Cross-CTA phase signals: every consumer thread of every rank arrives (release,
-// cluster scope: its own DSMEM pushes and earlier loads are ordered before)
-// on the target's barrier; the target's threads wait with acquire.
+// Cross-CTA phase signals: after a CTA barrier over the consumers (which
+// orders every consumer thread's DSMEM pushes and earlier loads before it),
+// thread r arrives with release semantics at cluster scope on rank r's
+// barrier; the target's threads wait with acquire.
 __device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, int rank) {
   unsigned ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
@@ -183,9 +184,18 @@ __device__ __forceinline__ void tile_cols(const double* __restrict__ buf, const 
 // cx[j] += a, cy[j] += b for a warp-uniform runtime j (registers stay put)
 template <int NBM>
 __device__ __forceinline__ void add_at(double (&cx)[NBM], double (&cy)[NBM], int j, double a, double b) {
-#pragma unroll
-  for (int q = 0; q < NBM; ++q)
-    if (q == j) cx[q] += a, cy[q] += b;
+  switch (j) {  // warp-uniform: one indirect branch instead of NBM predicated adds
+#define SGW_CASE(q) \
+  case q:           \
+    if (q < NBM) cx[q < NBM ? q : 0] += a, cy[q < NBM ? q : 0] += b; \
+    break;
+    SGW_CASE(0) SGW_CASE(1) SGW_CASE(2) SGW_CASE(3) SGW_CASE(4) SGW_CASE(5) SGW_CASE(6) SGW_CASE(7)
+    SGW_CASE(8) SGW_CASE(9) SGW_CASE(10) SGW_CASE(11) SGW_CASE(12) SGW_CASE(13) SGW_CASE(14) SGW_CASE(15)
+    SGW_CASE(16) SGW_CASE(17) SGW_CASE(18) SGW_CASE(19) SGW_CASE(20) SGW_CASE(21) SGW_CASE(22) SGW_CASE(23)
+#undef SGW_CASE
+    default:
+      break;
+  }
 }
 
 template <int CS, int NBM>
@@ -222,8 +232,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) ticket[i] = -1;
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
-    mbar_init(slot_bar, CS * kSwWarps * 32);
-    mbar_init(tpart_bar, CS * kSwWarps * 32);
+    mbar_init(slot_bar, CS);
+    mbar_init(tpart_bar, CS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // b_0, read before the first cluster barrier (line 0 is rewritten only at the end)
@@ -373,8 +383,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
           double* dst = cluster.map_shared_rank(slots, r);
           dst[rank * L.slot_len + i - L.own[r]] = red[i];
         }
-#pragma unroll
-        for (int r = 0; r < CS; ++r) mbar_arrive_remote(slot_bar, r);
+        consumers_sync();  // every thread's pushes precede thread 0's release
+        if (tid < CS) mbar_arrive_remote(slot_bar, tid);
       }
     } else {
       // input z_k / x_{k+1}: the owned rows, summed over the ranks in order
@@ -439,12 +449,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
             for (int rr = 0; rr < CS; ++rr) dst[rr][to + i - tl] = val[u];
         }
       }
-      if (CS > 1) {
-#pragma unroll
-        for (int r = 0; r < CS; ++r) mbar_arrive_remote(tpart_bar, r);
-      } else {
-        consumers_sync();
-      }
+      consumers_sync();  // CS > 1: every thread's pushes precede the releases below
+      if (CS > 1 && tid < CS) mbar_arrive_remote(tpart_bar, tid);
     }
     pos += n;
   }
