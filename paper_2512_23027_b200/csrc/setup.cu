@@ -498,10 +498,10 @@ void GpuSolver::build_device_inputs(const Stencils& stc) {
     SgOpArgs& a = sgop_args_;
     sgop_tile_stencils(*sgop_, stc.Kg.data(), stc.Mg.data(), P.nx - 1, P.ny - 1, 1, NIN, kt, mt, a);
     Kp_.upload(kt), Mp_.upload(mt);
-    a.K = Kp_.p, a.M = Mp_.p;
+    a.K = Kp_.p, a.M = Mp_.p, a.Mg = Mg.p;
     a.xterm = a.yterm = n;
     a.xpitch = a.ypitch = P.nx - 1;
-    Xt_.alloc(sgop_xt_doubles(*sgop_, a));
+    if (sgop_packs_x(*sgop_)) Xt_.alloc(sgop_xt_doubles(*sgop_, a));
     a.xt = Xt_.p;
     yglob_.alloc(NSTATE);
   }

@@ -40,6 +40,7 @@ struct SgOpArgs {
   ll xterm, xitem, yterm, yitem;
   int W, H, xpitch, ypitch, tiles_x, tiles_y, items;
   double alpha, beta, gamma;
+  const double* Mg;                  // mass stencils in grid layout [item][4][H][W]
 };
 #define XW 34
 #define RUP16(v) (((v) + 15) / 16 * 16)
@@ -55,14 +56,20 @@ struct SgOpArgs {
 #define MBUF RUP16(MPI)
 #define KSTG RUP16(IC * KPI)
 #define NODES (32 * R)
-#define NC (R * G)                 /* warps; warp 0 also feeds the pipeline */
-#define NTHR (32 * NC)
+#define NC (R * G)                 /* consumer warps; PROD: warp NC feeds the pipeline, else warp 0 */
+#define NTHR (32 * (NC + PROD))
 
 extern __shared__ __align__(1024) double sm[];
+#if XG
+/* x and M come from global memory (L2-resident): the ring holds only K */
+#define KS (sm)
+#define REDSEP (sm + S * KSTG)
+#else
 #define XS (sm)
 #define MS (sm + 2 * XBUF)
 #define KS (sm + 2 * XBUF + 2 * MBUF)
 #define REDSEP (sm + 2 * XBUF + 2 * MBUF + S * KSTG)
+#endif
 #define BARS ((unsigned long long*)(REDSEP + (RED_ALIAS ? 0 : (G - 1) * NT * NODES)))
 #define KFULL(i) (BARS + (i))
 #define KEMPTY(i) (BARS + S + (i))
@@ -100,12 +107,14 @@ __device__ __forceinline__ void tile_coords(const SgOpArgs& A, int t, int& tx, i
 
 // x tile and M block of tile t into buffer t & 1 (two bulk copies, lane 0).
 __device__ __forceinline__ void load_xm(const SgOpArgs& A, int t, int lane) {
-  if (lane != 0) return;
+  if (XG || lane != 0) return;
   if (t >= 2) mbar_wait(XEMPTY(t & 1), (unsigned)((t >> 1) - 1) & 1u);
   const ll tile = blockIdx.x + t * gridDim.x;
   mbar_expect_tx(XFULL(t & 1), (unsigned)((XBUF + MPI) * 8));
+#if !XG
   bulk(XS + (t & 1) * XBUF, A.xt + tile * XBUF, XBUF * 8, XFULL(t & 1));
   bulk(MS + (t & 1) * MBUF, A.M + tile * MPI, MPI * 8, XFULL(t & 1));
+#endif
 }
 
 // K chunk q (stage q % S) of this CTA: IC input terms of its tile q / NCHUNK.
@@ -140,6 +149,12 @@ __device__ __forceinline__ void issue_k(const SgOpArgs& A, int q, int nst, int l
 #define K_W(ii) kb[(ii) * KPI + KOE + ly * 33 + lane]
 #define K_N(ii) kb[(ii) * KPI + KON + (ly + 1) * 32 + lane]
 #define K_S(ii) kb[(ii) * KPI + KON + ly * 32 + lane]
+#if PROD
+// the producer warp runs the ring ahead; consumers only wait for their chunk
+#define STAGE_IN(ch)                                                   \
+  mbar_wait(KFULL(s % S), (unsigned)(s / S) & 1u);                     \
+  kb = KS + (s % S) * KSTG;
+#else
 // warp 0 feeds the ring S - 2 chunks ahead (and the next tile's x / M at
 // mid-tile), then every warp waits for its chunk
 #define STAGE_IN(ch)                                                   \
@@ -150,10 +165,21 @@ __device__ __forceinline__ void issue_k(const SgOpArgs& A, int q, int nst, int l
   }                                                                    \
   mbar_wait(KFULL(s % S), (unsigned)(s / S) & 1u);                     \
   kb = KS + (s % S) * KSTG;
+#endif
 #define STAGE_OUT()                                                    \
   __syncwarp();                                                        \
   if (lane == 0) mbar_arrive(KEMPTY(s % S));                           \
   ++s;
+
+// producer warp: per tile its x / M buffer, then the tile's K chunks, paced by
+// the consumers' releases
+__device__ __forceinline__ void producer(const SgOpArgs& A, int mytiles, int nst, int lane) {
+  int q = 0;
+  for (int t = 0; t < mytiles; ++t) {
+    load_xm(A, t, lane);
+    for (int ch = 0; ch < NCHUNK; ++ch, ++q) issue_k(A, q, nst, lane);
+  }
+}
 
 @GROUPS@
 
@@ -169,18 +195,18 @@ extern "C" __global__ void __launch_bounds__(NTHR, 1) sgop_kernel(const SgOpArgs
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+#if PROD
+  if (warp == NC) {
+    producer(A, mytiles, nst, lane);
+    return;
+  }
+#else
   if (warp == 0) {
-    if (lane == 0)
-      for (int q = 0; q < PF; ++q)
-        if (q < nst) {
-          unsigned b;
-          const double* src = k_chunk(A, q, b);
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(b) : "memory");
-        }
     for (int q = 0; q < S - 2; ++q) issue_k(A, q, nst, lane);
     load_xm(A, 0, lane);
     __syncwarp();
   }
+#endif
   const int ly = warp / G, gq = warp % G;
   @DISPATCH@
 }
@@ -196,9 +222,10 @@ std::string dlit(double v) {
 }  // namespace
 
 struct SgOpJit {
-  int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255;
+  int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255, prod = 0;
   bool red_alias = true;  // partial sums reuse the tile's x buffer (after the mass step)
   bool jouter = false;    // k-resident code shape (see sgop_source)
+  bool xg = true;         // x and M read from global memory (no packed x tiles, K-only ring)
   size_t smem = 0;
   std::vector<double> coef;  // c_ijk in generated order (__constant__ gcoef)
   cudaLibrary_t lib = nullptr;
@@ -213,6 +240,7 @@ static long long sgop_smem_doubles(const SgOpJit& J) {
   const long long xw = 34;
   auto up = [](long long v) { return (v + 15) / 16 * 16; };
   const long long kpi = (97LL * J.R + 33) / 2 * 2, mpi = (130LL * J.R + 66) / 2 * 2;
+  if (J.xg) return J.S * up((long long)J.IC * kpi) + (long long)(J.G - 1) * J.NT * 32 * J.R + 2 * J.S + 4;
   return 2 * up(J.NT * (J.R + 2) * xw) + 2 * up(mpi) + J.S * up((long long)J.IC * kpi) +
          (J.red_alias ? 0 : (long long)(J.G - 1) * J.NT * 32 * J.R) + 2 * J.S + 4;  // + barriers
 }
@@ -243,16 +271,19 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   if (J->jouter) GI = 1;
   if (GJ > 6) return std::string();  // larger PCE bases: the generic kernel (step.cu)
   J->G = GJ * GI;
-  J->IC = J->jouter ? 4 : NIN >= 48 ? 12 : NIN >= 24 ? 4 : 2;
+  J->IC = J->jouter ? 4 : NIN >= 64 ? 16 : NIN >= 48 ? 12 : NIN >= 24 ? 4 : 2;  // measured at C2 (L2 flushed): 16 best
   if (const char* e = std::getenv("SGW_SGOP_IC")) J->IC = std::max(1, std::atoi(e));  // tuning hook
   const int jg = (NT + GJ - 1) / GJ;
   const int est = J->jouter ? 2 * (5 * J->IC + NT + 5) + 60 : 2 * (5 * jg + NT) + 80;
   J->NCHUNK = (NIN + J->IC - 1) / J->IC;
   J->R = std::max(1, std::min(16, 65536 / est / (32 * J->G)));
+  if (const char* e = std::getenv("SGW_SGOP_PROD")) J->prod = std::atoi(e) != 0;  // tuning hook: producer warp
   if (const char* e = std::getenv("SGW_SGOP_R")) J->R = std::max(1, std::atoi(e));  // tuning hook
   const long long budget = 220 * 1024 / 8;
+  if (const char* e = std::getenv("SGW_SGOP_XG")) J->xg = std::atoi(e) != 0;  // tuning hook
+  if (J->jouter) J->xg = false;
   for (;; --J->R) {
-    J->red_alias = (long long)(J->G - 1) * NT * 32 * J->R <= (long long)NT * (J->R + 2) * 34;
+    J->red_alias = !J->xg && (long long)(J->G - 1) * NT * 32 * J->R <= (long long)NT * (J->R + 2) * 34;
     J->S = 3;
     if (sgop_smem_doubles(*J) <= budget || J->R == 1) break;
   }
@@ -264,7 +295,8 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
     }
   }
   if (const char* e = std::getenv("SGW_SGOP_S")) J->S = std::max(3, std::atoi(e));  // tuning hook
-  J->regs = std::min(255, (65536 / (32 * J->R * J->G)) & ~7);
+  // registers are split per SM sub-partition: the warp count per partition sets the cap
+  J->regs = std::min(255, 16384 / (32 * ((J->R * J->G + J->prod + 3) / 4)) & ~7);
   const int R = J->R, G = J->G, IC = J->IC;
   // full (i, j) -> [(k, c)] expansion of the j <= k tensor (pce.hpp:24-40)
   std::map<std::pair<int, int>, std::vector<std::pair<int, double>>> pairs;
@@ -285,7 +317,14 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
     load[g] += wj[j] + 7;
   }
   // timing experiment only (SGW_SGOP_DBG=1): stream and synchronise, skip the stencil math
-  const bool dbg_nomath = std::getenv("SGW_SGOP_DBG") && std::atoi(std::getenv("SGW_SGOP_DBG")) >= 1;
+  const bool dbg_nomath = std::getenv("SGW_SGOP_DBG") && std::atoi(std::getenv("SGW_SGOP_DBG")) == 1;
+  // per pair: one 5-FMA chain (fewest issue slots) or two chains plus an add
+  // interleaving: NI input terms per block, NIL pair chains in flight
+  int NI = 2, NIL = 4;
+  bool lit = true;  // c_ijk as literals in the code (immediates when short) instead of constant-bank loads
+  if (const char* e = std::getenv("SGW_SGOP_LIT")) lit = std::atoi(e) != 0;  // tuning hook
+  if (const char* e = std::getenv("SGW_SGOP_NI")) NI = std::max(1, std::atoi(e));    // tuning hooks
+  if (const char* e = std::getenv("SGW_SGOP_NIL")) NIL = std::max(1, std::atoi(e));
   // generated per-group tile loops
   std::string groups, dispatch = "switch (gq) {\n";
   for (int g = 0; g < G; ++g) {
@@ -300,13 +339,28 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
     c += "  int s = 0;\n  for (int t = 0; t < mytiles; ++t) {\n";
     c += "    const int tile = blockIdx.x + t * gridDim.x;\n";
     c += "    const int tx = tile % A.tiles_x, ty = (tile / A.tiles_x) % A.tiles_y, it = tile / (A.tiles_x * A.tiles_y);\n";
-    c += "    double* xb = XS + (t & 1) * XBUF;\n    const double* mb = MS + (t & 1) * MBUF;\n";
+    if (J->xg) {
+      c += "    const int gx = tx * 32 + lane, gy = ty * R + ly;\n";
+      c += "    const bool valid = gx < A.W && gy < A.H;\n";
+      c += "    const bool hw = valid && gx > 0, he = valid && gx + 1 < A.W, hs = valid && gy > 0, hn = valid && gy + 1 < A.H;\n";
+      c += "    const double* xg = A.x + it * A.xitem + (ll)(valid ? gy : 0) * A.xpitch + (valid ? gx : 0);\n";
+      c += "#define XGV(j, dy, dx, ok) ((ok) ? __ldg(xg + (j) * A.xterm + (dy) * A.xpitch + (dx)) : 0.0)\n";
+    } else {
+      c += "    double* xb = XS + (t & 1) * XBUF;\n    const double* mb = MS + (t & 1) * MBUF;\n";
+    }
     c += "    const double* kb;\n    (void)tx, (void)ty;\n";
     for (int ch = 0; ch < J->NCHUNK; ++ch) {
-      if (ch == 0)  // x / M of this tile
+      if (ch == 0 && J->xg && !J->jouter)  // neighbourhoods from global memory before the first wait
+        for (int j : js) {
+          const std::string J0 = std::to_string(j);
+          c += "    const double x" + J0 + "c = XGV(" + J0 + ", 0, 0, valid), x" + J0 + "e = XGV(" + J0 +
+               ", 0, 1, he), x" + J0 + "w = XGV(" + J0 + ", 0, -1, hw), x" + J0 + "n = XGV(" + J0 +
+               ", 1, 0, hn), x" + J0 + "s = XGV(" + J0 + ", -1, 0, hs);\n";
+        }
+      if (ch == 0 && !J->xg)  // x / M of this tile
         c += "    mbar_wait(XFULL(t & 1), (unsigned)(t >> 1) & 1u);\n";
       c += "    STAGE_IN(" + std::to_string(ch) + ");\n";
-      if (ch == 0 && !J->jouter) {
+      if (ch == 0 && !J->jouter && !J->xg) {
         for (int j : js) {
           const std::string J0 = std::to_string(j);
           c += "    const double x" + J0 + "c = XV(" + J0 + ", 0, 0), x" + J0 + "e = XV(" + J0 + ", 0, 1), x" + J0 +
@@ -348,31 +402,88 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
         c += "    }\n    STAGE_OUT();\n";
         continue;
       }
-      for (int i = ch * IC; i < std::min(NIN, (ch + 1) * IC); ++i) {
-        if (i % GI != igrp) continue;
-        std::string body;
-        for (int j : js) {
-          auto it = pairs.find({i, j});
-          if (it == pairs.end()) continue;
-          const std::string J0 = std::to_string(j);
-          body += "      { const double v = fma(kd, x" + J0 + "c, ke * x" + J0 + "e) + fma(kw, x" + J0 +
-                  "w, fma(kn, x" + J0 + "n, ks * x" + J0 + "s));\n";
-          for (auto& kc : it->second) {
-            body += "        y" + std::to_string(kc.first) + " = fma(gcoef[" + std::to_string(J->coef.size()) +
-                    "], v, y" + std::to_string(kc.first) + ");\n";
-            J->coef.push_back(kc.second);
+      // pairs of NI consecutive input terms at a time, their 5-FMA chains
+      // interleaved term by term (independent chains hide the DFMA latency)
+      std::vector<int> iis;
+      for (int i = ch * IC; i < std::min(NIN, (ch + 1) * IC); ++i)
+        if (i % GI == igrp) iis.push_back(i);
+      for (size_t b = 0; b < iis.size() && !dbg_nomath; b += NI) {
+        struct P { std::string ki, xj; const std::vector<std::pair<int, double>>* kc; };
+        std::vector<P> ps;
+        std::string kdecl;
+        for (size_t u = b; u < std::min(iis.size(), b + NI); ++u) {
+          const int i = iis[u];
+          const std::string ii = std::to_string(i - ch * IC), K = "k" + std::to_string(u - b);
+          bool any = false;
+          for (int j : js) {
+            auto it = pairs.find({i, j});
+            if (it == pairs.end()) continue;
+            ps.push_back({K, "x" + std::to_string(j), &it->second});
+            any = true;
           }
-          body += "      }\n";
+          if (any)
+            kdecl += "      const double " + K + "d = K_D(" + ii + "), " + K + "e = K_E(" + ii + "), " + K + "w = K_W(" + ii +
+                     "), " + K + "n = K_N(" + ii + "), " + K + "s = K_S(" + ii + ");\n";
         }
-        if (body.empty() || dbg_nomath) continue;
-        const std::string ii = std::to_string(i - ch * IC);
-        c += "    {\n      const double kd = K_D(" + ii + "), ke = K_E(" + ii + "), kw = K_W(" + ii + "), kn = K_N(" + ii +
-             "), ks = K_S(" + ii + ");\n" + body + "    }\n";
+        if (ps.empty()) continue;
+        c += "    {\n" + kdecl;
+        for (size_t q0 = 0; q0 < ps.size(); q0 += NIL) {
+          const size_t q1 = std::min(ps.size(), q0 + NIL);
+          std::string l0 = "      double", l1, l2, l3, l4, l5;
+          for (size_t q = q0; q < q1; ++q) {
+            const std::string v = "v" + std::to_string(q - q0), &k = ps[q].ki, &x = ps[q].xj;
+            l0 += std::string(q == q0 ? " " : ", ") + v + " = " + k + "d * " + x + "c";
+            l1 += "      " + v + " = fma(" + k + "e, " + x + "e, " + v + ");\n";
+            l2 += "      " + v + " = fma(" + k + "w, " + x + "w, " + v + ");\n";
+            l3 += "      " + v + " = fma(" + k + "n, " + x + "n, " + v + ");\n";
+            l4 += "      " + v + " = fma(" + k + "s, " + x + "s, " + v + ");\n";
+            for (auto& kc : *ps[q].kc) {
+              const std::string cf = lit ? dlit(kc.second) : "gcoef[" + std::to_string(J->coef.size()) + "]";
+              l5 += "      y" + std::to_string(kc.first) + " = fma(" + cf + ", " + v + ", y" + std::to_string(kc.first) +
+                    ");\n";
+              J->coef.push_back(kc.second);
+            }
+          }
+          c += "      {\n" + l0 + ";\n" + l1 + l2 + l3 + l4 + l5 + "      }\n";
+        }
+        c += "    }\n";
       }
       c += "    STAGE_OUT();\n";
     }
     // mass on own terms (owner groups), then the fixed-order sum of the G partials
-    if (owner) {
+    auto emit_q = [&]() {
+    // gamma M x2 on own terms, only when x2 is given (a uniform branch); inside,
+    // predicated loads (no branches) so that all of them are in flight together
+    for (int k : js) c += "    double q" + std::to_string(k) + " = 0.0;\n";
+    c += "    if (A.x2 && valid) {\n";
+    c += "      const double* x2p = A.x2 + it * A.xitem + (ll)gy * A.xpitch + gx;\n";
+    c += "      const bool zE = gx + 1 < A.W, zW = gx > 0, zN = gy + 1 < A.H, zS = gy > 0;\n";
+    for (int k : js) {
+      const std::string K0 = std::to_string(k);
+      c += "      { const double* p = x2p + " + K0 + " * A.xterm;\n";
+      c += "        const double a0 = __ldg(p), a1 = zE ? __ldg(p + 1) : 0.0, a2 = zW ? __ldg(p - 1) : 0.0, "
+           "a3 = zN ? __ldg(p + A.xpitch) : 0.0, a4 = zS ? __ldg(p - A.xpitch) : 0.0, "
+           "a5 = (zN && zE) ? __ldg(p + A.xpitch + 1) : 0.0, a6 = (zS && zW) ? __ldg(p - A.xpitch - 1) : 0.0;\n";
+      c += "        q" + K0 + " = fma(msw, a6, fma(mne, a5, fma(ms_, a4, fma(mn, a3, fma(mw, a2, fma(me, a1, md * a0)))))); }\n";
+    }
+    c += "    }\n";
+    };
+    if (owner && J->xg) {
+    // mass stencil M [item][4][H][W] (diag, E, N, NE) from global memory
+    c += "    const ll pl = (ll)A.W * A.H;\n";
+    c += "    const double* mg = A.Mg + it * 4 * pl + (ll)(valid ? gy : 0) * A.W + (valid ? gx : 0);\n";
+    c += "    const double md = valid ? __ldg(mg) : 0.0, me = valid ? __ldg(mg + pl) : 0.0, mw = hw ? __ldg(mg + pl - 1) : 0.0, "
+         "mn = valid ? __ldg(mg + 2 * pl) : 0.0, ms_ = hs ? __ldg(mg + 2 * pl - A.W) : 0.0, "
+         "mne = valid ? __ldg(mg + 3 * pl) : 0.0, msw = (hs && hw) ? __ldg(mg + 3 * pl - A.W - 1) : 0.0;\n";
+    for (int k : js) {
+      const std::string K0 = std::to_string(k);
+      c += "    double m" + K0 + " = fma(md, x" + K0 + "c, fma(me, x" + K0 + "e, fma(mw, x" + K0 + "w, fma(mn, x" + K0 +
+           "n, fma(ms_, x" + K0 + "s, fma(mne, XGV(" + K0 + ", 1, 1, hn && he), msw * XGV(" + K0 +
+           ", -1, -1, hs && hw)))))));\n";
+    }
+    emit_q();
+    }
+    if (owner && !J->xg) {
     c += "    const double md = mb[ly * 32 + lane], me = mb[KOE + ly * 33 + lane + 1], mw = mb[KOE + ly * 33 + lane], "
          "mn = mb[MON + (ly + 1) * 32 + lane], ms_ = mb[MON + ly * 32 + lane], mne = mb[MONE + (ly + 1) * 33 + lane + 1], "
          "msw = mb[MONE + ly * 33 + lane];\n";
@@ -388,19 +499,8 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
         c += "    double m" + K0 + " = fma(md, x" + K0 + "c, fma(me, x" + K0 + "e, fma(mw, x" + K0 + "w, fma(mn, x" + K0 +
              "n, fma(ms_, x" + K0 + "s, fma(mne, XV(" + K0 + ", 1, 1), msw * XV(" + K0 + ", -1, -1)))))));\n";
     }
-    for (int k : js) c += "    double q" + std::to_string(k) + " = 0.0;\n";
-    c += "    if (A.x2 && valid) {\n      const double* x2 = A.x2 + it * A.xitem + (ll)gy * A.xpitch + gx;\n";
-    c += "      const bool hw = gx > 0, he = gx + 1 < A.W, hs = gy > 0, hn = gy + 1 < A.H;\n";
-    for (int k : js) {
-      const std::string K0 = std::to_string(k);
-      c += "      { const double* p = x2 + " + K0 + " * A.xterm;\n";
-      c += "        double q = md * p[0];\n        if (he) q = fma(me, p[1], q);\n        if (hw) q = fma(mw, p[-1], q);\n";
-      c += "        if (hn) q = fma(mn, p[A.xpitch], q);\n        if (hs) q = fma(ms_, p[-A.xpitch], q);\n";
-      c += "        if (hn && he) q = fma(mne, p[A.xpitch + 1], q);\n        if (hs && hw) q = fma(msw, p[-A.xpitch - 1], q);\n";
-      c += "        q" + K0 + " = q; }\n";
-    }
-    c += "    }\n";
-    } else {
+    emit_q();
+    } else if (!owner && !J->xg) {
       c += "    const int gx = tx * 32 + lane, gy = ty * R + ly;\n    (void)gx, (void)gy, (void)it;\n";
     }
     c += J->red_alias ? "    consumers_sync();  // everyone is done with xb (mass step) / red (previous tile)\n    double* red = xb;\n"
@@ -429,14 +529,20 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
       c += "      yo[" + K0 + " * A.yterm] = fma(A.beta, " + sum + ", fma(A.alpha, m" + K0 + ", A.gamma * q" + K0 + "));\n";
     }
     if (owner) c += "    }\n";
-    c += "    __syncwarp();\n    if (lane == 0) mbar_arrive(XEMPTY(t & 1));  // x / M (and red) buffer free\n  }\n}\n";
+    if (J->xg)
+      c += "  }\n}\n#undef XGV\n";
+    else
+      c += "    __syncwarp();\n    if (lane == 0) mbar_arrive(XEMPTY(t & 1));  // x / M (and red) buffer free\n  }\n}\n";
     groups += c;
     dispatch += "    case " + std::to_string(g) + ": group" + std::to_string(g) + "(A, ly, lane, warp, mytiles, nst); break;\n";
   }
   dispatch += "  }";
+  // timing experiment only (SGW_SGOP_DBG=2): every warp runs group 0's code (half the code footprint)
+  if (std::getenv("SGW_SGOP_DBG") && std::atoi(std::getenv("SGW_SGOP_DBG")) == 2)
+    dispatch.replace(dispatch.find("switch (gq)"), 11, "switch (0)");
   int pf = 0;  // measured: L2 prefetch beyond the ring does not help here
   if (const char* e = std::getenv("SGW_SGOP_PF")) pf = std::max(0, std::atoi(e));  // tuning hook
-  std::string src = "#define PF " + std::to_string(pf) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
+  std::string src = "#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
                     "\n#define NT " + std::to_string(NT) + "\n#define NIN " + std::to_string(NIN) +
                     "\n#define R " + std::to_string(R) + "\n#define G " + std::to_string(G) + "\n#define IC " +
                     std::to_string(IC) + "\n#define S " + std::to_string(J->S) + "\n#define NCHUNK " +
@@ -554,9 +660,11 @@ void sgop_tile_stencils(const SgOpJit& J, const double* K, const double* M, int 
   a.W = W, a.H = H, a.tiles_x = tx_n, a.tiles_y = ty_n, a.items = items;
 }
 
+bool sgop_packs_x(const SgOpJit& J) { return !J.xg; }
+
 void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st) {
   const int tiles = a.tiles_x * a.tiles_y * a.items;
-  {
+  if (!J.xg) {
     const long long xbuf = ((long long)J.NT * (J.R + 2) * 34 + 15) / 16 * 16;
     const long long tot = (long long)tiles * J.NT * (J.R + 2) * 34;
     sgop_pack_x_kernel<<<(unsigned)std::min<long long>((tot + 255) / 256, 8 * kNumSMs * 4), 256, 0, st>>>(
@@ -566,7 +674,7 @@ void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st) {
   }
   const int grid = std::max(1, std::min(tiles, kNumSMs));
   void* args[] = {const_cast<SgOpArgs*>(&a)};
-  SGW_CUDA(cudaLaunchKernel((const void*)J.kern, dim3(grid), dim3(32 * J.R * J.G), args, J.smem, st));
+  SGW_CUDA(cudaLaunchKernel((const void*)J.kern, dim3(grid), dim3(32 * (J.R * J.G + J.prod)), args, J.smem, st));
   SGW_LAUNCHED();
 }
 

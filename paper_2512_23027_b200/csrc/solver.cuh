@@ -40,11 +40,13 @@ struct SgOpArgs {
   long long xterm, xitem, yterm, yitem;
   int W, H, xpitch, ypitch, tiles_x, tiles_y, items;
   double alpha, beta, gamma;
+  const double* Mg;  // mass stencils in grid layout [item][4][H][W] (read directly by the kernel)
 };
 struct SgOpJit;
 std::shared_ptr<SgOpJit> build_sgop(int NT, int NIN, const TensorHost& T);
 void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st);
 int sgop_rows(const SgOpJit& J);
+bool sgop_packs_x(const SgOpJit& J);  // the operator reads x through packed tiles (scratch sgop_xt_doubles)
 long long sgop_xt_doubles(const SgOpJit& J, const SgOpArgs& a);
 // Tile-major copies of grid stencils K [item][i][3][H][W], M [item][4][H][W]
 // (row-major, pitch W) in the operator's tile order; sets a.tiles_x/tiles_y.

@@ -93,8 +93,8 @@ void GpuSolver::apply_block(int op, const double* x, double* y) {
     SGW_LAUNCHED();
   } else {
     SgOpArgs a = sgop_args_;
-    a.x = x, a.x2 = nullptr, a.y = y;
-    a.alpha = cm, a.beta = ck, a.gamma = 0.0;
+    a.x = x, a.x2 = op == 3 ? x : nullptr, a.y = y;  // op 3: the step's form (+ M x2), for benchmarks
+    a.alpha = cm, a.beta = ck, a.gamma = op == 3 ? 1.0 : 0.0;
     launch_sgop(*sgop_, a, st_);
   }
   KP.end(st_);
@@ -448,17 +448,32 @@ void GpuSolver::gather_state(double* dst) {
 // Interior rows of the local force from the global operator: the stencil of a
 // subdomain-interior node only touches that subdomain's elements, so its local
 // row equals the global row (f_ext added on term 0, weight 1).
+// The JIT operator's y = a0 M uc + a1 sum c K uc arrives in yg; the mass term
+// of um (M um_k, a 7-point stencil) is added here, where the loads are cheap.
 __global__ void interior_from_global_kernel(LocalArgs A, int n, const double* __restrict__ yg,
+                                            const double* __restrict__ Mg, const double* __restrict__ um,
                                             const double* __restrict__ fnext, int fdof, double fval,
                                             double* __restrict__ yI, int ns) {
   const long long total = (long long)ns * A.H * A.B;
+  const int rw = A.nx - 1, rh = A.ny - 1;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int row = int(t % A.B), jl = int((t / A.B) % A.H) + 1, s = int(t / ((long long)A.B * A.H));
     const int il = row / A.nt + 1, k = row % A.nt;
     const int lid = jl * (A.mx + 1) + il;
     if (A.lid_to_p[(long long)s * A.nl + lid] != -2) continue;  // unit row of a ragged block
     const int d = lid_dof(A, s, il, jl);
-    double f = yg[(long long)k * n + d];
+    const int gi = d % rw, gj = d / rw;
+    const double* uk = um + (long long)k * n;
+    double q = 0.0;
+#pragma unroll
+    for (int dir = 0; dir < 7; ++dir) {
+      const int i2 = gi + sDI[dir], j2 = gj + sDJ[dir];
+      if (i2 >= 0 && i2 < rw && j2 >= 0 && j2 < rh) {
+        const int nb = j2 * rw + i2;
+        q += mco(Mg, n, d, nb, dir) * __ldg(uk + nb);
+      }
+    }
+    double f = yg[(long long)k * n + d] + q;
     if (k == 0) {
       if (fnext) f += fnext[d];
       else if (d == fdof) f += fval;
@@ -483,8 +498,8 @@ int GpuSolver::step(int* iters_out) {
     // interior rows: f = M um + a0 M uc + a1 sum c K uc on the global grid (JIT
     // operator), copied into the block rows; interface rows: local stencils
     SgOpArgs sa = sgop_args_;
-    sa.x = uc.p, sa.x2 = um.p, sa.y = yglob_.p;
-    sa.alpha = P.alpha0, sa.beta = P.alpha1, sa.gamma = 1.0;
+    sa.x = uc.p, sa.x2 = nullptr, sa.y = yglob_.p;  // + M um in interior_from_global_kernel
+    sa.alpha = P.alpha0, sa.beta = P.alpha1, sa.gamma = 0.0;
     {
       cudaEvent_t e0;
       KP.begin(K_SGOP, st_, &e0);
@@ -492,8 +507,8 @@ int GpuSolver::step(int* iters_out) {
       KP.end(st_);
     }
     const long long tI = (long long)NS * G.H * B;
-    interior_from_global_kernel<<<std::min(cdiv(tI, 256), 65535), 256, 0, st_>>>(A, n, yglob_.p, fvec, fdof, fval,
-                                                                                   yI.p, NS);
+    interior_from_global_kernel<<<std::min(cdiv(tI, 256), 65535), 256, 0, st_>>>(A, n, yglob_.p, Mg.p, um.p, fvec,
+                                                                                   fdof, fval, yI.p, NS);
     SGW_LAUNCHED();
     local_force_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
         A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, yI.p, fG.p, NS, ilist_.p,

@@ -507,7 +507,8 @@ class SgSolver:
         return out
 
     def bench_kernel(self, which, reps=20):
-        """Average device ms of one Schur matvec (0), NN2 apply (1) or SG-operator apply (2)."""
+        """Average device ms of one Schur matvec (0), NN2 apply (1), SG-operator apply (2) or the
+        step's SG-operator form with the mass term of a second input (3)."""
         o = np.zeros(1)
         _check(load_library().sgw_bench_kernel(self._h, which, reps, _p(o)))
         return float(o[0])

@@ -20,7 +20,8 @@ nx = c["nx"]
 coeff = sg.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
 t = sg.triple_products(c["L"], c["p_in"], c["p_out"])
 s = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, t, params=sg.NewmarkParams(dt=c["dt"]))
-ms = s.bench_kernel(2, reps=reps)
+which = int(os.environ.get("SGOP_WHICH", "2"))  # 3: the step's form with the M x2 term
+ms = s.bench_kernel(which, reps=reps)
 n = (nx - 1) ** 2
 pairs = len({(i, j) for i, j, k in zip(t.i, t.j, t.k)} | {(i, k) for i, j, k in zip(t.i, t.j, t.k)})
 nbytes = 8.0 * n * (3 * t.n_input + 2 * t.n_output)

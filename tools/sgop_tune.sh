@@ -1,9 +1,17 @@
+#!/bin/bash
+# SG-operator shape sweep (standalone apply at C2); one line per config in gpurun_out/sgop_tune.log
 set -u
-for cfg in "jout 0 0 0" "jout 4 0 0" "jout 2 6 0" "jout 2 4 0" "xres 0 0 0"; do
-  set -- $cfg
-  env="SGW_SGOP_MODE=$1"
-  [ "$2" != "0" ] && env="$env SGW_SGOP_R=$2"
-  [ "$3" != "0" ] && env="$env SGW_SGOP_IC=$3"
+mkdir -p gpurun_out
+: > gpurun_out/sgop_tune.log
+while read -r cfg; do
+  [ -z "$cfg" ] && continue
   echo "== $cfg" >> gpurun_out/sgop_tune.log
-  env $env timeout 300 python tools/sgop_bench.py C2 20 >> gpurun_out/sgop_tune.log 2>&1
-done
+  env $cfg timeout 300 python tools/sgop_bench.py C2 20 2>&1 | tail -1 >> gpurun_out/sgop_tune.log
+done <<'CFGS'
+SGW_SGOP_X=0
+SGOP_WHICH=3
+SGW_SGOP_IC=21
+SGW_SGOP_IC=28
+SGW_SGOP_IC=16 SGW_SGOP_S=4
+SGW_SGOP_PROD=1 SGW_SGOP_R=3 SGW_SGOP_IC=16
+CFGS
