@@ -75,6 +75,7 @@ extern __shared__ __align__(1024) double sm[];
 #define KEMPTY(i) (BARS + S + (i))
 #define XFULL(i) (BARS + 2 * S + (i))
 #define XEMPTY(i) (BARS + 2 * S + 2 + (i))
+#define KCNT ((int*)(BARS + 2 * S + 4))  /* LA: per-stage release counters */
 __constant__ double gcoef[NCOEF];
 
 __device__ __forceinline__ unsigned su(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -140,6 +141,16 @@ __device__ __forceinline__ void issue_k(const SgOpArgs& A, int q, int nst, int l
   bulk(KS + (q % S) * KSTG, src, bytes, KFULL(q % S));
 }
 
+// LA: issue chunk q into its (released) stage, no wait
+__device__ __forceinline__ void issue_k_now(const SgOpArgs& A, int q, int nst) {
+  if (q >= nst) return;
+  unsigned bytes;
+  const double* src = k_chunk(A, q, bytes);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(KFULL(q % S), bytes);
+  bulk(KS + (q % S) * KSTG, src, bytes, KFULL(q % S));
+}
+
 // shared-memory reads of the current tile: x (center at [ly+1][lane+1]);
 // K of input term ii: own diag / E / N, west neighbour's E, south neighbour's N;
 // M likewise plus own NE and the south-west neighbour's NE
@@ -154,6 +165,14 @@ __device__ __forceinline__ void issue_k(const SgOpArgs& A, int q, int nst, int l
 #define STAGE_IN(ch)                                                   \
   mbar_wait(KFULL(s % S), (unsigned)(s / S) & 1u);                     \
   kb = KS + (s % S) * KSTG;
+#elif LA
+#define STAGE_IN(ch)                                                   \
+  if (warp == 0 && (ch) == NCHUNK / 2 && t + 1 < mytiles) {            \
+    load_xm(A, t + 1, lane);                                           \
+    __syncwarp();                                                      \
+  }                                                                    \
+  mbar_wait(KFULL(s % S), (unsigned)(s / S) & 1u);                     \
+  kb = KS + (s % S) * KSTG;
 #else
 // warp 0 feeds the ring S - 2 chunks ahead (and the next tile's x / M at
 // mid-tile), then every warp waits for its chunk
@@ -166,10 +185,24 @@ __device__ __forceinline__ void issue_k(const SgOpArgs& A, int q, int nst, int l
   mbar_wait(KFULL(s % S), (unsigned)(s / S) & 1u);                     \
   kb = KS + (s % S) * KSTG;
 #endif
+#if LA
+// the last warp to release a stage refills it at once (S chunks in flight)
+#define STAGE_OUT()                                                    \
+  __syncwarp();                                                        \
+  if (lane == 0) {                                                     \
+    __threadfence_block();                                             \
+    if (atomicAdd(KCNT + s % S, 1) == NC - 1) {                        \
+      KCNT[s % S] = 0;                                                 \
+      issue_k_now(A, s + S, nst);                                      \
+    }                                                                  \
+  }                                                                    \
+  ++s;
+#else
 #define STAGE_OUT()                                                    \
   __syncwarp();                                                        \
   if (lane == 0) mbar_arrive(KEMPTY(s % S));                           \
   ++s;
+#endif
 
 // producer warp: per tile its x / M buffer, then the tile's K chunks, paced by
 // the consumers' releases
@@ -190,7 +223,7 @@ extern "C" __global__ void __launch_bounds__(NTHR, 1) sgop_kernel(const SgOpArgs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nst = mytiles * NCHUNK;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(KFULL(i), 1), mbar_init(KEMPTY(i), NC);
+    for (int i = 0; i < S; ++i) mbar_init(KFULL(i), 1), mbar_init(KEMPTY(i), NC), KCNT[i] = 0;
     for (int i = 0; i < 2; ++i) mbar_init(XFULL(i), 1), mbar_init(XEMPTY(i), NC);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -199,6 +232,13 @@ extern "C" __global__ void __launch_bounds__(NTHR, 1) sgop_kernel(const SgOpArgs
   if (warp == NC) {
     producer(A, mytiles, nst, lane);
     return;
+  }
+#elif LA
+  if (threadIdx.x == 0)
+    for (int q = 0; q < S; ++q) issue_k_now(A, q, nst);
+  if (warp == 0) {
+    load_xm(A, 0, lane);
+    __syncwarp();
   }
 #else
   if (warp == 0) {
@@ -222,7 +262,7 @@ std::string dlit(double v) {
 }  // namespace
 
 struct SgOpJit {
-  int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255, prod = 0;
+  int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255, prod = 0, la = 0;
   bool red_alias = true;  // partial sums reuse the tile's x buffer (after the mass step)
   bool jouter = false;    // k-resident code shape (see sgop_source)
   bool xg = true;         // x and M read from global memory (no packed x tiles, K-only ring)
@@ -240,9 +280,9 @@ static long long sgop_smem_doubles(const SgOpJit& J) {
   const long long xw = 34;
   auto up = [](long long v) { return (v + 15) / 16 * 16; };
   const long long kpi = (97LL * J.R + 33) / 2 * 2, mpi = (130LL * J.R + 66) / 2 * 2;
-  if (J.xg) return J.S * up((long long)J.IC * kpi) + (long long)(J.G - 1) * J.NT * 32 * J.R + 2 * J.S + 4;
+  if (J.xg) return J.S * up((long long)J.IC * kpi) + (long long)(J.G - 1) * J.NT * 32 * J.R + 3 * J.S + 4;
   return 2 * up(J.NT * (J.R + 2) * xw) + 2 * up(mpi) + J.S * up((long long)J.IC * kpi) +
-         (J.red_alias ? 0 : (long long)(J.G - 1) * J.NT * 32 * J.R) + 2 * J.S + 4;  // + barriers
+         (J.red_alias ? 0 : (long long)(J.G - 1) * J.NT * 32 * J.R) + 3 * J.S + 4;  // + barriers, counters
 }
 
 // CUDA source of the operator specialised for (NT, NIN, T); fills J's shape.
@@ -278,6 +318,8 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   J->NCHUNK = (NIN + J->IC - 1) / J->IC;
   J->R = std::max(1, std::min(16, 65536 / est / (32 * J->G)));
   if (const char* e = std::getenv("SGW_SGOP_PROD")) J->prod = std::atoi(e) != 0;  // tuning hook: producer warp
+  if (const char* e = std::getenv("SGW_SGOP_LA")) J->la = std::atoi(e) != 0;      // tuning hook: last-arriver refill
+  if (J->prod) J->la = 0;
   if (const char* e = std::getenv("SGW_SGOP_R")) J->R = std::max(1, std::atoi(e));  // tuning hook
   const long long budget = 220 * 1024 / 8;
   if (const char* e = std::getenv("SGW_SGOP_XG")) J->xg = std::atoi(e) != 0;  // tuning hook
@@ -542,7 +584,7 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
     dispatch.replace(dispatch.find("switch (gq)"), 11, "switch (0)");
   int pf = 0;  // measured: L2 prefetch beyond the ring does not help here
   if (const char* e = std::getenv("SGW_SGOP_PF")) pf = std::max(0, std::atoi(e));  // tuning hook
-  std::string src = "#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
+  std::string src = "#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
                     "\n#define NT " + std::to_string(NT) + "\n#define NIN " + std::to_string(NIN) +
                     "\n#define R " + std::to_string(R) + "\n#define G " + std::to_string(G) + "\n#define IC " +
                     std::to_string(IC) + "\n#define S " + std::to_string(J->S) + "\n#define NCHUNK " +

@@ -9,9 +9,11 @@ while read -r cfg; do
   env $cfg timeout 300 python tools/sgop_bench.py C2 20 2>&1 | tail -1 >> gpurun_out/sgop_tune.log
 done <<'CFGS'
 SGW_SGOP_X=0
+SGW_SGOP_LA=0
+SGW_SGOP_IC=12
+SGW_SGOP_IC=8
+SGW_SGOP_IC=6
+SGW_SGOP_DBG=1
+SGW_SGOP_IC=8 SGW_SGOP_DBG=1
 SGOP_WHICH=3
-SGW_SGOP_IC=21
-SGW_SGOP_IC=28
-SGW_SGOP_IC=16 SGW_SGOP_S=4
-SGW_SGOP_PROD=1 SGW_SGOP_R=3 SGW_SGOP_IC=16
 CFGS
