@@ -19,6 +19,7 @@
 // the true residual are evaluated on device exactly as src/pcg.cpp:30-40.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "solver.cuh"
@@ -27,6 +28,24 @@
 namespace cg = cooperative_groups;
 
 namespace sgw {
+
+// A TilePack walked in contiguous tile ranges, one per CTA (tiles are ordered
+// matrix by matrix, row-major over the lower tiles (I, J <= I)).  A CTA keeps
+// the local input vector of its current matrix and a local accumulator in
+// shared memory, adds every tile's row and column products into it, and at
+// a matrix boundary writes the accumulator as its partial of that matrix:
+// y_s = sum over the CTAs covering s of their partials, in CTA order.
+struct RangePack {
+  const double* tiles;
+  const int* nt;              // tiles per side, per matrix
+  const long long* xoff;      // local vector offset per matrix (padded, 64 nt)
+  const long long* t_first;   // [G + 1] first tile of each CTA's range
+  const int4* start;          // [G] {matrix, I, J} of each CTA's first tile
+  const int* c0;              // per matrix: first CTA covering it
+  const int* ncta;            // per matrix: CTAs covering it
+  const long long* pbase;     // per matrix: offset of its partials in part
+  double* part;               // partials [pbase[s] + (c - c0[s]) 64 nt[s] + i]
+};
 
 struct FusedPcg {
   long long NG, ncol_total;
@@ -61,7 +80,13 @@ struct FusedPcg {
   double* tphase;                // 8 accumulated phase times (ns), CTA 0
   double *ucl, *wr;              // B_s u_c (c-space) and Psi_s B_s u_c (r-space, padded)
   long long rlen;                // padded r-space length
+  RangePack rs, rq;              // contiguous tile ranges per CTA of S and Q
+  int nst, maxlen;               // ring stages; longest local vector (doubles)
+  int l2pf;                      // tiles hinted into L2 beyond the ring at a phase switch
+  int psi_late;                  // Psi^T f_r after the Q tiles instead of before
 };
+
+extern __shared__ __align__(128) double dyn_smem[];  // ring stages, local vector, accumulator
 
 struct Smem {
   double csum[8][kTile];
@@ -86,7 +111,8 @@ struct PhaseClock {
   }
 };
 
-constexpr int kRing = 3;                       // tile stages per CTA
+constexpr int kUnroll = 8;  // independent loads in flight per thread in the glue loops
+constexpr int kMaxRing = 8;                    // tile stages per CTA (runtime depth A.nst)
 constexpr unsigned kTileBytes = kTile * kTile * 8;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -99,38 +125,47 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
       "W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(su32(b)), "r"(parity)
       : "memory");
 }
+// Streamed tiles are read once per phase and are far larger than L2: load
+// them evict-first so that Psi, F_cc^-1, the partials and the vectors stay
+// resident in L2 across phases.
 __device__ __forceinline__ void mb_load(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(b))
-               : "memory");
+  asm volatile(
+      "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
+      : "memory");
 }
 
-// Per-CTA ring of 32 KB tile stages filled by TMA bulk copies.  Tiles of a
-// phase are this CTA's t = blockIdx.x + k gridDim; thread 0 keeps kRing of
-// them in flight.  The matrices are constant, so the next phase's tiles may be
-// issued ahead (across grid barriers) whenever the phase is known.
+// Per-CTA ring of 32 KB tile stages filled by TMA bulk copies.  The tiles of
+// a phase are this CTA's contiguous range; thread 0 keeps nst of them in
+// flight.  The matrices are constant, so the next phase's tiles may be issued
+// ahead (across grid barriers) whenever the phase is known.
 struct Ring {
   double* stage;
   unsigned long long* full;
+  int nst;
   int consumed, issued;  // consumed: uniform; issued: thread 0
-  int pre_kind, pre_n;   // tiles of set pre_kind already issued for the next phase
+  int pre_kind;          // tile set whose first tiles are already issued for the next phase
 };
 
-__device__ __forceinline__ void ring_issue(Ring& R, const double* tiles, long long ntiles, int k) {
-  const long long t = blockIdx.x + (long long)k * gridDim.x;
-  if (t >= ntiles) return;
-  const int st = R.issued % kRing;
-  mb_load(R.stage + (size_t)st * kTile * kTile, tiles + t * (kTile * kTile), kTileBytes, &R.full[st]);
+__device__ __forceinline__ void ring_issue(Ring& R, const RangePack& P, long long k) {
+  const long long t = P.t_first[blockIdx.x] + k;
+  if (t >= P.t_first[blockIdx.x + 1]) return;
+  const int st = R.issued % R.nst;
+  mb_load(R.stage + (size_t)st * kTile * kTile, P.tiles + t * (kTile * kTile), kTileBytes, &R.full[st]);
   ++R.issued;
 }
-// issue the first tiles of set `kind` for the next tile phase (thread 0)
-__device__ __forceinline__ void ring_prefetch(Ring& R, int kind, const double* tiles, long long ntiles) {
+// issue the first tiles of set `kind` for the next tile phase (thread 0),
+// and hint the following l2pf tiles into L2 (they stream during glue phases)
+__device__ __forceinline__ void ring_prefetch(Ring& R, int kind, const RangePack& P, int l2pf) {
   if (threadIdx.x == 0) {
-    int n = 0;
-    for (; n < kRing && blockIdx.x + (long long)n * gridDim.x < ntiles; ++n) ring_issue(R, tiles, ntiles, n);
-    R.pre_n = n;
+    for (int n = 0; n < R.nst; ++n) ring_issue(R, P, n);
+    const long long t1 = P.t_first[blockIdx.x + 1];
+    for (long long t = P.t_first[blockIdx.x] + R.nst, e = t + l2pf; t < e && t < t1; ++t)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.tiles + t * (kTile * kTile)), "r"(kTileBytes)
+                   : "memory");
   }
   R.pre_kind = kind;
 }
@@ -188,23 +223,24 @@ __device__ __forceinline__ void write_local_s(const FusedPcg& A, double* li, lon
   }
 }
 
-__device__ __forceinline__ void load_tile_smem(const double* T, double2 (&v)[8]) {
+// One 64x64 lower tile T_IJ (stage, row-major, diagonal tiles full) times the
+// local vector xs: accI += T xs_J, accJ += T^T xs_I (I != J).  256 threads:
+// warp w streams rows 8w..8w+7 (128-bit shared loads, lane = 2 columns); the 8
+// row sums use a butterfly multi-row reduction, the column sums a shared
+// 8 x 64 scratch.  Every accumulator entry has one writer.
+__device__ __forceinline__ void tile_acc(const double* T, const double* xI, const double* xJ, bool diag, double* accI,
+                                         double* accJ, Smem& sm) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double2* T2 = reinterpret_cast<const double2*>(T);
+  double2 v[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = T2[(w * 8 + k) * (kTile / 2) + lane];
-}
-
-// tile math of tiles.cuh::tile_symv on preloaded rows, x from shared memory
-__device__ __forceinline__ void tile_math(const double2 (&v)[8], const Smem& sm, bool diag, double* rowpart,
-                                          double* colpart, Smem& smw) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const double2 xj = reinterpret_cast<const double2*>(sm.xJ)[lane];
+  const double2 xj = reinterpret_cast<const double2*>(xJ)[lane];
   double rs[8], c0 = 0.0, c1 = 0.0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     rs[k] = v[k].x * xj.x + v[k].y * xj.y;
-    const double xv = sm.xI[w * 8 + k];
+    const double xv = xI[w * 8 + k];
     c0 += v[k].x * xv;
     c1 += v[k].y * xv;
   }
@@ -229,61 +265,80 @@ __device__ __forceinline__ void tile_math(const double2 (&v)[8], const Smem& sm,
   rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], 1);
   if ((lane & 3) == 0) {
     const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    rowpart[w * 8 + row] = rs[0];
+    accI[w * 8 + row] += rs[0];
   }
   if (!diag) {
-    smw.csum[w][2 * lane] = c0;
-    smw.csum[w][2 * lane + 1] = c1;
+    sm.csum[w][2 * lane] = c0;
+    sm.csum[w][2 * lane + 1] = c1;
     __syncthreads();
     if (threadIdx.x < kTile) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += smw.csum[k][threadIdx.x];
-      colpart[threadIdx.x] = s;
+      for (int k = 0; k < 8; ++k) s += sm.csum[k][threadIdx.x];
+      accJ[threadIdx.x] += s;
     }
   }
 }
 
-// One tile phase over this CTA's tiles of a packed set, x segments gathered
-// by `xval(segment, i)` (global loads issued before the stage wait).
+// write the accumulator as this CTA's partial of matrix s
+__device__ __forceinline__ void range_flush(const RangePack& P, int s, int len, const double* acc) {
+  double* dst = P.part + P.pbase[s] + (long long)(blockIdx.x - P.c0[s]) * len;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) dst[i] = acc[i];
+}
+
+// One tile phase over this CTA's contiguous tile range of a pack; the local
+// input vector of each matrix is gathered by xval(local offset) into xs.
 template <typename XF>
-__device__ void tile_phase(Ring& R, int kind, const int2* __restrict__ tx, const double* __restrict__ tiles,
-                           long long ntiles, double* rowp, double* colp, Smem& sm, XF xval) {
-  if (R.pre_kind != kind) ring_prefetch(R, kind, tiles, ntiles);
-  int k = 0;
-  const bool gthr = threadIdx.x < 2 * kTile;
-  const int gi = threadIdx.x & (kTile - 1);
-  const long long G = gridDim.x, t0 = blockIdx.x;
-  // software pipeline: descriptors two tiles ahead, x values one tile ahead,
-  // so no load sits on the critical path of the tile being computed
-  int2 dc = t0 < ntiles ? tx[t0] : make_int2(0, 0);
-  int2 dn = t0 + G < ntiles ? tx[t0 + G] : make_int2(0, 0);
-  double xc = (t0 < ntiles && gthr) ? xval((threadIdx.x < kTile ? dc.x : dc.y) + gi) : 0.0;
-  for (long long t = t0; t < ntiles; t += G, ++k) {
-    double xn = 0.0;
-    if (t + G < ntiles && gthr) xn = xval((threadIdx.x < kTile ? dn.x : dn.y) + gi);
-    const int2 dnn = t + 2 * G < ntiles ? tx[t + 2 * G] : make_int2(0, 0);
-    const int st = R.consumed % kRing;
-    mb_wait(&R.full[st], (R.consumed / kRing) & 1);
-    if (gthr) (threadIdx.x < kTile ? sm.xI : sm.xJ)[gi] = xc;
-    __syncthreads();
-    double2 v[8];
-    load_tile_smem(R.stage + (size_t)st * kTile * kTile, v);
-    tile_math(v, sm, dc.x == dc.y, rowp + t * kTile, colp + t * kTile, sm);
-    __syncthreads();  // stage and x segments consumed
-    if (threadIdx.x == 0) ring_issue(R, tiles, ntiles, k + kRing);
-    ++R.consumed;
-    dc = dn;
-    dn = dnn;
-    xc = xn;
-  }
+__device__ void range_phase(Ring& R, int kind, const RangePack& P, double* xs, double* acc, Smem& sm, XF xval) {
+  if (R.pre_kind != kind) ring_prefetch(R, kind, P, 0);
   R.pre_kind = 0;
+  const long long t0 = P.t_first[blockIdx.x], t1 = P.t_first[blockIdx.x + 1];
+  if (t0 >= t1) return;
+  const int4 st0 = P.start[blockIdx.x];
+  int s = st0.x, I = st0.y, J = st0.z, cur = -1, len = 0, nt = 0;
+  for (long long t = t0, k = 0; t < t1; ++t, ++k) {
+    if (s != cur) {
+      if (cur >= 0) range_flush(P, cur, len, acc);  // same thread owns index i in both loops
+      cur = s, nt = P.nt[s], len = kTile * nt;
+      const long long xo = P.xoff[s];
+      for (int i = threadIdx.x; i < len; i += blockDim.x) xs[i] = xval(xo + i), acc[i] = 0.0;
+      __syncthreads();
+    }
+    const int stg = R.consumed % R.nst;
+    mb_wait(&R.full[stg], (R.consumed / R.nst) & 1);
+    tile_acc(R.stage + (size_t)stg * kTile * kTile, xs + I * kTile, xs + J * kTile, I == J, acc + I * kTile,
+             acc + J * kTile, sm);
+    __syncthreads();  // stage consumed, accumulator updated
+    if (threadIdx.x == 0) ring_issue(R, P, k + R.nst);
+    ++R.consumed;
+    if (++J > I) {
+      J = 0;
+      if (++I == nt) I = 0, ++s;
+    }
+  }
+  range_flush(P, cur, len, acc);
+}
+
+// y_s[i] from the partials of the CTAs covering matrix s (CTA order)
+__device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i) {
+  const int len = kTile * P.nt[s], n = P.ncta[s];
+  const double* p = P.part + P.pbase[s] + i;
+  double y = 0.0;
+  int k = 0;
+  for (; k + 4 <= n; k += 4) {
+    const double a = __ldcg(p + (long long)k * len), b = __ldcg(p + (long long)(k + 1) * len),
+                 c = __ldcg(p + (long long)(k + 2) * len), d = __ldcg(p + (long long)(k + 3) * len);
+    y += a, y += b, y += c, y += d;
+  }
+  for (; k < n; ++k) y += __ldcg(p + (long long)k * len);
+  return y;
 }
 
 // mode 0: x vector = first ? z : z + beta p (lazy p update); mode 1: x
-__device__ void s_tiles_phase(const FusedPcg& A, Ring& R, Smem& sm, int mode, bool first, double beta) {
-  tile_phase(R, 1, A.s_tx, A.s_tiles, A.s_ntiles, A.s_row, A.s_col, sm, [&](long long o) {
-    return mode ? A.li_x[o] : (first ? A.li_z[o] : A.li_z[o] + beta * A.li_p[o]);
+__device__ void s_tiles_phase(const FusedPcg& A, Ring& R, Smem& sm, double* xs, double* acc, int mode, bool first,
+                              double beta) {
+  range_phase(R, 1, A.rs, xs, acc, sm, [&](long long o) {
+    return mode ? __ldcg(A.li_x + o) : (first ? __ldcg(A.li_z + o) : __ldcg(A.li_z + o) + beta * __ldcg(A.li_p + o));
   });
 }
 
@@ -292,20 +347,21 @@ __device__ __forceinline__ double s_reduce(const FusedPcg& A, long long q) {
   double y = 0.0;
   for (int e = 0; e < A.inv_cnt[gq]; ++e) {
     const int s = A.inv_s[4 * gq + e], pp = A.inv_p[4 * gq + e];
-    y += tile_reduce(A.s_row, A.s_col, A.s_base[s], A.s_nt[s], j * A.ng[s] + pp);
+    y += range_reduce(A.rs, s, j * A.ng[s] + pp);
   }
   return y;
 }
+
 
 // z = NN2(r) from the local inputs fr/fc; returns r.z
 __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_group& g, PhaseClock& pc) {
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   const long long gwarp = gtid >> 5, nwarps = gstride >> 5;
-  // 4. Q tiles + Psi^T f_r
-  tile_phase(R, 2, A.q_tx, A.q_tiles, A.q_ntiles, A.q_row, A.q_col, sm, [&](long long o) { return A.fr[o]; });
-  ring_prefetch(R, 1, A.s_tiles, A.s_ntiles);  // next iteration's S tiles stream in during 5-7
-  if (A.NC > 0) {
+  // 4. Psi^T f_r (the first Q tiles stream in meanwhile), Q tiles
+  double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;
+  ring_prefetch(R, 2, A.rq, A.l2pf);
+  auto psi_t = [&]() {
     for (long long wv = gwarp; wv < A.ncol_total; wv += nwarps) {
       int lo = 0, hi = A.NS;  // subdomain s with coff[s] <= wv < coff[s+1]
       while (hi - lo > 1) {
@@ -317,11 +373,16 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
       const double* col = A.Psi + A.psioff[s] + (long long)c * rs;
       const double* f = A.fr + A.roff[s];
       double acc = 0.0;
+#pragma unroll kUnroll
       for (int a = lane; a < rs; a += 32) acc += col[a] * f[a];
       acc = warp_sum(acc);
       if (lane == 0) A.dsub[wv] = A.fc[wv] - acc;
     }
-  }
+  };
+  if (A.NC > 0 && !A.psi_late) psi_t();
+  range_phase(R, 2, A.rq, xs, xs + A.maxlen, sm, [&](long long o) { return __ldcg(A.fr + o); });
+  ring_prefetch(R, 1, A.rs, A.l2pf);  // next iteration's S tiles stream in during 5-7
+  if (A.NC > 0 && A.psi_late) psi_t();
   g.sync();
   pc.tick(3);
   if (A.NC > 0) {
@@ -342,6 +403,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
     for (long long row = gwarp; row < A.NC; row += nwarps) {
       const double* col = A.Finv + row * A.NC;
       double acc = 0.0;
+#pragma unroll kUnroll
       for (int c = lane; c < A.NC; c += 32) acc += col[c] * __ldcg(A.dco + c);
       acc = warp_sum(acc);
       if (lane == 0) {
@@ -368,7 +430,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
       const double* u = A.ucl + A.coff[s];
       const int cs = A.NT * A.nc[s];
       double acc = 0.0;
-#pragma unroll 4
+#pragma unroll kUnroll
       for (int c = 0; c < cs; ++c) acc += P[(long long)c * rs] * __ldcg(u + c);
       A.wr[i] = acc;
     }
@@ -387,7 +449,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
       double v;
       if (kind >= 0) {
         const int ar = j * A.nr[s] + kind;
-        v = tile_reduce(A.q_row, A.q_col, A.q_base[s], A.q_nt[s], ar);
+        v = range_reduce(A.rq, s, ar);
         if (A.NC > 0) v -= __ldcg(A.wr + A.roff[s] + ar);  // u_r = Q f_r - Psi u_c
       } else {
         v = A.NC > 0 ? __ldcg(A.ucl + A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)) : 0.0;
@@ -406,15 +468,16 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
 __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   cg::grid_group g = cg::this_grid();
   __shared__ Smem sm;
-  __shared__ unsigned long long ring_bar[kRing];
-  extern __shared__ __align__(128) double ring_stage[];
+  __shared__ unsigned long long ring_bar[kMaxRing];
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
   const bool leader = gtid == 0;
-  Ring R{ring_stage, ring_bar, 0, 0, 0, 0};
+  Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0};
+  double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;  // local input vector, then the accumulator
+  double* xacc = xs + A.maxlen;
   PhaseClock pc{leader && A.tphase != nullptr, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pc.last));
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kRing; ++i) mb_init(&ring_bar[i], 1);
+    for (int i = 0; i < A.nst; ++i) mb_init(&ring_bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -442,7 +505,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   int it = 0;
   while (it < A.max_iter) {
     // 1-2: q = S p_new, p.q
-    s_tiles_phase(A, R, sm, 0, first, beta);
+    s_tiles_phase(A, R, sm, xs, xacc, 0, first, beta);
     g.sync();
     pc.tick(0);
     acc = 0.0;
@@ -474,7 +537,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
       // recurrence hit the target; confirm with the true residual b - S x
       for (long long q = gtid; q < A.NG; q += gstride) write_local_s(A, A.li_x, q, A.x[q]);
       g.sync();
-      s_tiles_phase(A, R, sm, 1, false, 0.0);
+      s_tiles_phase(A, R, sm, xs, xacc, 1, false, 0.0);
       g.sync();
       acc = 0.0;
       for (long long q = gtid; q < A.NG; q += gstride) {
@@ -514,11 +577,40 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   }
   // drain tile copies still in flight before the CTA's shared memory goes away
   if (threadIdx.x == 0)
-    for (int c = R.consumed; c < R.issued; ++c) mb_wait(&R.full[c % kRing], (c / kRing) & 1);
+    for (int c = R.consumed; c < R.issued; ++c) mb_wait(&R.full[c % R.nst], (c / R.nst) & 1);
   __syncthreads();
 }
 
 // --------------------------------------------------------------- host ----
+void RangeBufs::plan(const TilePack& tp, int grid) {
+  std::vector<long long> tf(grid + 1), pb(tp.nmat + 1, 0);
+  std::vector<int4> st(grid, make_int4(0, 0, 0, 0));
+  std::vector<int> c0(tp.nmat, 0), nc(tp.nmat, 0);
+  for (int c = 0; c <= grid; ++c) tf[c] = tp.n_tiles * c / grid;
+  // matrix, I, J of every CTA's first tile; CTAs covering each matrix
+  auto cta_of = [&](long long t) {  // CTA whose range holds tile t
+    return int(std::upper_bound(tf.begin(), tf.end(), t) - tf.begin()) - 1;
+  };
+  for (int c = 0; c < grid; ++c) {
+    if (tf[c] >= tf[c + 1]) continue;
+    const int s = int(std::upper_bound(tp.tile_base.begin(), tp.tile_base.end(), tf[c]) - tp.tile_base.begin()) - 1;
+    long long r = tf[c] - tp.tile_base[s];
+    int I = 0;
+    while (r > I) r -= ++I;  // row-major lower order: row I holds I + 1 tiles
+    st[c] = make_int4(s, I, int(r), 0);
+  }
+  for (int s = 0; s < tp.nmat; ++s) {
+    const int a = cta_of(tp.tile_base[s]), b = cta_of(tp.tile_base[s + 1] - 1);
+    c0[s] = a, nc[s] = b - a + 1;
+    pb[s + 1] = pb[s] + (long long)nc[s] * kTile * tp.ntile[s];
+  }
+  t_first.upload(tf), start.upload(st);
+  this->c0.upload(c0), ncta.upload(nc), pbase.upload(pb);
+  part.alloc(std::max<long long>(1, pb[tp.nmat]));
+  SGW_CUDA(cudaMemset(part.p, 0, part.n * sizeof(double)));  // slots of CTAs with empty ranges stay 0
+}
+
+
 void GpuSolver::setup_fused_pcg() {
   tphase_.alloc(8), tphase_.zero(st_);
   if (comm_) {  // sharded: the host-driven loop with a sum over ranks after each scatter
@@ -533,13 +625,37 @@ void GpuSolver::setup_fused_pcg() {
       for (int p = 0; p < ng_[s]; ++p) smap[Sp.xoff[s] + (long long)j * ng_[s] + p] = j * G.n_iface + sd.iface_pos[p];
   }
   smap_.upload(smap);
-  int dev = 0, sms = 0, nb = 0;
+  int dev = 0, sms = 0, nb = 0, smem_sm = 0, smem_blk = 0;
   SGW_CUDA(cudaGetDevice(&dev));
   SGW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const size_t dsm = (size_t)kRing * kTileBytes;
-  SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pcg_fused_kernel, 256, dsm));
-  fused_grid_ = std::max(1, nb) * sms;
+  SGW_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  SGW_CUDA(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // shared memory per CTA: the tile ring, the local input vector and the
+  // accumulator of the longest local vector.  Default two CTAs per SM (more
+  // warps for the scatter phases; measured 0.56 vs 0.64 ms per C2 iteration
+  // with one CTA and a deeper ring) if each gets >= 2 stages, else one with the
+  // deepest ring that fits.  SGW_PCG_BPS / SGW_PCG_RING tune.
+  fused_maxlen_ = 0;
+  for (int s = 0; s < NS; ++s) fused_maxlen_ = std::max({fused_maxlen_, kTile * Sp.ntile[s], kTile * Qp.ntile[s]});
+  cudaFuncAttributes fa{};
+  SGW_CUDA(cudaFuncGetAttributes(&fa, (const void*)pcg_fused_kernel));
+  int bps = 2;
+  if (const char* e = std::getenv("SGW_PCG_BPS")) bps = std::max(1, std::atoi(e));
+  const long long vec = 2LL * fused_maxlen_ * 8;
+  for (;; --bps) {
+    const long long avail = std::min<long long>(smem_blk, smem_sm / bps - 1024) - (long long)fa.sharedSizeBytes - vec;
+    fused_nst_ = (int)std::min<long long>(kMaxRing, avail / kTileBytes);
+    if (fused_nst_ >= 2 || bps == 1) break;
+  }
+  if (const char* e = std::getenv("SGW_PCG_RING")) fused_nst_ = std::min(kMaxRing, std::atoi(e));
+  if (fused_nst_ < 1) throw Error(4, "persistent PCG: local vectors exceed shared memory");
+  fused_smem_ = (size_t)fused_nst_ * kTileBytes + (size_t)vec;
+  SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused_smem_));
+  SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pcg_fused_kernel, 256, fused_smem_));
+  fused_grid_ = std::max(1, std::min(nb, bps)) * sms;
+  rs_.plan(Sp, fused_grid_);
+  rq_.plan(Qp, fused_grid_);
   fused_part_.alloc(size_t(8) * fused_grid_);
   fused_out_.alloc(4);
   fused_hist_.alloc(P.max_iter + 8);
@@ -574,9 +690,15 @@ int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vecto
   A.li_z = li_z_.p, A.li_p = li_p_.p, A.li_x = li_xx_.p;
   A.tphase = KP.on ? tphase_.p : nullptr;
   A.ucl = ucl_.p, A.wr = wr_.p, A.rlen = Qp.xlen;
+  A.rs = RangePack{Sp.tiles.p, Sp.d_ntile.p, Sp.d_xoff.p, rs_.t_first.p, rs_.start.p, rs_.c0.p, rs_.ncta.p, rs_.pbase.p, rs_.part.p};
+  A.rq = RangePack{Qp.tiles.p, Qp.d_ntile.p, Qp.d_xoff.p, rq_.t_first.p, rq_.start.p, rq_.c0.p, rq_.ncta.p, rq_.pbase.p, rq_.part.p};
+  A.nst = fused_nst_, A.maxlen = fused_maxlen_;
+  A.l2pf = 0, A.psi_late = 1;
+  if (const char* e = std::getenv("SGW_PCG_PSI_LATE")) A.psi_late = std::atoi(e);  // tuning hook
+  if (const char* e = std::getenv("SGW_PCG_L2PF")) A.l2pf = std::max(0, std::atoi(e));  // tuning hook
   void* args[] = {&A};
   SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_fused_kernel, dim3(fused_grid_), dim3(256), args,
-                                       (size_t)kRing * kTileBytes, st_));
+                                       fused_smem_, st_));
   SGW_LAUNCHED();
   int out[3] = {0, 0, 0};
   SGW_CUDA(cudaMemcpyAsync(out, fused_out_.p, sizeof(out), cudaMemcpyDeviceToHost, st_));

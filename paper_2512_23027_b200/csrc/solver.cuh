@@ -107,6 +107,16 @@ struct TilePack {
   long long bytes() const { return n_tiles * kTile * kTile * 8; }
 };
 
+// Contiguous per-CTA tile ranges of a TilePack for the persistent PCG kernel
+// (pcg_fused.cu RangePack): CTA c walks tiles [t_first[c], t_first[c + 1]).
+struct RangeBufs {
+  DBuf<long long> t_first, pbase;
+  DBuf<int4> start;
+  DBuf<int> c0, ncta;
+  DBuf<double> part;
+  void plan(const TilePack& tp, int grid);
+};
+
 // G tensor lists by output term k: entries (i, j, g) in for_each order.
 struct GList {
   const int *ptr, *i, *j;
@@ -302,6 +312,9 @@ class GpuSolver {
   void setup_fused_pcg();
   int pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist);
   DBuf<int> smap_, fused_out_;
+  RangeBufs rs_, rq_;
+  int fused_nst_ = 3, fused_maxlen_ = 0;
+  size_t fused_smem_ = 0;
   DBuf<double> fused_part_, fused_hist_, li_z_, li_p_, li_xx_, ucl_, wr_;
  public:
   DBuf<double> tphase_;  // per-phase ns of the persistent PCG kernel (profiling)

@@ -71,10 +71,30 @@ __device__ __forceinline__ void tile_symv(const double* __restrict__ T, const do
 __device__ __forceinline__ double tile_reduce(const double* __restrict__ rowpart, const double* __restrict__ colpart,
                                               long long base, int nt, int i) {
   const int I = i / kTile, r = i % kTile;
-  const long long rowb = base + (long long)I * (I + 1) / 2;
+  const double* rp = rowpart + (base + (long long)I * (I + 1) / 2) * kTile + r;
+  // the partials were written by other CTAs before a grid barrier: L2 loads,
+  // issued 8 at a time (the sum order stays J ascending, then K ascending)
+  constexpr int U = 8;
   double s = 0.0;
-  for (int J = 0; J <= I; ++J) s += rowpart[(rowb + J) * kTile + r];
-  for (int K = I + 1; K < nt; ++K) s += colpart[(base + (long long)K * (K + 1) / 2 + I) * kTile + r];
+  int J = 0;
+  for (; J + U <= I + 1; J += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcg(rp + (long long)(J + u) * kTile);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += v[u];
+  }
+  for (; J <= I; ++J) s += __ldcg(rp + (long long)J * kTile);
+  const double* cp = colpart + (base + I) * kTile + r;  // tile (K, I) at base + K(K+1)/2 + I
+  int K = I + 1;
+  for (; K + U <= nt; K += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcg(cp + (long long)(K + u) * (K + u + 1) / 2 * kTile);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += v[u];
+  }
+  for (; K < nt; ++K) s += __ldcg(cp + (long long)K * (K + 1) / 2 * kTile);
   return s;
 }
 
