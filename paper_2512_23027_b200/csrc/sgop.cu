@@ -83,8 +83,15 @@ __device__ __forceinline__ void cp8(double* s, const double* g, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(su(s)), "l"(g), "r"(ok ? 8 : 0) : "memory");
 }
 __device__ __forceinline__ void bulk(double* s, const double* g, unsigned bytes, unsigned long long* bar) {
+#if EF
+  /* stencils stream once per apply: evict-first keeps x and M resident in L2 */
+  asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+               " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
+               :: "r"(su(s)), "l"(g), "r"(bytes), "r"(su(bar)) : "memory");
+#else
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(su(s)), "l"(g), "r"(bytes), "r"(su(bar)) : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned n) {
   asm volatile("mbarrier.init.shared.b64 [%0], %1;" :: "r"(su(bar)), "r"(n) : "memory");
@@ -584,7 +591,9 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
     dispatch.replace(dispatch.find("switch (gq)"), 11, "switch (0)");
   int pf = 0;  // measured: L2 prefetch beyond the ring does not help here
   if (const char* e = std::getenv("SGW_SGOP_PF")) pf = std::max(0, std::atoi(e));  // tuning hook
-  std::string src = "#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
+  int ef = 1;
+  if (const char* e = std::getenv("SGW_SGOP_EF")) ef = std::atoi(e);  // tuning hook
+  std::string src = "#define EF " + std::to_string(ef) + "\n#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
                     "\n#define NT " + std::to_string(NT) + "\n#define NIN " + std::to_string(NIN) +
                     "\n#define R " + std::to_string(R) + "\n#define G " + std::to_string(G) + "\n#define IC " +
                     std::to_string(IC) + "\n#define S " + std::to_string(J->S) + "\n#define NCHUNK " +
