@@ -18,6 +18,7 @@
  *   sgw_apply_block     SgSolver::apply_block_{mass,stiffness,transient}  sg.hpp:58-60, src/sg.cpp:425-447
  *   sgw_schur_matvec    SchurSystem::matvec           include/sgwave/dd.hpp:85, src/dd.cpp:142-157
  *   sgw_apply_nn2       SchurSystem::apply_nn2        include/sgwave/dd.hpp:88, src/dd.cpp:199-253
+ *   sgw_apply_precond   make_preconditioner / apply_{lumped,nn1,nn2}  dd.hpp:86-88,102, src/dd.cpp:159-253
  *   sgw_pcg             pcg(matvec, apply_nn2, ...)   include/sgwave/pcg.hpp:20-21, src/pcg.cpp:7-50
  *   sgw_coarse_operator SchurSystem::coarse_operator  include/sgwave/dd.hpp:90
  *   sgw_lognormal_coeff lognormal_pce(kle_exponential(...))  src/lognormal.cpp:8-40, src/kle.cpp:80-133
@@ -79,6 +80,11 @@ typedef struct sgw_problem {
    * world_size 1 runs the sharded code path on a 1-rank communicator.      */
   int rank, world_size;
   const void* nccl_id;
+  /* PrecondKind (dd.hpp:98) of the PCG: 0 nn2 (the SG path, sg.cpp:330),
+   * 1 nn1 (dd.cpp:178-195), 2 lumped (dd.cpp:159-176, gg_action = the
+   * flattened A_GG block as DetSolver's K~_GG, det_loop.cpp:165-167).
+   * DetSolver::set_preconditioner / SolveOptions::precond (det_loop.hpp:14). */
+  int precond;
 } sgw_problem;
 
 /* ForceFn (det_loop.hpp:32): kind 0 none; 1 Ricker wavelet
@@ -121,6 +127,9 @@ int sgw_set_stream(sgw_solver* s, void* cuda_stream);
 int sgw_apply_block(sgw_solver* s, int op, const double* x, double* y);
 int sgw_schur_matvec(sgw_solver* s, const double* x, double* y);
 int sgw_apply_nn2(sgw_solver* s, const double* r, double* z);
+/* make_preconditioner(schur, kind)(r) (dd.cpp): kind 0 nn2, 1 nn1, 2 lumped;
+ * nn1 / lumped need problem->precond == kind (SGW_EINVAL otherwise).       */
+int sgw_apply_precond(sgw_solver* s, int kind, const double* r, double* z);
 /* PCG on S u = rhs with NN2 (src/pcg.cpp:7-50).  history: >= max_iter + 2. */
 int sgw_pcg(sgw_solver* s, const double* rhs, double* x, int* iterations, int* converged,
             double* residual_history, int history_cap);

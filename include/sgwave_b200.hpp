@@ -35,7 +35,17 @@ struct NewmarkParams {  // newmark.hpp:11-19
   double dt = 0.0;
 };
 
-struct SgOptions {  // sg.hpp:13-19 (threads: accepted, unused on the GPU)
+enum class PrecondKind { lumped, nn1, nn2 };  // dd.hpp:98
+inline int precond_code(PrecondKind k) { return k == PrecondKind::nn2 ? 0 : k == PrecondKind::nn1 ? 1 : 2; }
+inline PrecondKind precond_from_string(const std::string& name) {  // dd.hpp:100
+  if (name == "lumped") return PrecondKind::lumped;
+  if (name == "nn1") return PrecondKind::nn1;
+  if (name == "nn2") return PrecondKind::nn2;
+  throw std::invalid_argument("unknown preconditioner: " + name);
+}
+
+struct SgOptions {  // sg.hpp:13-19 (threads: accepted, unused on the GPU) + SolveOptions::precond
+  PrecondKind precond = PrecondKind::nn2;
   double tol = 1e-8;
   int max_iter = 500;
   int threads = 1;
@@ -134,6 +144,15 @@ class SchurSystem {  // dd.hpp:71-96 (view on the solver's interface system)
     detail::check(sgw_apply_nn2(h_, r.data(), z.data()));
     return z;
   }
+  // make_preconditioner(system, kind)(r) (dd.cpp:159-253); nn1 / lumped need
+  // the solver to be built with that preconditioner
+  Vec apply_precond(PrecondKind kind, const Vec& r) const {
+    Vec z(n_);
+    detail::check(sgw_apply_precond(h_, precond_code(kind), r.data(), z.data()));
+    return z;
+  }
+  Vec apply_nn1(const Vec& r) const { return apply_precond(PrecondKind::nn1, r); }
+  Vec apply_lumped(const Vec& r) const { return apply_precond(PrecondKind::lumped, r); }
   Vec coarse_operator() const {  // column-major n_coarse x n_coarse
     Vec f(size_t(nc_) * nc_);
     detail::check(sgw_coarse_operator(h_, f.data()));
@@ -180,7 +199,7 @@ class SgSolver {  // sg.hpp:43-98
     pr.density = density, pr.alpha0 = alpha0, pr.alpha1 = alpha1;
     pr.gamma = params.gamma, pr.zeta = params.zeta, pr.dt = params.dt;
     pr.tol = opt_.tol, pr.max_iter = opt_.max_iter, pr.device = opt_.device;
-    pr.rank = 0, pr.world_size = 1, pr.nccl_id = nullptr;
+    pr.rank = 0, pr.world_size = 1, pr.nccl_id = nullptr, pr.precond = precond_code(opt_.precond);
     if (pr.n_input != tensor.n_input)
       throw std::invalid_argument("SgSolver: coefficient terms do not match tensor input size");
     detail::check(sgw_create(&pr, &h_));

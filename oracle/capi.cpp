@@ -97,7 +97,7 @@ int orc_nearest_node(int nx, int ny, double x, double y) {
 int orc_solver_create(int nx, int ny, int px, int py, int n_in, const double* coeff, int n_out,
                       int n_ent, const int* ei, const int* ej, const int* ek, const double* ev,
                       double density, double alpha0, double alpha1, double gamma, double zeta,
-                      double dt, double tol, int max_iter, int threads, void** out) {
+                      double dt, double tol, int max_iter, int threads, int precond, void** out) {
   try {
     auto h = std::make_unique<Handle>();
     h->mesh = build_unit_square_mesh(nx, ny);
@@ -121,6 +121,8 @@ int orc_solver_create(int nx, int ny, int px, int py, int n_in, const double* co
     o.tol = tol;
     o.max_iter = max_iter;
     o.threads = threads;
+    if (precond < 0 || precond > 2) throw std::invalid_argument("unknown preconditioner");
+    o.precond = precond;
     h->solver = std::make_unique<SgSolver>(h->mesh, h->part, f, t, density, alpha0, alpha1, p, o);
     *out = h.release();
     return 0;
@@ -157,12 +159,16 @@ int orc_apply_block(void* hp, int op, const double* x, double* y) {
   }
 }
 
-// which: 0 matvec (src/dd.cpp:142-157), 1 apply_nn2 (src/dd.cpp:199-253)
+// which: 0 matvec (src/dd.cpp:142-157), 1 apply_nn2 (src/dd.cpp:199-253),
+//        2 apply_nn1 (:178-195), 3 apply_lumped (:159-176)
 int orc_schur_apply(void* hp, int which, const double* x, double* y) {
   try {
     const SgSolver& s = *static_cast<Handle*>(hp)->solver;
     const Vec xv(x, x + s.schur().n_global);
-    const Vec out = which == 0 ? s.schur().matvec(xv) : s.schur().apply_nn2(xv);
+    const Vec out = which == 0   ? s.schur().matvec(xv)
+                    : which == 1 ? s.schur().apply_nn2(xv)
+                    : which == 2 ? s.schur().apply_nn1(xv)
+                                 : s.schur().apply_lumped(xv);
     std::memcpy(y, out.data(), sizeof(double) * out.size());
     return 0;
   } catch (const std::exception& e) {
@@ -256,7 +262,7 @@ int orc_single_block_nn2(int n, const double* a, const double* r, double* z, dou
     sys.n_global = n;
     sys.n_corner = 0;
     sys.locals.push_back(std::move(ls));
-    sys.finalize();
+    sys.finalize(false);
     const Vec rv(r, r + n);
     const Vec zv = sys.apply_nn2(rv);
     std::memcpy(z, zv.data(), sizeof(double) * n);

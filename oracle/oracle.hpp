@@ -177,6 +177,8 @@ InterfaceLayout build_interface_layout(const Partition& part, const DirichletRed
 
 struct LocalSchur {
   Dense S;
+  Dense Kgg;  // flattened interface block A_GG (lumped preconditioner's gg_action, det_loop.cpp:165-167)
+  Llt S_llt;  // llt_regularized(S) (NN1, dd.cpp:115)
   std::vector<Index> gmap, r_idx, c_idx, corner_gmap;
   Vec weights;
   Dense S_rc;
@@ -190,9 +192,12 @@ class SchurSystem {  // include/sgwave/dd.hpp:71-96
   Index n_global = 0, n_corner = 0;
   int n_threads = 1;
   std::vector<LocalSchur> locals;
-  void finalize();                     // src/dd.cpp:98-140 (build_nn1 = false)
+  void finalize(bool build_nn1);       // src/dd.cpp:98-140
   Vec matvec(const Vec& x) const;      // src/dd.cpp:142-157
+  Vec apply_lumped(const Vec& r) const;  // src/dd.cpp:159-176 (gg_action = Kgg)
+  Vec apply_nn1(const Vec& r) const;   // src/dd.cpp:178-195
   Vec apply_nn2(const Vec& r) const;   // src/dd.cpp:199-253
+  Vec apply(int kind, const Vec& r) const;  // make_preconditioner: 0 nn2, 1 nn1, 2 lumped
   const Dense& coarse_operator() const { return fcc_; }
 
  private:
@@ -218,7 +223,8 @@ struct NewmarkParams {  // include/sgwave/newmark.hpp:11-19
   double mass_factor() const { return 1.0 / (zeta * dt * dt); }
   double damping_factor() const { return gamma / (zeta * dt); }
 };
-struct SgOptions {  // include/sgwave/sg.hpp:15-21
+struct SgOptions {  // include/sgwave/sg.hpp:15-21 (+ SolveOptions::precond, det_loop.hpp:14)
+  int precond = 0;  // 0 nn2 (the SG path, sg.cpp:330), 1 nn1, 2 lumped
   double tol = 1e-8;
   int max_iter = 500;
   int threads = 1;

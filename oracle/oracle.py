@@ -42,7 +42,7 @@ def lib():
         L.orc_triple_products.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int)] * 3 + [C.c_void_p] * 4
         L.orc_nearest_node.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double]
         L.orc_solver_create.argtypes = ([C.c_int] * 5 + [_dp, C.c_int, C.c_int, _ip, _ip, _ip, _dp]
-                                        + [C.c_double] * 7 + [C.c_int, C.c_int, C.POINTER(C.c_void_p)])
+                                        + [C.c_double] * 7 + [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)])
         L.orc_solver_destroy.argtypes = [C.c_void_p]
         L.orc_solver_sizes.argtypes = [C.c_void_p, np.ctypeslib.ndpointer(dtype=np.int64)]
         L.orc_apply_block.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
@@ -137,19 +137,24 @@ def cfl_dt(nx, c0_max, sigma, cfl=0.65):
 
 
 # ----------------------------------------------------------------- solver --
+# PrecondKind (include/sgwave/dd.hpp:98): the SG path always uses nn2 (src/sg.cpp:330);
+# the deterministic DetSolver (det_loop.hpp:14) selects any of the three.
+PRECONDS = {"nn2": 0, "nn1": 1, "lumped": 2}
+
+
 class SgSolver:
     """Oracle SgSolver (src/sg.cpp).  Same constructor arguments as the
     reference, with the mesh/partition given by their structured sizes."""
 
     def __init__(self, nx, ny, px, py, coeff, tensor: Tensor, density=1.0, alpha0=0.5445, alpha1=0.0174,
-                 dt=1e-3, gamma=0.5, zeta=0.25, tol=1e-8, max_iter=500, threads=None):
+                 dt=1e-3, gamma=0.5, zeta=0.25, tol=1e-8, max_iter=500, threads=None, precond="nn2"):
         self.nx, self.ny = nx, ny
         coeff = np.ascontiguousarray(coeff, np.float64)
         threads = threads or os.cpu_count() or 1
         h = C.c_void_p()
         _check(lib().orc_solver_create(nx, ny, px, py, coeff.shape[0], coeff, tensor.n_output, len(tensor.v),
                                        tensor.i, tensor.j, tensor.k, tensor.v, density, alpha0, alpha1, gamma,
-                                       zeta, dt, tol, max_iter, threads, C.byref(h)))
+                                       zeta, dt, tol, max_iter, threads, PRECONDS[precond], C.byref(h)))
         self._h = h
         s = np.zeros(6, np.int64)
         lib().orc_solver_sizes(self._h, s)
@@ -177,6 +182,24 @@ class SgSolver:
         r = np.ascontiguousarray(r, np.float64)
         z = np.zeros(self.n_global)
         _check(lib().orc_schur_apply(self._h, 1, r, z))
+        return z
+
+    def apply_nn1(self, r):
+        """SchurSystem::apply_nn1 (src/dd.cpp:178-195); needs precond="nn1"."""
+        return self._schur_apply(2, r)
+
+    def apply_lumped(self, r):
+        """SchurSystem::apply_lumped (src/dd.cpp:159-176); needs precond="lumped"."""
+        return self._schur_apply(3, r)
+
+    def apply_precond(self, kind, r):
+        """make_preconditioner(system, kind) (src/dd.cpp) applied to r."""
+        return self._schur_apply({"nn2": 1, "nn1": 2, "lumped": 3}[kind], r)
+
+    def _schur_apply(self, which, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.zeros(self.n_global)
+        _check(lib().orc_schur_apply(self._h, which, r, z))
         return z
 
     def coarse_operator(self):

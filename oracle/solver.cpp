@@ -104,8 +104,8 @@ LocalSchur make_flat_maps(const SubdomainDofs& sd, int n_blocks, Index n_iface, 
   return ls;
 }
 
-// src/dd.cpp:98-140 (build_nn1 = false)
-void SchurSystem::finalize() {
+// src/dd.cpp:98-140
+void SchurSystem::finalize(bool build_nn1) {
   const int ns = int(locals.size());
   std::vector<Dense> coarse(ns);
   parallel_for(ns, n_threads, [&](int s) {
@@ -120,6 +120,7 @@ void SchurSystem::finalize() {
     for (Index b = 0; b < nc; ++b)
       for (Index a = 0; a < nc; ++a) scc(a, b) = ls.S(ls.c_idx[a], ls.c_idx[b]);
     ls.Srr_llt = llt_regularized(srr);
+    if (build_nn1) ls.S_llt = llt_regularized(ls.S);
     if (nc > 0) {
       coarse[s] = scc;
       if (nr > 0) {
@@ -161,6 +162,48 @@ Vec SchurSystem::matvec(const Vec& x) const {
   for (int s = 0; s < ns; ++s)
     for (Index k = 0; k < locals[s].n_flat(); ++k) y[locals[s].gmap[k]] += contrib[s][k];
   return y;
+}
+
+// src/dd.cpp:159-176 and :178-195: z = sum_s R_s^T D_s A_s D_s R_s r with
+// A_s = K~_GG,s (lumped, the solver's gg_action) or S_s^-1 (NN1)
+template <typename F>
+static Vec one_level(const SchurSystem& sys, const Vec& r, F&& local) {
+  const int ns = int(sys.locals.size());
+  std::vector<Vec> contrib(ns);
+  parallel_for(ns, sys.n_threads, [&](int s) {
+    const LocalSchur& ls = sys.locals[s];
+    Vec rl(ls.n_flat());
+    for (Index k = 0; k < ls.n_flat(); ++k) rl[k] = r[ls.gmap[k]] * ls.weights[k];
+    Vec zl = local(ls, rl);
+    for (Index k = 0; k < ls.n_flat(); ++k) zl[k] *= ls.weights[k];
+    contrib[s] = std::move(zl);
+  });
+  Vec z(sys.n_global, 0.0);
+  for (int s = 0; s < ns; ++s)
+    for (Index k = 0; k < sys.locals[s].n_flat(); ++k) z[sys.locals[s].gmap[k]] += contrib[s][k];
+  return z;
+}
+
+Vec SchurSystem::apply_lumped(const Vec& r) const {
+  return one_level(*this, r, [](const LocalSchur& ls, const Vec& rl) {
+    if (ls.Kgg.rows != ls.n_flat()) throw std::invalid_argument("lumped preconditioner: K~_GG not assembled");
+    Vec zl(rl.size());
+    gemv(ls.Kgg, rl.data(), zl.data());
+    return zl;
+  });
+}
+
+Vec SchurSystem::apply_nn1(const Vec& r) const {
+  return one_level(*this, r, [](const LocalSchur& ls, const Vec& rl) {
+    if (ls.S_llt.n != ls.n_flat()) throw std::invalid_argument("nn1 preconditioner: S_s not factored");
+    Vec zl = rl;
+    ls.S_llt.solve_in_place(zl.data());
+    return zl;
+  });
+}
+
+Vec SchurSystem::apply(int kind, const Vec& r) const {
+  return kind == 1 ? apply_nn1(r) : kind == 2 ? apply_lumped(r) : apply_nn2(r);
 }
 
 // src/dd.cpp:199-253
@@ -470,6 +513,7 @@ void SgSolver::assemble_subdomains() {
           }
       });
     }
+    if (opt_.precond == 2) ls.Kgg = ls.S;  // A_GG before the elimination
     if (ni > 0 && ng > 0) {
       // S -= A_IG^T A_II^{-1} A_IG, panels of RHS in band index space, columns
       // ordered by their first non-zero band row so panels skip leading zeros.
@@ -508,7 +552,7 @@ void SgSolver::assemble_subdomains() {
     }
     schur_.locals[s] = std::move(ls);
   });
-  schur_.finalize();
+  schur_.finalize(opt_.precond == 1);
 }
 
 void SgSolver::interior_solve(int s, double* flat) const {
@@ -601,7 +645,7 @@ Vec SgSolver::step_rhs_and_solve(const StateTriple& st, const Vec& f_next, PcgRe
   }
   const double tp = now_s();
   const LinearOp mv = [this](const Vec& x) { return schur_.matvec(x); };
-  const LinearOp pc = [this](const Vec& r) { return schur_.apply_nn2(r); };
+  const LinearOp pc = [this](const Vec& r) { return schur_.apply(opt_.precond, r); };
   const Vec u_iface = pcg(mv, pc, g_iface, opt_.tol, opt_.max_iter, report);
   t_pcg += now_s() - tp;
   Vec u_next(N);

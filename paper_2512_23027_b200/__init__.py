@@ -6,6 +6,8 @@ over ctypes.  There is no CPU fallback: importing the solver requires the
 compiled libsgw_b200.so and every compute call runs on the GPU.
 """
 from .sgwave import (  # noqa: F401
+    PRECONDS,
+    DetSolver,
     ForceSpec,
     LocalGroup,
     NewmarkParams,
@@ -14,6 +16,8 @@ from .sgwave import (  # noqa: F401
     SgHistory,
     SgOptions,
     SgSolver,
+    SolveOptions,
+    TimeHistory,
     TripleTensor,
     gaussian_pulse,
     lib_path,
@@ -22,6 +26,8 @@ from .sgwave import (  # noqa: F401
     nccl_unique_id,
     nearest_node,
     moments,
+    precond_from_string,
+    run_precond_comparison,
     ricker,
     shard_plan,
     triple_products,

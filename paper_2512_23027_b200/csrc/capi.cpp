@@ -89,6 +89,8 @@ Problem problem_from(const sgw_problem* p) {
     P.density = p->density, P.alpha0 = p->alpha0, P.alpha1 = p->alpha1;
     P.gamma = p->gamma, P.zeta = p->zeta, P.dt = p->dt, P.tol = p->tol, P.max_iter = p->max_iter;
     P.device = p->device, P.rank = p->rank, P.world = p->world_size < 1 ? 1 : p->world_size;
+    if (p->precond < 0 || p->precond > 2) throw Error(SGW_EINVAL, "unknown preconditioner");  // precond_from_string
+    P.precond = p->precond;
     if (P.rank < 0 || P.rank >= P.world) throw Error(SGW_EINVAL, "rank out of range");
     if (P.world > P.px * P.py) throw Error(SGW_EINVAL, "more ranks than subdomains");
     return P;
@@ -185,6 +187,18 @@ int sgw_apply_nn2(sgw_solver* s, const double* r, double* z) {
     h2d(dx, r, g.NG, g.stream());
     dy.alloc(g.NG);
     g.apply_nn2(dx.p, dy.p);
+    d2h(z, dy.p, g.NG, g.stream());
+  });
+}
+
+int sgw_apply_precond(sgw_solver* s, int kind, const double* r, double* z) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    if (kind < 0 || kind > 2) throw Error(SGW_EINVAL, "unknown preconditioner");
+    DBuf<double> dx, dy;
+    h2d(dx, r, g.NG, g.stream());
+    dy.alloc(g.NG);
+    g.apply_precond(kind, dx.p, dy.p);
     d2h(z, dy.p, g.NG, g.stream());
   });
 }

@@ -395,6 +395,29 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
   ++T.nn2s;
 }
 
+// ------------------------------------------------------- lumped / NN1 ----
+// z = sum_s R_s^T D_s A_s D_s R_s r (dd.cpp:159-195), A_s = S_s^-1 (NN1) or
+// K~_GG,s (lumped), both held as packed symmetric tiles
+void GpuSolver::apply_one_level(TilePack& tp, const double* r, double* z) {
+  gather_li(r, li_x.p, true);
+  symv(tp, li_x.p, nullptr);
+  const int grid = red_grid(NG);
+  scatter_kernel<true><<<grid, 256, 0, st_>>>(z, nullptr, tp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
+                                              inv_p.p, ng_d.p, G.n_iface, NG, 1, tp.rowpart.p, tp.colpart.p,
+                                              tp.d_tile_base.p, tp.d_ntile.p, nullptr, nullptr, nullptr, nullptr);
+  SGW_LAUNCHED();
+  allreduce(z, NG);
+  ++T.nn2s;
+}
+
+void GpuSolver::apply_precond(int kind, const double* r, double* z) {
+  if (kind == 0) return apply_nn2(r, z);
+  TilePack& tp = kind == 1 ? Sinvp : Aggp;
+  if (kind < 0 || kind > 2 || tp.nmat == 0)
+    throw Error(1, "preconditioner not built: construct the solver with this preconditioner");
+  apply_one_level(tp, r, z);
+}
+
 // -------------------------------------------------------------- vectors ----
 void GpuSolver::dot_dev(const double* a, const double* b, long long len, double* out) {
   dot_kernel<<<red_grid(len), 256, 0, st_>>>(a, b, len, dpart.p, dcount.p, out, nullptr);
@@ -413,7 +436,7 @@ double GpuSolver::dot_host(const double* a, const double* b, long long len) {
 // src/pcg.cpp:7-50: x0 = 0; stop on the recurrence residual, confirm with the
 // true residual, restart from it (without resetting p) if the check fails.
 int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
-  if (use_fused_ && !comm_) return pcg_fused(b, x, converged, hist);
+  if (use_fused_ && !comm_ && P.precond == 0) return pcg_fused(b, x, converged, hist);
   cudaEventRecord(ev_[0], st_);
   const long long N = NG;
   const int grid = red_grid(N);
@@ -435,7 +458,7 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     return 0;
   }
   SGW_CUDA(cudaMemcpyAsync(vr.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
-  apply_nn2(vr.p, vz.p);
+  apply_precond(P.precond, vr.p, vz.p);
   dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
   SGW_LAUNCHED();
   cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 1);
@@ -463,7 +486,7 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     SGW_CUDA(cudaMemcpyAsync(h_scal_, scal.p + RR, sizeof(double), cudaMemcpyDeviceToHost, st_));
   };
   auto precond_half = [&]() {
-    apply_nn2(vr.p, vz.p);
+    apply_precond(P.precond, vr.p, vz.p);
     dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
     SGW_LAUNCHED();
     cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 0);
@@ -562,7 +585,7 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     } else if (hist) {
       hist->push_back(rel);
     }
-    apply_nn2(vr.p, vz.p);
+    apply_precond(P.precond, vr.p, vz.p);
     dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
     SGW_LAUNCHED();
     cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 0);

@@ -572,6 +572,8 @@ void GpuSolver::setup_interior_and_schur(int b0, int nb) {
   Sdense_.zero(st_);
   assemble_gg_kernel<<<dim3(cdiv(amax, 128), ns), 128, 0, st_>>>(A, ip_off.p + b0, iface_lid_.p, Sdense_.p, amax, ns);
   SGW_LAUNCHED();
+  if (P.precond == 2)  // lumped: K~_GG before the elimination (det_loop.cpp:165-167, flattened)
+    for (int q = 0; q < ns; ++q) pack_tiles_range(Aggp, b0 + q, Sdense_.p + size_t(q) * amax * amax, amax, st_);
   DBuf<double> R, Y;
   R.alloc(size_t(ns) * B * amax);
   Y.alloc(size_t(ns) * B * amax);
@@ -619,6 +621,8 @@ void GpuSolver::plan_nn2() {
   for (int s = 0; s < ns; ++s) dimsS[s] = nt * ng_[s], dimsQ[s] = nt * nr_[s];
   Sp.plan(dimsS);
   Qp.plan(dimsQ);
+  if (P.precond == 1) Sinvp.plan(dimsS);
+  if (P.precond == 2) Aggp.plan(dimsS);
   roff_ = Qp.xoff;
   d_roff.upload(roff_);
   psioff_.assign(ns + 1, 0);
@@ -665,10 +669,18 @@ void GpuSolver::nn2_batch(int b0, int nb, std::vector<double>& fcc) {
       for (int r : sd.r_local) hr.push_back(j * ng_[s] + r);
       for (int c : sd.c_local) hc.push_back(j * ng_[s] + c);
     }
-    (void)a;
     ri.upload(hr);
     ci.upload(hc);
     const double* Ss = Sdense_.p + size_t(s - b0) * amax * amax;
+    if (P.precond == 1 && a > 0) {  // NN1: llt_regularized(S_s) (dd.cpp:115) as an explicit inverse
+      DBuf<double> Sf;
+      Sf.alloc((size_t)a * a);
+      SGW_CUDA(cudaMemcpy2DAsync(Sf.p, a * sizeof(double), Ss, amax * sizeof(double), a * sizeof(double), a,
+                                 cudaMemcpyDeviceToDevice, st_));
+      spd_inverse(sol_, st_, Sf.p, a, work, info, ("S of subdomain " + std::to_string(s)).c_str());
+      pack_tiles_range(Sinvp, s, Sf.p, a, st_);
+      SGW_CUDA(cudaStreamSynchronize(st_));
+    }
     if (rs > 0) {
       Srr.alloc((size_t)rs * rs);
       extract_kernel<<<cdiv((long long)rs * rs, 256), 256, 0, st_>>>(Ss, amax, ri.p, rs, ri.p, rs, Srr.p);

@@ -192,6 +192,10 @@ class GpuSolver {
   void apply_block(int op, const double* x, double* y);                 // K11
   void schur_matvec(const double* x, double* y);                        // K1
   void apply_nn2(const double* r, double* z);                           // K2-K4
+  // make_preconditioner(schur, kind) (dd.cpp:159-253): 0 nn2, 1 nn1, 2 lumped
+  // (nn1 / lumped need Problem::precond == kind: their local operators are
+  // built at setup only when selected)
+  void apply_precond(int kind, const double* r, double* z);
   int pcg(const double* b, double* x, bool* converged, std::vector<double>* hist);  // K5
   void init_state(const double* u0_nodal_dev, const double* v0_nodal_dev, double f0_scale);
   void set_force_point(int node, double f0, double t0, double amp);
@@ -290,8 +294,9 @@ class GpuSolver {
   std::vector<long long> roff_, coff_, psioff_;
   DBuf<long long> d_roff, d_coff, d_psioff;
 
-  // PCG matrices
-  TilePack Sp, Qp;
+  // PCG matrices (Sinvp: S_s^-1 for NN1, Aggp: A_GG,s for lumped; only when selected)
+  TilePack Sp, Qp, Sinvp, Aggp;
+  void apply_one_level(TilePack& tp, const double* r, double* z);
   DBuf<double> Psi, Finv;
   std::vector<double> fcc_host_;
   // interior factor

@@ -47,7 +47,7 @@ class _Problem(C.Structure):
                 ("density", C.c_double), ("alpha0", C.c_double), ("alpha1", C.c_double),
                 ("gamma", C.c_double), ("zeta", C.c_double), ("dt", C.c_double),
                 ("tol", C.c_double), ("max_iter", C.c_int), ("device", C.c_int),
-                ("rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p)]
+                ("rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p), ("precond", C.c_int)]
 
 
 class _Force(C.Structure):
@@ -79,6 +79,7 @@ def load_library():
     L.sgw_apply_block.argtypes = [vp, ip, vp, vp]
     L.sgw_schur_matvec.argtypes = [vp, vp, vp]
     L.sgw_apply_nn2.argtypes = [vp, vp, vp]
+    L.sgw_apply_precond.argtypes = [vp, C.c_int, vp, vp]
     L.sgw_pcg.argtypes = [vp, vp, vp, vp, vp, vp, ip]
     L.sgw_coarse_operator.argtypes = [vp, vp]
     L.sgw_run.argtypes = [vp, vp, vp, ip, C.POINTER(_Force), C.POINTER(_History)]
@@ -196,7 +197,8 @@ class NewmarkParams:  # include/sgwave/newmark.hpp:11-19
 
 
 @dataclass
-class SgOptions:  # include/sgwave/sg.hpp:15-21
+class SgOptions:  # include/sgwave/sg.hpp:15-21 (+ SolveOptions::precond, det_loop.hpp:14)
+    precond: str = "nn2"  # PrecondKind: "nn2" (the SG path, sg.cpp:330), "nn1", "lumped"
     tol: float = 1e-8
     max_iter: int = 500
     store_full: bool = False
@@ -303,11 +305,36 @@ class SchurSystem:
         _check(load_library().sgw_apply_nn2(self._s._h, _p(r), _p(z)))
         return z
 
+    def apply_nn1(self, r):
+        """SchurSystem::apply_nn1 (src/dd.cpp:178-195); the solver must use precond "nn1"."""
+        return self.apply_precond("nn1", r)
+
+    def apply_lumped(self, r):
+        """SchurSystem::apply_lumped (src/dd.cpp:159-176); the solver must use precond "lumped"."""
+        return self.apply_precond("lumped", r)
+
+    def apply_precond(self, kind, r):
+        """make_preconditioner(system, kind)(r) (src/dd.cpp)."""
+        r = _f64(r)
+        z = np.zeros(self._s.n_global)
+        _check(load_library().sgw_apply_precond(self._s._h, precond_from_string(kind), _p(r), _p(z)))
+        return z
+
     def coarse_operator(self):
         n = self.n_corner
         out = np.zeros(n * n)
         _check(load_library().sgw_coarse_operator(self._s._h, _p(out)))
         return out.reshape(n, n).T.copy()
+
+
+PRECONDS = ("nn2", "nn1", "lumped")
+
+
+def precond_from_string(name) -> int:
+    """precond_from_string (include/sgwave/dd.hpp:100): unknown names are rejected."""
+    if name not in PRECONDS:
+        raise SgInvalidArgument(SGW_EINVAL, f"unknown preconditioner {name!r}")
+    return PRECONDS.index(name)
 
 
 def shard_plan(n_sub: int, world_size: int) -> list[range]:
@@ -391,7 +418,7 @@ class SgSolver:
         prob = _Problem(nx, ny, px, py, self._coeff.shape[0], _p(self._coeff), int(tensor.n_output), len(tv),
                         _p(ti), _p(tj), _p(tk), _p(tv), density, alpha0, alpha1, self.params.gamma,
                         self.params.zeta, self.params.dt, self.options.tol, self.options.max_iter,
-                        self.options.device, rank, world_size, None)
+                        self.options.device, rank, world_size, None, precond_from_string(self.options.precond))
         if self._coeff.shape[0] != tensor.n_input:
             raise SgInvalidArgument(SGW_EINVAL, "SgSolver: coefficient terms do not match tensor input size")
         self.rank, self.world_size = rank, world_size
@@ -512,3 +539,94 @@ class SgSolver:
         o = np.zeros(1)
         _check(load_library().sgw_bench_kernel(self._h, which, reps, _p(o)))
         return float(o[0])
+
+
+# ----------------------------------------------------- deterministic solver --
+@dataclass
+class SolveOptions:  # include/sgwave/det_loop.hpp:14-21
+    precond: str = "nn2"
+    tol: float = 1e-8
+    max_iter: int = 500
+    store_full: bool = False
+    probe_nodes: list = field(default_factory=list)
+    device: int = 0
+
+
+@dataclass
+class TimeHistory:  # include/sgwave/det_loop.hpp:23-30
+    times: np.ndarray
+    probe_u: np.ndarray                 # n_probes x (n_steps + 1)
+    full_u: np.ndarray | None           # (n_steps + 1) x n_dofs
+    iterations: np.ndarray              # PcgReport::iterations per step
+    residual: np.ndarray
+
+    def mean_iterations(self):          # det_loop.cpp:10-15
+        return float(self.iterations.mean()) if len(self.iterations) else 0.0
+
+
+class DetSolver:
+    """DetSolver (include/sgwave/det_loop.hpp:37-52, src/det_loop.cpp) on the
+    B200 path: the deterministic problem is the SG system with one chaos term
+    (c_000 = 1, the coefficient field = speed_sq; test_sg.cpp:158-178), solved
+    by the same kernels with the lumped / NN1 / NN2 preconditioner.  The
+    preconditioner's local operators are built at construction, so
+    set_preconditioner() rebuilds the GPU solver (setup is seconds at these
+    sizes)."""
+
+    def __init__(self, nx, ny, px, py, speed_sq, density=1.0, alpha0=0.5445, alpha1=0.0174,
+                 params: NewmarkParams | None = None, options: SolveOptions | None = None):
+        self.nx, self.ny, self.px, self.py = nx, ny, px, py
+        self.speed_sq = _f64(speed_sq).reshape(1, -1)
+        self.density, self.alpha0, self.alpha1 = density, alpha0, alpha1
+        self.params = params or NewmarkParams()
+        self.options = options or SolveOptions()
+        self._build()
+
+    def _build(self):
+        o = self.options
+        self._sg = SgSolver(self.nx, self.ny, self.px, self.py, self.speed_sq, triple_products(1, 0, 0),
+                            self.density, self.alpha0, self.alpha1, self.params,
+                            SgOptions(precond=o.precond, tol=o.tol, max_iter=o.max_iter, store_full=o.store_full,
+                                      probe_nodes=list(o.probe_nodes), device=o.device))
+        self.n_dofs = self._sg.n_dofs
+
+    def schur(self):
+        return self._sg.schur()
+
+    def uses_direct(self):
+        return False
+
+    def set_preconditioner(self, kind):  # det_loop.hpp:50
+        precond_from_string(kind)
+        if kind != self.options.precond:
+            self.options.precond = kind
+            self._sg.close()
+            self._build()
+
+    def set_tolerance(self, tol):  # det_loop.hpp:51
+        if tol != self.options.tol:
+            self.options.tol = tol
+            self._sg.close()
+            self._build()
+
+    def run(self, u0_nodal, v0_nodal, n_steps, force: ForceSpec | None = None) -> TimeHistory:
+        h = self._sg.run(u0_nodal, v0_nodal, n_steps, force)
+        probe_u = h.probe_coeffs[:, 0, :] if h.probe_coeffs is not None else h.probe_mean
+        return TimeHistory(h.times, probe_u, h.full_state, h.iterations, h.residual)
+
+
+def run_precond_comparison(nx, dt, t_final, partitions, tol=1e-8, max_iter=500, device=0):
+    """run_precond_comparison (src/experiments.cpp:82-111): mean PCG iterations
+    of the Gaussian-pulse problem per preconditioner and partition."""
+    u0 = gaussian_pulse(nx, nx, 0.7, 0.7, 1.0, 0.01)
+    v0 = np.zeros_like(u0)
+    steps = int(math.ceil(t_final / dt - 1e-12))
+    out = {"subdomain_counts": [], "lumped": [], "nn1": [], "nn2": []}
+    for px, py in partitions:
+        out["subdomain_counts"].append(px * py)
+        for kind in ("lumped", "nn1", "nn2"):
+            s = DetSolver(nx, nx, px, py, np.ones((nx + 1) ** 2), 1.0, 0.5445, 0.0174, NewmarkParams(dt=dt),
+                          SolveOptions(precond=kind, tol=tol, max_iter=max_iter, device=device))
+            out[kind].append(s.run(u0, v0, steps).mean_iterations())
+            s._sg.close()
+    return out

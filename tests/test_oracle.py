@@ -233,3 +233,49 @@ def test_recorded_deterministic_nn2_iterations():
         u0 = O.gaussian_pulse(nx, nx)
         got.append(s.run(u0, 0 * u0, math.ceil(0.5 / 0.01 - 1e-12))["mean_iterations"])
     assert [f"{g:.1f}" for g in got] == ["3.0"] * 3
+
+
+# ------------------------------------- lumped / NN1 / NN2 ---
+def _det(nx, px, py, dt, precond, tol=1e-10, alpha0=0.5445, alpha1=0.0174):
+    """DetSolver(mesh, part, ones, 1, alpha0, alpha1, params, opt) of test_dd.cpp:54-66:
+    the SG solver with one PCE term (test_sg.cpp:158-178) and the chosen preconditioner."""
+    one = np.ones((1, (nx + 1) ** 2))
+    return O.SgSolver(nx, nx, px, py, one, O.triple_products(1, 0, 0), dt=dt, tol=tol, threads=2,
+                      alpha0=alpha0, alpha1=alpha1, precond=precond)
+
+
+@pytest.mark.parametrize("kind", ["lumped", "nn1", "nn2"])
+def test_preconditioners_are_symmetric(kind):
+    # test_dd.cpp:109-121 (epsilon 1e-10)
+    s = _det(8, 2, 2, 0.05, kind, alpha0=0.2, alpha1=0.01)
+    r1, r2 = rand(s.n_global, 1), rand(s.n_global, 2)
+    a, b = r2 @ s.apply_precond(kind, r1), r1 @ s.apply_precond(kind, r2)
+    assert abs(a - b) <= 1e-10 * max(abs(a), abs(b))
+
+
+@pytest.mark.parametrize("kind", ["lumped", "nn1", "nn2"])
+def test_dd_trajectory_matches_direct_for_every_preconditioner(kind):
+    # test_dd.cpp:248-270 (<= 1e-8); recorded proj/test_output.txt:43 (criterion 4):
+    # "nn2: 8.76e-14  nn1: 4.49e-13  lumped: 1.91e-15"
+    nx, dt, steps = 16, 0.02, 12
+    direct = _det(nx, 1, 1, dt, "nn2")
+    dd = _det(nx, 2, 2, dt, kind, tol=1e-12)
+    assert direct.uses_direct and not dd.uses_direct
+    u0 = O.gaussian_pulse(nx, nx)
+    a = direct.run(u0, 0 * u0, steps, store_full=True)["full"]
+    b = dd.run(u0, 0 * u0, steps, store_full=True)["full"]
+    assert np.abs(a - b).max() <= 1e-8
+
+
+def test_recorded_preconditioner_comparison():
+    # acceptance.cpp:156-177 (run_precond_comparison(40, 0.01, 0.5, {2x2, 4x2, 4x4}, 2, 1e-8, 500),
+    # experiments.cpp:82-111), recorded proj/test_output.txt:44:
+    # "lumped: 11.2/11.5/12.0 nn1: 3.7/3.9/4.0 nn2: 3.0/3.0/3.0"
+    nx, dt = 40, 0.01
+    steps = math.ceil(0.5 / dt - 1e-12)
+    u0 = O.gaussian_pulse(nx, nx)
+    got = {}
+    for kind in ("lumped", "nn1", "nn2"):
+        got[kind] = [f"{_det(nx, px, py, dt, kind, tol=1e-8).run(u0, 0 * u0, steps)['mean_iterations']:.1f}"
+                     for px, py in [(2, 2), (4, 2), (4, 4)]]
+    assert got == {"lumped": ["11.2", "11.5", "12.0"], "nn1": ["3.7", "3.9", "4.0"], "nn2": ["3.0", "3.0", "3.0"]}
