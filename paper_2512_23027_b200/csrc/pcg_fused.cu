@@ -190,12 +190,12 @@ __device__ __forceinline__ double grid_sum(double v, double* part, int slot, cg:
   v = block_total(v, sm);
   if (threadIdx.x == 0) part[(size_t)slot * gridDim.x + blockIdx.x] = v;
   g.sync();
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += __ldcg(part + (size_t)slot * gridDim.x + b);
-    s = warp_sum(s);
-    if (threadIdx.x == 0) sm.red[32] = s;
-  }
+  // all threads load the block totals (<= 2 each), then a fixed-shape block
+  // reduction: the same value, bitwise, in every CTA
+  double s = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += __ldcg(part + (size_t)slot * gridDim.x + b);
+  s = block_total(s, sm);
+  if (threadIdx.x == 0) sm.red[32] = s;
   __syncthreads();
   const double t = sm.red[32];
   __syncthreads();
