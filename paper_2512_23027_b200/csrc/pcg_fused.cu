@@ -29,61 +29,57 @@ namespace cg = cooperative_groups;
 
 namespace sgw {
 
-// A TilePack walked in contiguous tile ranges, one per CTA (tiles are ordered
-// matrix by matrix, row-major over the lower tiles (I, J <= I)).  A CTA keeps
-// the local input vector of its current matrix and a local accumulator in
-// shared memory, adds every tile's row and column products into it, and at
-// a matrix boundary writes the accumulator as its partial of that matrix:
-// y_s = sum over the CTAs covering s of their partials, in CTA order.
+// A tile pack walked in contiguous tile ranges, one per CTA.  Two kinds:
+//  * symmetric (S_s, Q_s): lower 64x64 tiles (I, J <= I), row-major over the
+//    tiles of a matrix, diagonal tiles full, 32 KB each;
+//  * rectangular (Psi_s^T): tiles (I, J), I over 64-wide corner-column chunks,
+//    J over 64-row blocks of the remaining dofs, row-major; tile (I, J) is the
+//    column-major 64 x w chunk of Psi_s (w = the chunk's valid columns, rows
+//    past r_s stored as zeros), i.e. row-major Psi^T rows of stride 64, w x 512
+//    bytes, so one bulk copy moves only stored data.
+// A CTA keeps the local input vector of its current matrix and a local
+// accumulator in shared memory, adds every tile's row and column products
+// into it (tile_acc), and at a matrix boundary writes the accumulator as its
+// partial of that matrix: y_s = sum over the CTAs covering s of their
+// partials, in CTA order.  Local vectors: symmetric [64 nt]; rectangular
+// [64 nI (corner chunks) | 64 nJ (remaining-dof blocks)].
 struct RangePack {
   const double* tiles;
-  const int* nt;              // tiles per side, per matrix
-  const long long* xoff;      // local vector offset per matrix (padded, 64 nt)
+  const long long* toff;      // per tile: offset in doubles (null: t * 4096)
+  const int* tbytes;          // per tile: bytes (null: 32 KB)
+  const int* nI;              // per matrix: tile rows (symmetric: tiles per side)
+  const int* nJ;              // per matrix: tile columns (rectangular only)
+  int rect;
   const long long* t_first;   // [G + 1] first tile of each CTA's range
   const int4* start;          // [G] {matrix, I, J} of each CTA's first tile
   const int* c0;              // per matrix: first CTA covering it
   const int* ncta;            // per matrix: CTAs covering it
   const long long* pbase;     // per matrix: offset of its partials in part
-  double* part;               // partials [pbase[s] + (c - c0[s]) 64 nt[s] + i]
+  double* part;               // partials [pbase[s] + (c - c0[s]) len_s + i]
 };
 
 struct FusedPcg {
-  long long NG, ncol_total;
+  long long NG;
   int n_iface, NT, NS, n_corner, NC, max_iter, hist_cap;
   double tol;
   const double* b;
-  double *x, *r, *z, *p, *q;
-  const int4* s_desc;
-  const double* s_tiles;
-  long long s_ntiles;
-  double *s_row, *s_col;
-  const long long *s_base, *s_xoff;
-  const int *s_nt, *smap;
-  const int4* q_desc;
-  const double* q_tiles;
-  long long q_ntiles;
-  double *q_row, *q_col;
-  const long long *q_base, *q_xoff;
-  const int* q_nt;
+  double *x, *r, *z, *p;
+  double* q;                     // scratch (true residual)
+  const long long *s_xoff, *q_xoff;
   double *fr, *fc;
-  const int *inv_cnt, *inv_s, *inv_p, *ip_off, *ng, *nr, *nc, *pkind, *cpos_flat, *cp_off;
+  const int *inv_cnt, *inv_s, *inv_p, *ip_off, *ng, *nr, *nc, *pkind;
   const double* iface_w;
   const int *cinv_cnt, *cinv_s, *cinv_c;
-  const long long *roff, *coff, *psioff;
-  const double *Psi, *Finv;
-  double *dsub, *dco, *uco;
+  const long long *roff, *coff;
+  const double* Finv;
+  double *dco, *uco, *ucl;       // d, u_c (flat coarse), B_s u_c (c-space, compact)
   double* part;  // 8 slots x gridDim
   int* out;      // [0] iterations, [1] converged
   double* hist;  // residual history, hist_cap entries
-  const int2 *s_tx, *q_tx;       // per-tile local offsets of the I / J segments
   double *li_z, *li_p, *li_x;    // z, p, x in S-local layout (written by their producers)
   double* tphase;                // 8 accumulated phase times (ns), CTA 0
-  double *ucl, *wr;              // B_s u_c (c-space) and Psi_s B_s u_c (r-space, padded)
-  long long rlen;                // padded r-space length
-  RangePack rs, rq;              // contiguous tile ranges per CTA of S and Q
+  RangePack rs, rq, rp;          // contiguous tile ranges per CTA of S, Q and Psi^T
   int nst, maxlen;               // ring stages; longest local vector (doubles)
-  int l2pf;                      // tiles hinted into L2 beyond the ring at a phase switch
-  int psi_late;                  // Psi^T f_r after the Q tiles instead of before
 };
 
 extern __shared__ __align__(128) double dyn_smem[];  // ring stages, local vector, accumulator
@@ -150,23 +146,31 @@ struct Ring {
   int pre_kind;          // tile set whose first tiles are already issued for the next phase
 };
 
-__device__ __forceinline__ void ring_issue(Ring& R, const RangePack& P, long long k) {
-  const long long t = P.t_first[blockIdx.x] + k;
-  if (t >= P.t_first[blockIdx.x + 1]) return;
+// tile k of this CTA's range of P, continuing into the range of `next` past
+// its end (the next walk's first tiles stream in during this one's tail)
+__device__ __forceinline__ void ring_issue(Ring& R, const RangePack& P, long long k, const RangePack* next) {
+  const RangePack* Q = &P;
+  long long t = P.t_first[blockIdx.x] + k;
+  const long long t1 = P.t_first[blockIdx.x + 1];
+  if (t >= t1) {
+    if (!next) return;
+    Q = next;
+    t = next->t_first[blockIdx.x] + (t - t1);
+    if (t >= next->t_first[blockIdx.x + 1]) return;
+  }
+  const double* src = Q->tiles + (Q->toff ? Q->toff[t] : t * (kTile * kTile));
+  const unsigned bytes = Q->tbytes ? (unsigned)Q->tbytes[t] : kTileBytes;
   const int st = R.issued % R.nst;
-  mb_load(R.stage + (size_t)st * kTile * kTile, P.tiles + t * (kTile * kTile), kTileBytes, &R.full[st]);
+  mb_load(R.stage + (size_t)st * kTile * kTile, src, bytes, &R.full[st]);
   ++R.issued;
 }
-// issue the first tiles of set `kind` for the next tile phase (thread 0),
-// and hint the following l2pf tiles into L2 (they stream during glue phases)
-__device__ __forceinline__ void ring_prefetch(Ring& R, int kind, const RangePack& P, int l2pf) {
-  if (threadIdx.x == 0) {
-    for (int n = 0; n < R.nst; ++n) ring_issue(R, P, n);
-    const long long t1 = P.t_first[blockIdx.x + 1];
-    for (long long t = P.t_first[blockIdx.x] + R.nst, e = t + l2pf; t < e && t < t1; ++t)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.tiles + t * (kTile * kTile)), "r"(kTileBytes)
-                   : "memory");
-  }
+// issue the first tiles of set `kind` for the next tile phase (thread 0).
+// The ring always holds the next nst tiles of the consumption sequence: a
+// walk of P chained to `next` consumes P's range, then next's; a walk without
+// `next` leaves the ring empty.
+__device__ __forceinline__ void ring_prefetch(Ring& R, int kind, const RangePack& P, const RangePack* next) {
+  if (threadIdx.x == 0)
+    for (int n = 0; n < R.nst; ++n) ring_issue(R, P, n, next);
   R.pre_kind = kind;
 }
 
@@ -287,42 +291,44 @@ __device__ __forceinline__ void range_flush(const RangePack& P, int s, int len, 
 }
 
 // One tile phase over this CTA's contiguous tile range of a pack; the local
-// input vector of each matrix is gathered by xval(local offset) into xs.
+// input vector of each matrix s is gathered by xval(s, i) into xs.  With
+// `next`, the first tiles of next's range are issued during this walk's tail
+// (the caller then marks them as prefetched).
 template <typename XF>
-__device__ void range_phase(Ring& R, int kind, const RangePack& P, double* xs, double* acc, Smem& sm, XF xval) {
-  if (R.pre_kind != kind) ring_prefetch(R, kind, P, 0);
+__device__ void range_phase(Ring& R, int kind, const RangePack& P, const RangePack* next, double* xs, double* acc,
+                            Smem& sm, XF xval) {
+  if (R.pre_kind != kind) ring_prefetch(R, kind, P, next);
   R.pre_kind = 0;
   const long long t0 = P.t_first[blockIdx.x], t1 = P.t_first[blockIdx.x + 1];
   if (t0 >= t1) return;
   const int4 st0 = P.start[blockIdx.x];
-  int s = st0.x, I = st0.y, J = st0.z, cur = -1, len = 0, nt = 0;
+  int s = st0.x, I = st0.y, J = st0.z, cur = -1, len = 0, nI = 0, nJ = 0, xoJ = 0;
   for (long long t = t0, k = 0; t < t1; ++t, ++k) {
     if (s != cur) {
       if (cur >= 0) range_flush(P, cur, len, acc);  // same thread owns index i in both loops
-      cur = s, nt = P.nt[s], len = kTile * nt;
-      const long long xo = P.xoff[s];
-      for (int i = threadIdx.x; i < len; i += blockDim.x) xs[i] = xval(xo + i), acc[i] = 0.0;
+      cur = s, nI = P.nI[s], nJ = P.rect ? P.nJ[s] : nI;
+      xoJ = P.rect ? kTile * nI : 0;
+      len = kTile * (P.rect ? nI + nJ : nI);
+      for (int i = threadIdx.x; i < len; i += blockDim.x) xs[i] = xval(s, i), acc[i] = 0.0;
       __syncthreads();
     }
     const int stg = R.consumed % R.nst;
     mb_wait(&R.full[stg], (R.consumed / R.nst) & 1);
-    tile_acc(R.stage + (size_t)stg * kTile * kTile, xs + I * kTile, xs + J * kTile, I == J, acc + I * kTile,
-             acc + J * kTile, sm);
+    tile_acc(R.stage + (size_t)stg * kTile * kTile, xs + I * kTile, xs + xoJ + J * kTile, !P.rect && I == J,
+             acc + I * kTile, acc + xoJ + J * kTile, sm);
     __syncthreads();  // stage consumed, accumulator updated
-    if (threadIdx.x == 0) ring_issue(R, P, k + R.nst);
+    if (threadIdx.x == 0) ring_issue(R, P, k + R.nst, next);
     ++R.consumed;
-    if (++J > I) {
+    if (P.rect ? ++J == nJ : ++J > I) {
       J = 0;
-      if (++I == nt) I = 0, ++s;
+      if (++I == nI) I = 0, ++s;
     }
   }
   range_flush(P, cur, len, acc);
 }
 
-// y_s[i] from the partials of the CTAs covering matrix s (CTA order)
-__device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i) {
-  const int len = kTile * P.nt[s], n = P.ncta[s];
-  const double* p = P.part + P.pbase[s] + i;
+// sum of the n CTA partials p[k len] of one local entry, k ascending
+__device__ __forceinline__ double partial_sum(const double* p, int len, int n) {
   double y = 0.0;
   int k = 0;
   for (; k + 4 <= n; k += 4) {
@@ -333,11 +339,21 @@ __device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i)
   for (; k < n; ++k) y += __ldcg(p + (long long)k * len);
   return y;
 }
+// y_s[i] from the partials of the CTAs covering symmetric matrix s
+__device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i) {
+  return partial_sum(P.part + P.pbase[s] + i, kTile * P.nI[s], P.ncta[s]);
+}
+// Psi^T x (corner part, i < 64 nI) or Psi x (remaining-dof part, offset 64 nI)
+// of rectangular matrix s
+__device__ __forceinline__ double rect_reduce(const RangePack& P, int s, int i) {
+  return partial_sum(P.part + P.pbase[s] + i, kTile * (P.nI[s] + P.nJ[s]), P.ncta[s]);
+}
 
 // mode 0: x vector = first ? z : z + beta p (lazy p update); mode 1: x
 __device__ void s_tiles_phase(const FusedPcg& A, Ring& R, Smem& sm, double* xs, double* acc, int mode, bool first,
                               double beta) {
-  range_phase(R, 1, A.rs, xs, acc, sm, [&](long long o) {
+  range_phase(R, 1, A.rs, nullptr, xs, acc, sm, [&](int s, int i) {
+    const long long o = A.s_xoff[s] + i;
     return mode ? __ldcg(A.li_x + o) : (first ? __ldcg(A.li_z + o) : __ldcg(A.li_z + o) + beta * __ldcg(A.li_p + o));
   });
 }
@@ -353,92 +369,101 @@ __device__ __forceinline__ double s_reduce(const FusedPcg& A, long long q) {
 }
 
 
-// z = NN2(r) from the local inputs fr/fc; returns r.z
+// z = NN2(r) from the local inputs fr/fc; returns r.z.
+//  4. Q_s f_r and Psi_s^T f_r: the Q tile walk, then the Psi^T tile walk on
+//     [0 | f_r] (corner part of its partials = Psi^T f_r)
+//  5. d = sum_s B_s^T (f_c - Psi_s^T f_r) (ascending s)
+//  6. u_c = F_cc^-1 d, and B_s u_c per subdomain (c-space)
+//  6b. Psi_s B_s u_c: the Psi^T tile walk on [B_s u_c | 0] (remaining-dof part)
+//  7. z = sum_s R_s^T D_s [Q f_r - Psi u_c ; u_c], r.z
+// Psi is read twice per iteration, as the reference's two S_rc products.
 __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_group& g, PhaseClock& pc) {
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   const long long gwarp = gtid >> 5, nwarps = gstride >> 5;
-  // 4. Psi^T f_r (the first Q tiles stream in meanwhile), Q tiles
   double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;
-  ring_prefetch(R, 2, A.rq, A.l2pf);
-  auto psi_t = [&]() {
-    for (long long wv = gwarp; wv < A.ncol_total; wv += nwarps) {
-      int lo = 0, hi = A.NS;  // subdomain s with coff[s] <= wv < coff[s+1]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (A.coff[mid] <= wv) lo = mid; else hi = mid;
-      }
-      const int s = lo;
-      const int c = int(wv - A.coff[s]), rs = A.NT * A.nr[s];
-      const double* col = A.Psi + A.psioff[s] + (long long)c * rs;
-      const double* f = A.fr + A.roff[s];
-      double acc = 0.0;
-#pragma unroll kUnroll
-      for (int a = lane; a < rs; a += 32) acc += col[a] * f[a];
-      acc = warp_sum(acc);
-      if (lane == 0) A.dsub[wv] = A.fc[wv] - acc;
-    }
-  };
-  if (A.NC > 0 && !A.psi_late) psi_t();
-  range_phase(R, 2, A.rq, xs, xs + A.maxlen, sm, [&](long long o) { return __ldcg(A.fr + o); });
-  ring_prefetch(R, 1, A.rs, A.l2pf);  // next iteration's S tiles stream in during 5-7
-  if (A.NC > 0 && A.psi_late) psi_t();
+  double* acc = xs + A.maxlen;
+  const bool coarse = A.NC > 0;
+  // 4.
+  range_phase(R, 2, A.rq, coarse ? &A.rp : &A.rs, xs, acc, sm,
+              [&](int s, int i) { return __ldcg(A.fr + A.q_xoff[s] + i); });
+  if (coarse) {
+    R.pre_kind = 3;
+    range_phase(R, 3, A.rp, nullptr, xs, acc, sm, [&](int s, int i) {
+      const int o = i - kTile * A.rp.nI[s];  // remaining-dof part: f_r (padded r-space layout)
+      return o >= 0 ? __ldcg(A.fr + A.roff[s] + o) : 0.0;
+    });
+    // the ring is empty: the same tiles again for 6b (then the next
+    // iteration's S tiles) stream in during 5-6
+    ring_prefetch(R, 3, A.rp, &A.rs);
+  } else {
+    R.pre_kind = 1;  // next iteration's S tiles stream in during 7
+  }
   g.sync();
   pc.tick(3);
-  if (A.NC > 0) {
-    // 5. d = sum_s B_s^T d_s (ascending s)
-    for (long long qc = gtid; qc < A.NC; qc += gstride) {
-      const int j = int(qc / A.n_corner), gc = int(qc % A.n_corner);
+  if (coarse) {
+    // 5. one warp per coarse dof: lane group e (8 lanes) takes subdomain e
+    //    (<= 4 share a cross point), its lanes split the CTA partials
+    for (long long qc = gwarp; qc < A.NC; qc += nwarps) {
+      const int j = int(qc / A.n_corner), gc = int(qc % A.n_corner), e = lane >> 3, kk = lane & 7;
       double d = 0.0;
-      for (int e = 0; e < A.cinv_cnt[gc]; ++e) {
-        const int s = A.cinv_s[4 * gc + e];
-        d += A.dsub[A.coff[s] + (long long)j * A.nc[s] + A.cinv_c[4 * gc + e]];
+      if (e < A.cinv_cnt[gc]) {
+        const int s = A.cinv_s[4 * gc + e], c = j * A.nc[s] + A.cinv_c[4 * gc + e];
+        const int len = kTile * (A.rp.nI[s] + A.rp.nJ[s]), n = A.rp.ncta[s];
+        const double* pp = A.rp.part + A.rp.pbase[s] + c;
+        for (int k = kk; k < n; k += 8) d -= __ldcg(pp + (long long)k * len);
+        if (kk == 0) d += __ldcg(A.fc + A.coff[s] + c);
       }
-      A.dco[qc] = d;
+      d = warp_sum(d);
+      if (lane == 0) A.dco[qc] = d;
     }
     g.sync();
     pc.tick(4);
-    // 6. u_c = F_cc^-1 d (symmetric: row = column), plus the per-subdomain
-    //    corner copies B_s u_c (c-space, compact)
+    // 6. (F_cc^-1 symmetric: row = column).  d staged in shared memory when
+    //    it fits; rows streamed with 16-byte loads
+    const bool dsm = A.NC <= 2 * A.maxlen;
+    if (dsm) {
+      for (int c = threadIdx.x; c < A.NC; c += blockDim.x) xs[c] = __ldcg(A.dco + c);
+      __syncthreads();
+    }
     for (long long row = gwarp; row < A.NC; row += nwarps) {
       const double* col = A.Finv + row * A.NC;
-      double acc = 0.0;
+      auto dv = [&](int c) { return dsm ? xs[c] : __ldcg(A.dco + c); };
+      const int h = int((row * A.NC) & 1);  // leading element before the 16-byte aligned part
+      const int n2 = (A.NC - h) >> 1;
+      const double2* c2 = reinterpret_cast<const double2*>(col + h);
+      double a = 0.0;
 #pragma unroll kUnroll
-      for (int c = lane; c < A.NC; c += 32) acc += col[c] * __ldcg(A.dco + c);
-      acc = warp_sum(acc);
+      for (int k = lane; k < n2; k += 32) {
+        const double2 v = __ldg(c2 + k);
+        a += v.x * dv(h + 2 * k) + v.y * dv(h + 2 * k + 1);
+      }
       if (lane == 0) {
-        A.uco[row] = acc;
+        if (h) a += __ldg(col) * dv(0);
+        if ((A.NC - h) & 1) a += __ldg(col + A.NC - 1) * dv(A.NC - 1);
+      }
+      a = warp_sum(a);
+      if (lane == 0) {
+        A.uco[row] = a;
         const int j = int(row / A.n_corner), gc = int(row % A.n_corner);
         for (int e = 0; e < A.cinv_cnt[gc]; ++e) {
           const int s = A.cinv_s[4 * gc + e];
-          A.ucl[A.coff[s] + (long long)j * A.nc[s] + A.cinv_c[4 * gc + e]] = acc;
+          A.ucl[A.coff[s] + (long long)j * A.nc[s] + A.cinv_c[4 * gc + e]] = a;
         }
       }
     }
     g.sync();
     pc.tick(5);
-    // 6b. w_s = Psi_s (B_s u_c) on the remaining dofs (r-space, coalesced over rows)
-    for (long long i = gtid; i < A.rlen; i += gstride) {
-      int lo = 0, hi = A.NS;  // subdomain of padded r-space index i
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (A.roff[mid] <= i) lo = mid; else hi = mid;
-      }
-      const int s = lo, a = int(i - A.roff[s]), rs = A.NT * A.nr[s];
-      if (a >= rs) continue;
-      const double* P = A.Psi + A.psioff[s] + a;
-      const double* u = A.ucl + A.coff[s];
-      const int cs = A.NT * A.nc[s];
-      double acc = 0.0;
-#pragma unroll kUnroll
-      for (int c = 0; c < cs; ++c) acc += P[(long long)c * rs] * __ldcg(u + c);
-      A.wr[i] = acc;
-    }
+    // 6b.
+    range_phase(R, 3, A.rp, &A.rs, xs, acc, sm, [&](int s, int i) {
+      return i < A.NT * A.nc[s] ? __ldcg(A.ucl + A.coff[s] + i) : 0.0;
+    });
+    R.pre_kind = 1;  // next iteration's S tiles stream in during 7
     g.sync();
     pc.tick(5);
   }
-  // 7. z = sum_s R_s^T D_s zeta_s ; r.z
-  double acc = 0.0;
+  // 7.
+  double rz = 0.0;
   for (long long q = gtid; q < A.NG; q += gstride) {
     const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
     double zq = 0.0;
@@ -450,17 +475,17 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
       if (kind >= 0) {
         const int ar = j * A.nr[s] + kind;
         v = range_reduce(A.rq, s, ar);
-        if (A.NC > 0) v -= __ldcg(A.wr + A.roff[s] + ar);  // u_r = Q f_r - Psi u_c
+        if (coarse) v -= rect_reduce(A.rp, s, kTile * A.rp.nI[s] + ar);  // u_r = Q f_r - Psi u_c
       } else {
-        v = A.NC > 0 ? __ldcg(A.ucl + A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)) : 0.0;
+        v = coarse ? __ldcg(A.ucl + A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)) : 0.0;
       }
       zq += wgt * v;
     }
     A.z[q] = zq;
     write_local_s(A, A.li_z, q, zq);
-    acc += A.r[q] * zq;
+    rz += A.r[q] * zq;
   }
-  const double rzv = grid_sum(acc, A.part, 4, g, sm);
+  const double rzv = grid_sum(rz, A.part, 4, g, sm);
   pc.tick(6);
   return rzv;
 }
@@ -476,6 +501,10 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   double* xacc = xs + A.maxlen;
   PhaseClock pc{leader && A.tphase != nullptr, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pc.last));
+  // stages start zeroed: rows past a narrow Psi chunk then always hold finite
+  // values (they only meet zero inputs or padding outputs)
+  for (int i = threadIdx.x; i < A.nst * kTile * kTile; i += blockDim.x) dyn_smem[i] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the first bulk copy overwrites them
   if (threadIdx.x == 0) {
     for (int i = 0; i < A.nst; ++i) mb_init(&ring_bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -582,34 +611,94 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
 }
 
 // --------------------------------------------------------------- host ----
-void RangeBufs::plan(const TilePack& tp, int grid) {
-  std::vector<long long> tf(grid + 1), pb(tp.nmat + 1, 0);
+// Contiguous tile ranges per CTA over a pack whose matrix s holds tiles
+// [tile_base[s], tile_base[s + 1]) in row-major order: lower tiles of an
+// nI x nI symmetric matrix (nJ empty), or all nI x nJ tiles (rectangular).
+void RangeBufs::plan(const std::vector<long long>& tile_base, const std::vector<int>& nI, const std::vector<int>& nJ,
+                     int grid) {
+  const int nmat = int(nI.size());
+  const bool rect = !nJ.empty();
+  const long long n_tiles = tile_base[nmat];
+  std::vector<long long> tf(grid + 1), pb(nmat + 1, 0);
   std::vector<int4> st(grid, make_int4(0, 0, 0, 0));
-  std::vector<int> c0(tp.nmat, 0), nc(tp.nmat, 0);
-  for (int c = 0; c <= grid; ++c) tf[c] = tp.n_tiles * c / grid;
-  // matrix, I, J of every CTA's first tile; CTAs covering each matrix
-  auto cta_of = [&](long long t) {  // CTA whose range holds tile t
+  std::vector<int> c0(nmat, 0), nc(nmat, 0);
+  for (int c = 0; c <= grid; ++c) tf[c] = n_tiles * c / grid;
+  auto cta_of = [&](long long t) {  // CTA whose (non-empty) range holds tile t
     return int(std::upper_bound(tf.begin(), tf.end(), t) - tf.begin()) - 1;
   };
-  for (int c = 0; c < grid; ++c) {
+  for (int c = 0; c < grid; ++c) {  // matrix, I, J of every CTA's first tile
     if (tf[c] >= tf[c + 1]) continue;
-    const int s = int(std::upper_bound(tp.tile_base.begin(), tp.tile_base.end(), tf[c]) - tp.tile_base.begin()) - 1;
-    long long r = tf[c] - tp.tile_base[s];
+    const int s = int(std::upper_bound(tile_base.begin(), tile_base.end(), tf[c]) - tile_base.begin()) - 1;
+    long long r = tf[c] - tile_base[s];
     int I = 0;
-    while (r > I) r -= ++I;  // row-major lower order: row I holds I + 1 tiles
+    if (rect) {
+      I = int(r / nJ[s]), r %= nJ[s];
+    } else {
+      while (r > I) r -= ++I;  // row I holds I + 1 tiles
+    }
     st[c] = make_int4(s, I, int(r), 0);
   }
-  for (int s = 0; s < tp.nmat; ++s) {
-    const int a = cta_of(tp.tile_base[s]), b = cta_of(tp.tile_base[s + 1] - 1);
-    c0[s] = a, nc[s] = b - a + 1;
-    pb[s + 1] = pb[s] + (long long)nc[s] * kTile * tp.ntile[s];
+  for (int s = 0; s < nmat; ++s) {  // CTAs covering each matrix and its partials
+    if (tile_base[s + 1] > tile_base[s]) {
+      const int a = cta_of(tile_base[s]), b = cta_of(tile_base[s + 1] - 1);
+      c0[s] = a, nc[s] = b - a + 1;
+    }
+    pb[s + 1] = pb[s] + (long long)nc[s] * kTile * (nI[s] + (rect ? nJ[s] : 0));
   }
   t_first.upload(tf), start.upload(st);
   this->c0.upload(c0), ncta.upload(nc), pbase.upload(pb);
-  part.alloc(std::max<long long>(1, pb[tp.nmat]));
+  part.alloc(std::max<long long>(1, pb[nmat]));
   SGW_CUDA(cudaMemset(part.p, 0, part.n * sizeof(double)));  // slots of CTAs with empty ranges stay 0
 }
 
+// Psi_s (column-major r_s x c_s) -> tile (I, J) = column-major 64 x w chunk of
+// columns [64 I, 64 I + w), rows [64 J, 64 J + 64) (zeros past r_s).  One CTA per tile.
+__global__ void psi_tiles_kernel(const double* __restrict__ Psi, const long long* __restrict__ psioff,
+                                 const int4* __restrict__ desc, const long long* __restrict__ toff,
+                                 const int* __restrict__ nr, const int* __restrict__ nc, int nt,
+                                 double* __restrict__ tiles) {
+  const int4 d = desc[blockIdx.x];  // {s, I, J, w}
+  const int rs = nt * nr[d.x];
+  const double* src = Psi + psioff[d.x];
+  double* dst = tiles + toff[blockIdx.x];
+  for (int e = threadIdx.x; e < d.w * kTile; e += blockDim.x) {
+    const int c = 64 * d.y + e / kTile, r = 64 * d.z + e % kTile;
+    dst[e] = r < rs ? src[(long long)c * rs + r] : 0.0;
+  }
+}
+
+void GpuSolver::build_psi_tiles() {
+  std::vector<int> nI(NS), nJ(NS);
+  std::vector<long long> base(NS + 1, 0), toff;
+  std::vector<int> bytes;
+  std::vector<int4> desc;
+  long long off = 0;
+  for (int s = 0; s < NS; ++s) {
+    const int cs = NT * nc_[s];
+    nI[s] = cdiv(cs, kTile), nJ[s] = Qp.ntile[s];  // Qp: the r_s = NT nr_s remaining dofs
+    for (int I = 0; I < nI[s]; ++I)
+      for (int J = 0; J < nJ[s]; ++J) {
+        const int w = std::min(kTile, cs - kTile * I);
+        desc.push_back(make_int4(s, I, J, w));
+        toff.push_back(off);
+        bytes.push_back(w * kTile * 8);
+        off += (long long)w * kTile;
+      }
+    base[s + 1] = (long long)desc.size();
+  }
+  psi_nI_ = nI, psi_nJ_ = nJ;
+  psi_tiles_.alloc(std::max<long long>(1, off));
+  psi_toff_.upload(toff), psi_tbytes_.upload(bytes), psi_dnI_.upload(nI), psi_dnJ_.upload(nJ);
+  if (!desc.empty()) {
+    DBuf<int4> d;
+    d.upload(desc);
+    psi_tiles_kernel<<<(unsigned)desc.size(), 256, 0, st_>>>(Psi.p, d_psioff.p, d.p, psi_toff_.p, nr_d.p, nc_d.p, NT,
+                                                             psi_tiles_.p);
+    SGW_LAUNCHED();
+    SGW_CUDA(cudaStreamSynchronize(st_));
+  }
+  rp_.plan(base, nI, nJ, fused_grid_);
+}
 
 void GpuSolver::setup_fused_pcg() {
   tphase_.alloc(8), tphase_.zero(st_);
@@ -617,26 +706,20 @@ void GpuSolver::setup_fused_pcg() {
     use_fused_ = false;
     return;
   }
-  // S-space local gather map (padded like Sp): global flat interface index or -1
-  std::vector<int> smap(Sp.xlen, -1);
-  for (int s = 0; s < NS; ++s) {
-    const auto& sd = G.sub[s];
-    for (int j = 0; j < NT; ++j)
-      for (int p = 0; p < ng_[s]; ++p) smap[Sp.xoff[s] + (long long)j * ng_[s] + p] = j * G.n_iface + sd.iface_pos[p];
-  }
-  smap_.upload(smap);
   int dev = 0, sms = 0, nb = 0, smem_sm = 0, smem_blk = 0;
   SGW_CUDA(cudaGetDevice(&dev));
   SGW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SGW_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   SGW_CUDA(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   // shared memory per CTA: the tile ring, the local input vector and the
-  // accumulator of the longest local vector.  Default two CTAs per SM (more
-  // warps for the scatter phases; measured 0.56 vs 0.64 ms per C2 iteration
-  // with one CTA and a deeper ring) if each gets >= 2 stages, else one with the
-  // deepest ring that fits.  SGW_PCG_BPS / SGW_PCG_RING tune.
+  // accumulator of the longest local vector (S_s, Q_s, or [corners | remaining
+  // dofs] of Psi_s).  Default two CTAs per SM (more warps for the scatter
+  // phases; measured 0.56 vs 0.64 ms per C2 iteration with one CTA and a
+  // deeper ring) if each gets >= 2 stages, else one with the deepest ring
+  // that fits.  SGW_PCG_BPS / SGW_PCG_RING tune.
   fused_maxlen_ = 0;
-  for (int s = 0; s < NS; ++s) fused_maxlen_ = std::max({fused_maxlen_, kTile * Sp.ntile[s], kTile * Qp.ntile[s]});
+  for (int s = 0; s < NS; ++s)
+    fused_maxlen_ = std::max({fused_maxlen_, kTile * Sp.ntile[s], kTile * (Qp.ntile[s] + cdiv(NT * nc_[s], kTile))});
   cudaFuncAttributes fa{};
   SGW_CUDA(cudaFuncGetAttributes(&fa, (const void*)pcg_fused_kernel));
   int bps = 2;
@@ -654,14 +737,14 @@ void GpuSolver::setup_fused_pcg() {
                                 (int)fused_smem_));
   SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pcg_fused_kernel, 256, fused_smem_));
   fused_grid_ = std::max(1, std::min(nb, bps)) * sms;
-  rs_.plan(Sp, fused_grid_);
-  rq_.plan(Qp, fused_grid_);
+  rs_.plan(Sp.tile_base, Sp.ntile, {}, fused_grid_);
+  rq_.plan(Qp.tile_base, Qp.ntile, {}, fused_grid_);
+  build_psi_tiles();
   fused_part_.alloc(size_t(8) * fused_grid_);
   fused_out_.alloc(4);
   fused_hist_.alloc(P.max_iter + 8);
   for (DBuf<double>* b : {&li_z_, &li_p_, &li_xx_}) b->alloc(Sp.xlen), b->zero(st_);  // padding stays 0
   ucl_.alloc(std::max<long long>(1, coff_.back())), ucl_.zero(st_);
-  wr_.alloc(std::max<long long>(1, Qp.xlen)), wr_.zero(st_);
   const char* e = std::getenv("SGW_PCG");
   use_fused_ = !(e && std::string(e) == "host");
 }
@@ -670,32 +753,26 @@ int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vecto
   cudaEventRecord(ev_[0], st_);
   FusedPcg A{};
   A.NG = NG;
-  A.ncol_total = coff_.back();
   A.n_iface = G.n_iface, A.NT = NT, A.NS = NS, A.n_corner = G.n_corner, A.NC = NC;
   A.max_iter = P.max_iter, A.hist_cap = (int)fused_hist_.n, A.tol = P.tol;
   A.b = b, A.x = x, A.r = vr.p, A.z = vz.p, A.p = vp.p, A.q = vq.p;
-  A.s_desc = Sp.desc.p, A.s_tiles = Sp.tiles.p, A.s_ntiles = Sp.n_tiles, A.s_row = Sp.rowpart.p,
-  A.s_col = Sp.colpart.p, A.s_base = Sp.d_tile_base.p, A.s_xoff = Sp.d_xoff.p, A.s_nt = Sp.d_ntile.p,
-  A.smap = smap_.p;
-  A.q_desc = Qp.desc.p, A.q_tiles = Qp.tiles.p, A.q_ntiles = Qp.n_tiles, A.q_row = Qp.rowpart.p,
-  A.q_col = Qp.colpart.p, A.q_base = Qp.d_tile_base.p, A.q_xoff = Qp.d_xoff.p, A.q_nt = Qp.d_ntile.p;
+  A.s_xoff = Sp.d_xoff.p, A.q_xoff = Qp.d_xoff.p;
   A.fr = r_x.p, A.fc = c_f.p;
   A.inv_cnt = inv_cnt.p, A.inv_s = inv_s.p, A.inv_p = inv_p.p, A.ip_off = ip_off.p, A.ng = ng_d.p, A.nr = nr_d.p,
-  A.nc = nc_d.p, A.pkind = pkind_.p, A.cpos_flat = cpos_flat_.p, A.cp_off = cp_off_.p, A.iface_w = iface_w.p;
+  A.nc = nc_d.p, A.pkind = pkind_.p, A.iface_w = iface_w.p;
   A.cinv_cnt = cinv_cnt.p, A.cinv_s = cinv_s.p, A.cinv_c = cinv_c.p;
-  A.roff = d_roff.p, A.coff = d_coff.p, A.psioff = d_psioff.p;
-  A.Psi = Psi.p, A.Finv = Finv.p, A.dsub = c_d.p, A.dco = dcoarse.p, A.uco = ucoarse.p;
+  A.roff = d_roff.p, A.coff = d_coff.p;
+  A.Finv = Finv.p, A.dco = dcoarse.p, A.uco = ucoarse.p, A.ucl = ucl_.p;
   A.part = fused_part_.p, A.out = fused_out_.p, A.hist = fused_hist_.p;
-  A.s_tx = Sp.tx.p, A.q_tx = Qp.tx.p;
   A.li_z = li_z_.p, A.li_p = li_p_.p, A.li_x = li_xx_.p;
   A.tphase = KP.on ? tphase_.p : nullptr;
-  A.ucl = ucl_.p, A.wr = wr_.p, A.rlen = Qp.xlen;
-  A.rs = RangePack{Sp.tiles.p, Sp.d_ntile.p, Sp.d_xoff.p, rs_.t_first.p, rs_.start.p, rs_.c0.p, rs_.ncta.p, rs_.pbase.p, rs_.part.p};
-  A.rq = RangePack{Qp.tiles.p, Qp.d_ntile.p, Qp.d_xoff.p, rq_.t_first.p, rq_.start.p, rq_.c0.p, rq_.ncta.p, rq_.pbase.p, rq_.part.p};
+  A.rs = RangePack{Sp.tiles.p, nullptr, nullptr, Sp.d_ntile.p, nullptr, 0, rs_.t_first.p, rs_.start.p, rs_.c0.p,
+                   rs_.ncta.p, rs_.pbase.p, rs_.part.p};
+  A.rq = RangePack{Qp.tiles.p, nullptr, nullptr, Qp.d_ntile.p, nullptr, 0, rq_.t_first.p, rq_.start.p, rq_.c0.p,
+                   rq_.ncta.p, rq_.pbase.p, rq_.part.p};
+  A.rp = RangePack{psi_tiles_.p, psi_toff_.p, psi_tbytes_.p, psi_dnI_.p, psi_dnJ_.p, 1, rp_.t_first.p, rp_.start.p,
+                   rp_.c0.p, rp_.ncta.p, rp_.pbase.p, rp_.part.p};
   A.nst = fused_nst_, A.maxlen = fused_maxlen_;
-  A.l2pf = 0, A.psi_late = 1;
-  if (const char* e = std::getenv("SGW_PCG_PSI_LATE")) A.psi_late = std::atoi(e);  // tuning hook
-  if (const char* e = std::getenv("SGW_PCG_L2PF")) A.l2pf = std::max(0, std::atoi(e));  // tuning hook
   void* args[] = {&A};
   SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_fused_kernel, dim3(fused_grid_), dim3(256), args,
                                        fused_smem_, st_));

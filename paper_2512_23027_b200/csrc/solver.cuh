@@ -114,7 +114,7 @@ struct RangeBufs {
   DBuf<int4> start;
   DBuf<int> c0, ncta;
   DBuf<double> part;
-  void plan(const TilePack& tp, int grid);
+  void plan(const std::vector<long long>& tile_base, const std::vector<int>& nI, const std::vector<int>& nJ, int grid);
 };
 
 // G tensor lists by output term k: entries (i, j, g) in for_each order.
@@ -317,10 +317,16 @@ class GpuSolver {
   void setup_fused_pcg();
   int pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist);
   DBuf<int> smap_, fused_out_;
-  RangeBufs rs_, rq_;
+  RangeBufs rs_, rq_, rp_;
+  // Psi_s^T as rectangular tiles for the persistent kernel (pcg_fused.cu)
+  DBuf<double> psi_tiles_;
+  DBuf<long long> psi_toff_;
+  DBuf<int> psi_tbytes_, psi_dnI_, psi_dnJ_;
+  std::vector<int> psi_nI_, psi_nJ_;
+  void build_psi_tiles();
   int fused_nst_ = 3, fused_maxlen_ = 0;
   size_t fused_smem_ = 0;
-  DBuf<double> fused_part_, fused_hist_, li_z_, li_p_, li_xx_, ucl_, wr_;
+  DBuf<double> fused_part_, fused_hist_, li_z_, li_p_, li_xx_, ucl_;
  public:
   DBuf<double> tphase_;  // per-phase ns of the persistent PCG kernel (profiling)
  private:

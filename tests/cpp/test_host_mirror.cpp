@@ -19,7 +19,7 @@ const char* orc_last_error();
 int orc_lognormal_coeff(int, int, double, double, double, double, int, int, double*, int, int*);
 int orc_triple_products(int, int, int, int, int*, int*, int*, int*, int*, int*, double*);
 int orc_solver_create(int, int, int, int, int, const double*, int, int, const int*, const int*, const int*,
-                      const double*, double, double, double, double, double, double, double, int, int, void**);
+                      const double*, double, double, double, double, double, double, double, int, int, int, void**);
 void orc_solver_destroy(void*);
 void orc_solver_sizes(void*, long long*);
 int orc_apply_block(void*, int, const double*, double*);
@@ -136,7 +136,7 @@ static void gpu_tests() {
   void* oh = nullptr;
   CHECK(orc_solver_create(c.nx, c.nx, c.px, c.px, t.n_input, flat.data(), t.n_output, (int)ev.size(), ei.data(),
                           ej.data(), ek.data(), ev.data(), 1.0, 0.5445, 0.0174, 0.5, 0.25, c.dt, 1e-10, 500, 2,
-                          &oh) == 0);
+                          /*precond nn2*/ 0, &oh) == 0);
   long long sz[6];
   orc_solver_sizes(oh, sz);
   CHECK(sz[1] == s.n_terms() && sz[0] == s.n_dofs() && sz[4] == s.schur().n_global());
