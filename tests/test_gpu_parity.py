@@ -95,6 +95,29 @@ def test_pcg_drivers_agree_with_oracle(gpu, monkeypatch, mode):
     assert np.linalg.norm(c.schur_matvec(x) - b) / np.linalg.norm(b) <= 1e-10
 
 
+@pytest.mark.parametrize("cfg", [(18, 3, 3, 1, 2, 2), (30, 5, 4, 1, 4, 4), (40, 4, 4, 3, 2, 3)])
+def test_fused_pcg_odd_term_counts(gpu, cfg):
+    # odd P+1 (3, 5): odd r_s / c_s / n_C in the persistent kernel's Psi tiles
+    # (column chunks of < 64, rows past r_s), the F_cc^-1 rows' 16-byte
+    # alignment, and ranges that split subdomains across CTAs; 3x3 / 5x4
+    # partitions with cross points; (40, 4x4, P+1 = 10) has full 64-wide chunks
+    nx, px, py, L, pin, pout = cfg
+    g, c = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 1e-3)
+    assert c.n_corner > 0
+    x = rand(g.n_global, 5)
+    assert relerr(g.schur().apply_nn2(x), c.apply_nn2(x)) <= 1e-10
+    b = c.schur_matvec(rand(g.n_global, 6))
+    xg, rep = g.pcg(b)
+    assert rep["converged"]
+    assert np.linalg.norm(c.schur_matvec(xg) - b) / np.linalg.norm(b) <= 1e-10
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 8, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 8, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
 def test_c1_trajectory_parity(gpu):
     # BASELINE configs[0] (C1): 64x64, 4x4, L=2, p_in 4, p_out 2, sigma 0.3, b 0.5,
     # dt 1e-3, 50 steps, tol 1e-10, Ricker f0 = 10 Hz at (0.5, 0.5)
