@@ -85,6 +85,13 @@ typedef struct sgw_problem {
    * flattened A_GG block as DetSolver's K~_GG, det_loop.cpp:165-167).
    * DetSolver::set_preconditioner / SolveOptions::precond (det_loop.hpp:14). */
   int precond;
+  /* Reduced-memory mode: 1 = the local Schur complements S_s
+   * are not stored; every S product applies A_GG - A_GI A_II^-1 A_IG per
+   * subdomain through the local stencils and one batched interior solve
+   * (sg.cpp:227-245 formed on the fly).  NN2 keeps its explicit S_rr^-1,
+   * Psi and F_cc^-1.  Saves the S tiles (1.3 GB at C2, 18 GB at C3) at the
+   * cost of one interior sweep per PCG iteration.                          */
+  int implicit_schur;
 } sgw_problem;
 
 /* ForceFn (det_loop.hpp:32): kind 0 none; 1 Ricker wavelet

@@ -46,6 +46,7 @@ inline PrecondKind precond_from_string(const std::string& name) {  // dd.hpp:100
 
 struct SgOptions {  // sg.hpp:13-19 (threads: accepted, unused on the GPU) + SolveOptions::precond
   PrecondKind precond = PrecondKind::nn2;
+  bool implicit_schur = false;  // reduced-memory mode (include/sgw.h)
   double tol = 1e-8;
   int max_iter = 500;
   int threads = 1;
@@ -200,6 +201,7 @@ class SgSolver {  // sg.hpp:43-98
     pr.gamma = params.gamma, pr.zeta = params.zeta, pr.dt = params.dt;
     pr.tol = opt_.tol, pr.max_iter = opt_.max_iter, pr.device = opt_.device;
     pr.rank = 0, pr.world_size = 1, pr.nccl_id = nullptr, pr.precond = precond_code(opt_.precond);
+    pr.implicit_schur = opt_.implicit_schur ? 1 : 0;
     if (pr.n_input != tensor.n_input)
       throw std::invalid_argument("SgSolver: coefficient terms do not match tensor input size");
     detail::check(sgw_create(&pr, &h_));

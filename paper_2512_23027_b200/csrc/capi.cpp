@@ -91,6 +91,7 @@ Problem problem_from(const sgw_problem* p) {
     P.device = p->device, P.rank = p->rank, P.world = p->world_size < 1 ? 1 : p->world_size;
     if (p->precond < 0 || p->precond > 2) throw Error(SGW_EINVAL, "unknown preconditioner");  // precond_from_string
     P.precond = p->precond;
+    P.implicit_schur = p->implicit_schur != 0;
     if (P.rank < 0 || P.rank >= P.world) throw Error(SGW_EINVAL, "rank out of range");
     if (P.world > P.px * P.py) throw Error(SGW_EINVAL, "more ranks than subdomains");
     return P;

@@ -22,6 +22,7 @@ struct Problem {
   double density = 1, alpha0 = 0, alpha1 = 0, gamma = 0.5, zeta = 0.25, dt = 0, tol = 1e-8;
   int max_iter = 500, device = 0, rank = 0, world = 1;
   int precond = 0;  // PrecondKind (dd.hpp:98): 0 nn2 (the SG path, sg.cpp:330), 1 nn1, 2 lumped
+  int implicit_schur = 0;  // reduced-memory mode: S_s applied through the interior solve, not stored
   double mass_scale = 0, stiff_scale = 0;  // src/sg.cpp:147-148
   int n_nodes() const { return (nx + 1) * (ny + 1); }
 };

@@ -94,7 +94,7 @@ __global__ void residual_kernel(double* __restrict__ rt, const double* __restric
 }
 
 // ------------------------------------------------------------- TilePack ----
-void TilePack::plan(const std::vector<int>& dims) {
+void TilePack::plan(const std::vector<int>& dims, bool alloc_tiles) {
   nmat = int(dims.size());
   dim = dims;
   ntile.resize(nmat);
@@ -118,9 +118,11 @@ void TilePack::plan(const std::vector<int>& dims) {
   n_tiles = tile_base[nmat];
   xlen = xoff[nmat];
   desc.upload(h);
-  tiles.alloc(size_t(n_tiles) * kTile * kTile);
-  rowpart.alloc(size_t(n_tiles) * kTile);
-  colpart.alloc(size_t(n_tiles) * kTile);
+  if (alloc_tiles) {
+    tiles.alloc(size_t(n_tiles) * kTile * kTile);
+    rowpart.alloc(size_t(n_tiles) * kTile);
+    colpart.alloc(size_t(n_tiles) * kTile);
+  }
   d_tile_base.upload(tile_base);
   d_xoff.upload(xoff);
   d_ntile.upload(ntile);
@@ -256,6 +258,7 @@ void GpuSolver::scatter_li(const double* li, double* glob, bool weighted, double
 
 // --------------------------------------------------------------- matvec ----
 void GpuSolver::schur_matvec(const double* x, double* y) {
+  if (P.implicit_schur) return schur_matvec_implicit(x, y);
   gather_li(x, li_x.p, false);
   symv(Sp, li_x.p, nullptr);
   const int grid = red_grid(NG);
@@ -436,7 +439,7 @@ double GpuSolver::dot_host(const double* a, const double* b, long long len) {
 // src/pcg.cpp:7-50: x0 = 0; stop on the recurrence residual, confirm with the
 // true residual, restart from it (without resetting p) if the check fails.
 int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
-  if (use_fused_ && !comm_ && P.precond == 0) return pcg_fused(b, x, converged, hist);
+  if (use_fused_ && !comm_ && P.precond == 0 && !P.implicit_schur) return pcg_fused(b, x, converged, hist);
   cudaEventRecord(ev_[0], st_);
   const long long N = NG;
   const int grid = red_grid(N);
@@ -469,6 +472,11 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
   // launches per iteration instead of ~15 kernels and 3 collectives.
   const bool graphs = !comm_ || comm_->capturable();
   auto matvec_half = [&]() {
+    if (P.implicit_schur) {
+      schur_matvec_implicit(vp.p, vq.p);  // sum over ranks included
+      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      SGW_LAUNCHED();
+    } else {
     gather_li(vp.p, li_x.p, false);
     symv(Sp, li_x.p, nullptr);
     scatter_kernel<true><<<grid, 256, 0, st_>>>(vq.p, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
@@ -476,7 +484,8 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
                                                 Sp.d_tile_base.p, Sp.d_ntile.p, comm_ ? nullptr : vp.p, dpart.p,
                                                 dcount.p, scal.p + PQ);
     SGW_LAUNCHED();
-    if (comm_) {
+    }
+    if (comm_ && !P.implicit_schur) {
       allreduce(vq.p, NG);
       dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();
@@ -546,6 +555,11 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
       continue;
     }
     // q = S p with p.q fused into the scatter
+    if (P.implicit_schur) {
+      schur_matvec_implicit(vp.p, vq.p);
+      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      SGW_LAUNCHED();
+    } else {
     gather_li(vp.p, li_x.p, false);
     symv(Sp, li_x.p, nullptr);
     scatter_kernel<true><<<grid, 256, 0, st_>>>(vq.p, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
@@ -553,7 +567,8 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
                                                 Sp.d_tile_base.p, Sp.d_ntile.p, comm_ ? nullptr : vp.p, dpart.p,
                                                 dcount.p, scal.p + PQ);
     SGW_LAUNCHED();
-    if (comm_) {  // sharded: q is complete only after the sum over ranks
+    }
+    if (comm_ && !P.implicit_schur) {  // sharded: q is complete only after the sum over ranks
       allreduce(vq.p, NG);
       dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();

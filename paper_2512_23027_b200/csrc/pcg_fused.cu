@@ -702,7 +702,7 @@ void GpuSolver::build_psi_tiles() {
 
 void GpuSolver::setup_fused_pcg() {
   tphase_.alloc(8), tphase_.zero(st_);
-  if (comm_) {  // sharded: the host-driven loop with a sum over ranks after each scatter
+  if (comm_ || P.implicit_schur) {  // sharded / reduced-memory: the host-driven loop
     use_fused_ = false;
     return;
   }

@@ -619,7 +619,7 @@ void GpuSolver::plan_nn2() {
   const int ns = NS, nt = NT;
   std::vector<int> dimsS(ns), dimsQ(ns);
   for (int s = 0; s < ns; ++s) dimsS[s] = nt * ng_[s], dimsQ[s] = nt * nr_[s];
-  Sp.plan(dimsS);
+  Sp.plan(dimsS, !P.implicit_schur);  // reduced-memory mode: layout only, no S tiles
   Qp.plan(dimsQ);
   if (P.precond == 1) Sinvp.plan(dimsS);
   if (P.precond == 2) Aggp.plan(dimsS);
@@ -656,7 +656,8 @@ void GpuSolver::plan_nn2() {
 // subdomain extract, invert, Psi, local coarse block (accumulated into fcc).
 void GpuSolver::nn2_batch(int b0, int nb, std::vector<double>& fcc) {
   const int nt = NT, amax = amax_;
-  for (int q = 0; q < nb; ++q) pack_tiles_range(Sp, b0 + q, Sdense_.p + size_t(q) * amax * amax, amax, st_);
+  if (!P.implicit_schur)
+    for (int q = 0; q < nb; ++q) pack_tiles_range(Sp, b0 + q, Sdense_.p + size_t(q) * amax * amax, amax, st_);
   DBuf<double> Srr, Src, Scc, work;
   DBuf<int> ri, ci, info;
   info.alloc(1);

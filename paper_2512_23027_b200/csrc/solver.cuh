@@ -103,7 +103,7 @@ struct TilePack {
   DBuf<double> tiles, rowpart, colpart;
   DBuf<long long> d_tile_base, d_xoff;
   DBuf<int> d_ntile, d_dim;
-  void plan(const std::vector<int>& dims);
+  void plan(const std::vector<int>& dims, bool alloc_tiles = true);
   long long bytes() const { return n_tiles * kTile * kTile * 8; }
 };
 
@@ -191,6 +191,9 @@ class GpuSolver {
   // reference-facing operations (device buffers in/out)
   void apply_block(int op, const double* x, double* y);                 // K11
   void schur_matvec(const double* x, double* y);                        // K1
+  // S x without stored S tiles (Problem::implicit_schur): per subdomain
+  // A_GG x - A_GI A_II^-1 A_IG x through the local stencils and one interior sweep
+  void schur_matvec_implicit(const double* x, double* y);
   void apply_nn2(const double* r, double* z);                           // K2-K4
   // make_preconditioner(schur, kind) (dd.cpp:159-253): 0 nn2, 1 nn1, 2 lumped
   // (nn1 / lumped need Problem::precond == kind: their local operators are

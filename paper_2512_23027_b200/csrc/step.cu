@@ -179,6 +179,9 @@ __global__ void local_force_kernel(LocalArgs A, int n, const double* __restrict_
 // Transient-operator product restricted to couplings between node classes.
 //  mode 0 (A_GI y):  out_LI[s][k*ng+p] = fG - sum_{interior nb} A(p,nb) y(nb)
 //  mode 1 (A_IG u):  out_I[s][..]      = sum_{interface nb} A(lid,nb) uLI(nb)
+//  mode 2 (S u):     out_LI[s][k*ng+p] = sum_{interface nb, self} A(p,nb) uLI(nb)
+//                                        - sum_{interior nb} A(p,nb) y(nb)
+//                    (y = A_II^-1 A_IG u: the implicit local Schur product)
 __global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict__ yI, const double* __restrict__ fG,
                                 const double* __restrict__ uLI, const int* __restrict__ ip_off,
                                 const int* __restrict__ iface_lid, double* __restrict__ outLI,
@@ -193,21 +196,25 @@ __global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict_
       lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
     }
     const int cls = A.lid_to_p[(long long)s * A.nl + lid];
-    if (mode == 0 ? cls < 0 : cls != -2) continue;
+    if (mode == 1 ? cls != -2 : cls < 0) continue;
     const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
     const double* Ms = A.Ml + (long long)s * 4 * A.nl;
     const double* Ks = A.Kl + (long long)s * A.nin * 3 * A.nl;
     const int ng = A.ng[s];
     double acc = 0.0;
-    for (int dir = 1; dir < 7; ++dir) {
+    for (int dir = mode == 2 ? 0 : 1; dir < 7; ++dir) {
       const int i2 = il + sDI[dir], j2 = jl + sDJ[dir];
       if (i2 < 0 || i2 > A.mx || j2 < 0 || j2 > A.my) continue;
       const int nb = j2 * (A.mx + 1) + i2;
       const int c2 = A.lid_to_p[(long long)s * A.nl + nb];
-      if (mode == 0 ? c2 != -2 : c2 < 0) continue;
-      // value of the other node for term j
+      if (mode == 0 ? c2 != -2 : mode == 1 ? c2 < 0 : c2 == -1) continue;
+      // value of the other node for term j (mode 2: interface u, interior -y)
       auto val = [&](int j) -> double {
-        return mode == 0 ? yI[interior_index(A, s, i2, j2, j)] : uLI[A.lioff[s] + (long long)j * ng + c2];
+        if (mode == 0 || (mode == 2 && c2 == -2)) {
+          const double y = yI[interior_index(A, s, i2, j2, j)];
+          return mode == 0 ? y : -y;
+        }
+        return uLI[A.lioff[s] + (long long)j * ng + c2];
       };
       acc += A.ms * mco(Ms, A.nl, lid, nb, dir) * val(k);
       if (dir < 5)
@@ -217,6 +224,8 @@ __global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict_
     if (mode == 0) {
       const long long o = A.lioff[s] + (long long)k * ng + cls;
       outLI[o] = fG[o] - acc;
+    } else if (mode == 2) {
+      outLI[A.lioff[s] + (long long)k * ng + cls] = acc;
     } else {
       outI[interior_index(A, s, il, jl, k)] = acc;
     }
@@ -340,6 +349,28 @@ void GpuSolver::mass_solve(double* x, const double* b) {
     SGW_LAUNCHED();
     rr = rr2;
   }
+}
+
+// Reduced-memory Schur product: y = sum_s R_s^T (A_GG,s -
+// A_GI,s A_II,s^-1 A_IG,s) R_s x with the subdomains' local stencils and one
+// batched interior sweep, instead of the stored dense S_s (dd.cpp:142-157 on
+// the S of sg.cpp:227-245).  Scratch: li_x (x local), wI (interior), li_y.
+void GpuSolver::schur_matvec_implicit(const double* x, double* y) {
+  const LocalArgs A = local_args();
+  const long long ti = (long long)n_ilist_ * NT, ta = (long long)n_alist_ * NT;
+  gather_li(x, li_x.p, false);
+  SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
+  if (n_alist_ > 0) {
+    coupling_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
+        A, 1, nullptr, nullptr, li_x.p, ip_off.p, iface_lid_.p, nullptr, wI.p, NS, alist_.p, n_alist_);
+    SGW_LAUNCHED();
+  }
+  sweep(wI.p);  // A_II^-1 A_IG x
+  coupling_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+      A, 2, wI.p, nullptr, li_x.p, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
+  SGW_LAUNCHED();
+  scatter_li(li_y.p, y, false, nullptr, nullptr);
+  allreduce(y, NG);
 }
 
 // ---------------------------------------------------------------- driver ---

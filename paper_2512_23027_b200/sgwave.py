@@ -47,7 +47,8 @@ class _Problem(C.Structure):
                 ("density", C.c_double), ("alpha0", C.c_double), ("alpha1", C.c_double),
                 ("gamma", C.c_double), ("zeta", C.c_double), ("dt", C.c_double),
                 ("tol", C.c_double), ("max_iter", C.c_int), ("device", C.c_int),
-                ("rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p), ("precond", C.c_int)]
+                ("rank", C.c_int), ("world_size", C.c_int), ("nccl_id", C.c_void_p), ("precond", C.c_int),
+                ("implicit_schur", C.c_int)]
 
 
 class _Force(C.Structure):
@@ -199,6 +200,7 @@ class NewmarkParams:  # include/sgwave/newmark.hpp:11-19
 @dataclass
 class SgOptions:  # include/sgwave/sg.hpp:15-21 (+ SolveOptions::precond, det_loop.hpp:14)
     precond: str = "nn2"  # PrecondKind: "nn2" (the SG path, sg.cpp:330), "nn1", "lumped"
+    implicit_schur: bool = False  # reduced-memory mode: S_s applied through the interior solve (include/sgw.h)
     tol: float = 1e-8
     max_iter: int = 500
     store_full: bool = False
@@ -418,7 +420,8 @@ class SgSolver:
         prob = _Problem(nx, ny, px, py, self._coeff.shape[0], _p(self._coeff), int(tensor.n_output), len(tv),
                         _p(ti), _p(tj), _p(tk), _p(tv), density, alpha0, alpha1, self.params.gamma,
                         self.params.zeta, self.params.dt, self.options.tol, self.options.max_iter,
-                        self.options.device, rank, world_size, None, precond_from_string(self.options.precond))
+                        self.options.device, rank, world_size, None, precond_from_string(self.options.precond),
+                        int(self.options.implicit_schur))
         if self._coeff.shape[0] != tensor.n_input:
             raise SgInvalidArgument(SGW_EINVAL, "SgSolver: coefficient terms do not match tensor input size")
         self.rank, self.world_size = rank, world_size

@@ -372,3 +372,28 @@ def test_c2_full_size_parity_and_properties(gpu):
     hc = cpu.run(z, z, 3, force_node=node, f0=bench.F0, t0=bench.T0, store_full=True)
     assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-8
+
+
+@pytest.mark.parametrize("cfg", [(16, 4, 2, 2, 4, 2), (22, 4, 3, 2, 2, 2)])
+def test_reduced_memory_mode_matches_oracle(gpu, cfg):
+    # S_s not stored, applied as A_GG - A_GI A_II^-1 A_IG through
+    # the local stencils and the interior sweep (include/sgw.h implicit_schur)
+    nx, px, py, L, pin, pout = cfg
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, L, pin)
+    t = O.triple_products(L, pin, pout)
+    mk = lambda imp: sg.SgSolver(nx, nx, px, py, coeff, t, params=sg.NewmarkParams(dt=1e-3),  # noqa: E731
+                                 options=sg.SgOptions(tol=1e-10, store_full=True, implicit_schur=imp))
+    g, e = mk(True), mk(False)
+    c = O.SgSolver(nx, nx, px, py, coeff, t, dt=1e-3, tol=1e-10)
+    assert g.device_bytes < e.device_bytes
+    x = rand(c.n_global, 4)
+    assert relerr(g.schur().matvec(x), c.schur_matvec(x)) <= 1e-10
+    b = c.schur_matvec(rand(c.n_global, 8))
+    xg, rep = g.pcg(b)
+    assert rep["converged"] and np.linalg.norm(c.schur_matvec(xg) - b) / np.linalg.norm(b) <= 1e-10
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 8, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 8, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
