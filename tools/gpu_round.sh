@@ -22,3 +22,9 @@ timeout 600 python tools/sgop_bench.py C2 5 > gpurun_out/sgop_plain.log 2>&1 && 
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgop_kernel -s 2 -c 1 \
     -o gpurun_out/prof_sgop python tools/sgop_bench.py C2 5 > gpurun_out/ncu_sgop.log 2>&1
 echo "rc=$?" >> gpurun_out/plain.log
+timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3.log 2> gpurun_out/bench_C3.err
+echo "C3 rc=$?" >> gpurun_out/bench_C3.err
+timeout 600 python bench.py --config C1 > gpurun_out/bench_C1.log 2> gpurun_out/bench_C1.err
+echo "C1 rc=$?" >> gpurun_out/bench_C1.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err
+echo "ref rc=$?" >> gpurun_out/bench_ref.err
