@@ -33,6 +33,12 @@ CONFIGS = {  # BASELINE.json configs
     "C1": dict(nx=64, px=4, L=2, p_in=4, p_out=2, sigma=0.3, b=0.5, dt=1e-3),
     "C2": dict(nx=256, px=8, L=3, p_in=6, p_out=3, sigma=0.3, b=0.5, dt=1e-3),
     "C3": dict(nx=512, px=16, L=4, p_in=6, p_out=3, sigma=0.4, b=0.3, dt=1e-3),
+    # configs[3]: ~224 GB in the explicit formulation -> sharded over >= 2 GPUs (--gpus N)
+    "C4": dict(nx=1024, px=32, L=6, p_in=4, p_out=2, sigma=0.3, b=0.5, dt=1e-3),
+    # configs[4], the random-dimension sweep at p_in = 4; L = 12, 16 need >= 4 GPUs
+    "C5L2": dict(nx=512, px=16, L=2, p_in=4, p_out=2, sigma=0.3, b=0.5, dt=1e-3),
+    "C5L4": dict(nx=512, px=16, L=4, p_in=4, p_out=2, sigma=0.3, b=0.5, dt=1e-3),
+    "C5L8": dict(nx=512, px=16, L=8, p_in=4, p_out=2, sigma=0.3, b=0.5, dt=1e-3),
 }
 ALPHA0, ALPHA1, TOL, F0, T0 = 0.5445, 0.0174, 1e-10, 10.0, 0.1
 

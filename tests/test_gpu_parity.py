@@ -118,6 +118,24 @@ def test_fused_pcg_odd_term_counts(gpu, cfg):
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
 
 
+def test_c5_l8_basis_small_mesh(gpu):
+    # the C5 L = 8 basis (P+1 = 45, p_in = 4: 495 input terms) on a small mesh:
+    # the JIT operator at 5 threads per node, odd P+1 everywhere in the PCG
+    nx = 12
+    g, c = pair(nx, 2, 2, 0.3, 0.5, 8, 4, 2, 1e-3)
+    assert g.n_terms == 45
+    x = rand(g.n_terms * g.n_dofs, 2)
+    assert relerr(g.apply_block_transient(x), c.apply_block(x, "transient")) <= 1e-12
+    r = rand(g.n_global, 3)
+    assert relerr(g.schur().apply_nn2(r), c.apply_nn2(r)) <= 1e-10
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 4, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 4, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
 def test_c1_trajectory_parity(gpu):
     # BASELINE configs[0] (C1): 64x64, 4x4, L=2, p_in 4, p_out 2, sigma 0.3, b 0.5,
     # dt 1e-3, 50 steps, tol 1e-10, Ricker f0 = 10 Hz at (0.5, 0.5)
