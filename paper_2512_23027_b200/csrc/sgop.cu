@@ -223,7 +223,7 @@ __device__ __forceinline__ void producer(const SgOpArgs& A, int mytiles, int nst
 
 @GROUPS@
 
-extern "C" __global__ void __launch_bounds__(NTHR, 1) sgop_kernel(const SgOpArgs A) {
+extern "C" __global__ void __launch_bounds__(NTHR, CPS) sgop_kernel(const SgOpArgs A) {
   const int ntiles = A.tiles_x * A.tiles_y * A.items;
   if ((int)blockIdx.x >= ntiles) return;
   const int mytiles = (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1;
@@ -270,6 +270,7 @@ std::string dlit(double v) {
 
 struct SgOpJit {
   int NT = 0, NIN = 0, R = 4, G = 2, IC = 4, S = 6, NCHUNK = 0, regs = 255, prod = 0, la = 0;
+  int cps = 1;  // CTAs per SM (shared memory and registers split between them)
   bool red_alias = true;  // partial sums reuse the tile's x buffer (after the mass step)
   bool jouter = false;    // k-resident code shape (see sgop_source)
   bool xg = true;         // x and M read from global memory (no packed x tiles, K-only ring)
@@ -295,6 +296,7 @@ static long long sgop_smem_doubles(const SgOpJit& J) {
 // CUDA source of the operator specialised for (NT, NIN, T); fills J's shape.
 std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   J->NT = NT, J->NIN = NIN;
+  if (const char* e = std::getenv("SGW_SGOP_CPS")) J->cps = std::max(1, std::min(4, std::atoi(e)));  // tuning hook
   // <= 7 input terms (35 neighbourhood values) per thread; threads per CTA
   // bounded by the register file (estimate: x and y live values + 40) and
   // the shared memory by the tile height R
@@ -323,12 +325,12 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   const int jg = (NT + GJ - 1) / GJ;
   const int est = J->jouter ? 2 * (5 * J->IC + NT + 5) + 60 : 2 * (5 * jg + NT) + 80;
   J->NCHUNK = (NIN + J->IC - 1) / J->IC;
-  J->R = std::max(1, std::min(16, 65536 / est / (32 * J->G)));
+  J->R = std::max(1, std::min(16, 65536 / J->cps / est / (32 * J->G)));
   if (const char* e = std::getenv("SGW_SGOP_PROD")) J->prod = std::atoi(e) != 0;  // tuning hook: producer warp
   if (const char* e = std::getenv("SGW_SGOP_LA")) J->la = std::atoi(e) != 0;      // tuning hook: last-arriver refill
   if (J->prod) J->la = 0;
   if (const char* e = std::getenv("SGW_SGOP_R")) J->R = std::max(1, std::atoi(e));  // tuning hook
-  const long long budget = 220 * 1024 / 8;
+  const long long budget = 220 * 1024 / 8 / J->cps;
   if (const char* e = std::getenv("SGW_SGOP_XG")) J->xg = std::atoi(e) != 0;  // tuning hook
   if (J->jouter) J->xg = false;
   for (;; --J->R) {
@@ -345,7 +347,7 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   }
   if (const char* e = std::getenv("SGW_SGOP_S")) J->S = std::max(3, std::atoi(e));  // tuning hook
   // registers are split per SM sub-partition: the warp count per partition sets the cap
-  J->regs = std::min(255, 16384 / (32 * ((J->R * J->G + J->prod + 3) / 4)) & ~7);
+  J->regs = std::min(255, 16384 / (32 * J->cps * ((J->R * J->G + J->prod + 3) / 4)) & ~7);
   const int R = J->R, G = J->G, IC = J->IC;
   // full (i, j) -> [(k, c)] expansion of the j <= k tensor (pce.hpp:24-40)
   std::map<std::pair<int, int>, std::vector<std::pair<int, double>>> pairs;
@@ -593,7 +595,7 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   if (const char* e = std::getenv("SGW_SGOP_PF")) pf = std::max(0, std::atoi(e));  // tuning hook
   int ef = 1;
   if (const char* e = std::getenv("SGW_SGOP_EF")) ef = std::atoi(e);  // tuning hook
-  std::string src = "#define EF " + std::to_string(ef) + "\n#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
+  std::string src = "#define CPS " + std::to_string(J->cps) + "\n#define EF " + std::to_string(ef) + "\n#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
                     "\n#define NT " + std::to_string(NT) + "\n#define NIN " + std::to_string(NIN) +
                     "\n#define R " + std::to_string(R) + "\n#define G " + std::to_string(G) + "\n#define IC " +
                     std::to_string(IC) + "\n#define S " + std::to_string(J->S) + "\n#define NCHUNK " +
@@ -723,7 +725,7 @@ void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st) {
         xbuf);
     SGW_LAUNCHED();
   }
-  const int grid = std::max(1, std::min(tiles, kNumSMs));
+  const int grid = std::max(1, std::min(tiles, J.cps * kNumSMs));
   void* args[] = {const_cast<SgOpArgs*>(&a)};
   SGW_CUDA(cudaLaunchKernel((const void*)J.kern, dim3(grid), dim3(32 * (J.R * J.G + J.prod)), args, J.smem, st));
   SGW_LAUNCHED();
