@@ -93,6 +93,41 @@ __global__ void residual_kernel(double* __restrict__ rt, const double* __restric
   finalize_sum(s, partials, counter, scal + RT, nullptr);
 }
 
+// (I (x) M) x = b by CG (initial acceleration, src/sg.cpp:370-376).  M is
+// SPD with kappa < 10, so CG reaches 1e-16 relative in a few dozen
+// iterations.  The scalars stay on the device (the interface CG's kernels with
+// z = r); the host reads r.r every 4 iterations only.
+void GpuSolver::mass_solve(double* x, const double* b) {
+  const long long N = (long long)NSTATE;
+  if (mass_w_.n != 3 * (size_t)N) mass_w_.alloc(3 * (size_t)N);
+  double *r = mass_w_.p, *p = mass_w_.p + N, *q = mass_w_.p + 2 * N;
+  SGW_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st_));
+  SGW_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  SGW_CUDA(cudaMemcpyAsync(p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  const double bb = dot_host(b, b, N);
+  if (bb == 0.0) return;
+  const int grid = red_grid(N);
+  dot_kernel<<<grid, 256, 0, st_>>>(r, r, N, dpart.p, dcount.p, scal.p + RZN, nullptr);  // rz = r.r
+  SGW_LAUNCHED();
+  for (int it = 0; it < 500;) {
+    for (int u = 0; u < 4; ++u, ++it) {
+      apply_block(0, p, q);
+      dot_kernel<<<grid, 256, 0, st_>>>(p, q, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      SGW_LAUNCHED();
+      cg_xr_kernel<<<grid, 256, 0, st_>>>(x, r, p, q, N, scal.p, dpart.p, dcount.p);  // alpha = rz / pq
+      SGW_LAUNCHED();
+      dot_kernel<<<grid, 256, 0, st_>>>(r, r, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
+      SGW_LAUNCHED();
+      cg_p_kernel<<<grid, 256, 0, st_>>>(p, r, N, scal.p, 0);  // p = r + (rz_new / rz) p
+      SGW_LAUNCHED();
+    }
+    double rr = 0.0;
+    SGW_CUDA(cudaMemcpyAsync(&rr, scal.p + RZN, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    SGW_CUDA(cudaStreamSynchronize(st_));
+    if (!(rr > 1e-32 * bb)) break;
+  }
+}
+
 // ------------------------------------------------------------- TilePack ----
 void TilePack::plan(const std::vector<int>& dims, bool alloc_tiles) {
   nmat = int(dims.size());

@@ -340,6 +340,7 @@ class GpuSolver {
   DBuf<double> vb, vx, vr, vz, vp, vq, vrt;
   DBuf<double> fI, yI, wI, fG;
   DBuf<double> scal;  // device scalars
+  DBuf<double> init_w_, mass_w_;  // init_state / mass_solve work vectors (kept across runs)
   DBuf<double> dpart;
   DBuf<unsigned> dcount;
   // forcing

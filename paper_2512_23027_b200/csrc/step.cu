@@ -325,32 +325,6 @@ __global__ void init_resid_kernel(double* __restrict__ res, const double* __rest
     res[i] = res[i] - a0 * mv[i] - a1 * kv[i] - ku[i];
 }
 
-// (I (x) M) x = b by CG (initial acceleration, src/sg.cpp:370-376).  M is
-// SPD with kappa < 10, so CG reaches 1e-15 in a few dozen iterations.
-void GpuSolver::mass_solve(double* x, const double* b) {
-  const long long N = (long long)NSTATE;
-  DBuf<double> r, p, q;
-  r.alloc(N), p.alloc(N), q.alloc(N);
-  SGW_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st_));
-  SGW_CUDA(cudaMemcpyAsync(r.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
-  SGW_CUDA(cudaMemcpyAsync(p.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
-  const double bb = dot_host(b, b, N);
-  if (bb == 0.0) return;
-  double rr = bb;
-  const int grid = std::min(cdiv(N, 256), 4096);
-  for (int it = 0; it < 500 && rr > 1e-32 * bb; ++it) {
-    apply_block(0, p.p, q.p);
-    const double pq = dot_host(p.p, q.p, N);
-    const double alpha = rr / pq;
-    cg_mass_update<<<grid, 256, 0, st_>>>(x, r.p, p.p, q.p, nullptr, N, alpha);
-    SGW_LAUNCHED();
-    const double rr2 = dot_host(r.p, r.p, N);
-    axpby_kernel<<<grid, 256, 0, st_>>>(p.p, r.p, N, rr2 / rr, 1.0);
-    SGW_LAUNCHED();
-    rr = rr2;
-  }
-}
-
 // Reduced-memory Schur product: y = sum_s R_s^T (A_GG,s -
 // A_GI,s A_II,s^-1 A_IG,s) R_s x with the subdomains' local stencils and one
 // batched interior sweep, instead of the stored dense S_s (dd.cpp:142-157 on
@@ -428,12 +402,13 @@ void GpuSolver::init_state(const double* u0_nodal, const double* v0_nodal, doubl
   t_now = 0.0;
   step_index = 0;
   // resid = f0 - a0 M v - a1 K v - K u
-  DBuf<double> mv, kv, ku, res;
-  mv.alloc(NSTATE), kv.alloc(NSTATE), ku.alloc(NSTATE), res.alloc(NSTATE);
+  // work vectors kept across runs (a cudaMalloc / cudaFree per run would synchronise)
+  if (init_w_.n != 4 * NSTATE) init_w_.alloc(4 * NSTATE);
+  struct { double* p; } mv{init_w_.p}, kv{init_w_.p + NSTATE}, ku{init_w_.p + 2 * NSTATE}, res{init_w_.p + 3 * NSTATE};
   apply_block(0, v.p, mv.p);
   apply_block(1, v.p, kv.p);
   apply_block(1, u.p, ku.p);
-  res.zero(st_);
+  SGW_CUDA(cudaMemsetAsync(res.p, 0, NSTATE * sizeof(double), st_));
   double fval = 0.0;
   const double* fvec = force_at(0.0, 0, &fval);
   if (fvec)
