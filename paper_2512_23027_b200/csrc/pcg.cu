@@ -474,7 +474,7 @@ double GpuSolver::dot_host(const double* a, const double* b, long long len) {
 // src/pcg.cpp:7-50: x0 = 0; stop on the recurrence residual, confirm with the
 // true residual, restart from it (without resetting p) if the check fails.
 int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
-  if (use_fused_ && !comm_ && P.precond == 0 && !P.implicit_schur) return pcg_fused(b, x, converged, hist);
+  if (fused_ok()) return pcg_fused(b, x, converged, hist);
   cudaEventRecord(ev_[0], st_);
   const long long N = NG;
   const int grid = red_grid(N);

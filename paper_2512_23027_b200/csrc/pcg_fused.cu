@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "solver.cuh"
 #include "tiles.cuh"
@@ -750,6 +751,16 @@ void GpuSolver::setup_fused_pcg() {
 }
 
 int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist) {
+  pcg_fused_launch(b, x);
+  SGW_CUDA(cudaEventSynchronize(ev_[1]));
+  return pcg_fused_finish(converged, hist);
+}
+
+// Asynchronous half: the kernel, then its outputs (iterations, convergence,
+// residual history) copied into pinned host memory; pcg_fused_finish reads them
+// once the stream has passed ev_[1] (step() launches the recovery first).
+void GpuSolver::pcg_fused_launch(const double* b, double* x) {
+  if (!h_fused_) SGW_CUDA(cudaMallocHost(&h_fused_, (4 + fused_hist_.n) * sizeof(double)));
   cudaEventRecord(ev_[0], st_);
   FusedPcg A{};
   A.NG = NG;
@@ -777,10 +788,14 @@ int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vecto
   SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_fused_kernel, dim3(fused_grid_), dim3(256), args,
                                        fused_smem_, st_));
   SGW_LAUNCHED();
-  int out[3] = {0, 0, 0};
-  SGW_CUDA(cudaMemcpyAsync(out, fused_out_.p, sizeof(out), cudaMemcpyDeviceToHost, st_));
+  SGW_CUDA(cudaMemcpyAsync(h_fused_, fused_out_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  SGW_CUDA(cudaMemcpyAsync(h_fused_ + 4, fused_hist_.p, fused_hist_.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
   cudaEventRecord(ev_[1], st_);
-  SGW_CUDA(cudaEventSynchronize(ev_[1]));
+}
+
+int GpuSolver::pcg_fused_finish(bool* converged, std::vector<double>* hist) {
+  int out[3];
+  std::memcpy(out, h_fused_, sizeof(out));
   float ms = 0;
   cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
   T.pcg_ms += ms;
@@ -789,13 +804,8 @@ int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vecto
   T.nn2s += out[0];
   *converged = out[1] != 0;
   const int hl = std::min<int>(out[2], (int)fused_hist_.n);
-  std::vector<double> h(std::max(hl, 1));
-  SGW_CUDA(cudaMemcpy(h.data(), fused_hist_.p, hl * sizeof(double), cudaMemcpyDeviceToHost));
-  last_rel = hl > 0 ? h[hl - 1] : 0.0;
-  if (hist) {
-    h.resize(hl);
-    *hist = h;
-  }
+  last_rel = hl > 0 ? h_fused_[4 + hl - 1] : 0.0;
+  if (hist) hist->assign(h_fused_ + 4, h_fused_ + 4 + hl);
   return out[0];
 }
 

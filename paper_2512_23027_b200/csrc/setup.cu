@@ -436,6 +436,7 @@ GpuSolver::~GpuSolver() {
   if (graph_mv_) cudaGraphExecDestroy(graph_mv_);
   if (graph_pc_) cudaGraphExecDestroy(graph_pc_);
   if (h_scal_) cudaFreeHost(h_scal_);
+  if (h_fused_) cudaFreeHost(h_fused_);
   if (own_stream_ && st_) cudaStreamDestroy(st_);
 }
 

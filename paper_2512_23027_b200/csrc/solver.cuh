@@ -319,6 +319,10 @@ class GpuSolver {
   // persistent cooperative PCG (pcg_fused.cu)
   void setup_fused_pcg();
   int pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist);
+  void pcg_fused_launch(const double* b, double* x);
+  int pcg_fused_finish(bool* converged, std::vector<double>* hist);
+  bool fused_ok() const { return use_fused_ && !comm_ && P.precond == 0 && !P.implicit_schur; }
+  double* h_fused_ = nullptr;  // pinned: persistent PCG outputs [4 ints as doubles' room][history]
   DBuf<int> smap_, fused_out_;
   RangeBufs rs_, rq_, rp_;
   // Psi_s^T as rectangular tiles for the persistent kernel (pcg_fused.cu)

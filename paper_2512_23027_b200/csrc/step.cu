@@ -532,9 +532,17 @@ int GpuSolver::step(int* iters_out) {
   allreduce(vb.p, NG);
   cudaEventRecord(ev_[3], st_);
   bool conv = false;
-  const int it = pcg(vb.p, vx.p, &conv, nullptr);
-  if (!conv)
-    throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+  // persistent PCG: its convergence is read after the recovery is launched
+  // (no host round trip between the solve and the rest of the step)
+  const bool deferred = fused_ok();
+  int it = 0;
+  if (deferred) {
+    pcg_fused_launch(vb.p, vx.p);
+  } else {
+    it = pcg(vb.p, vx.p, &conv, nullptr);
+    if (!conv)
+      throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+  }
   cudaEventRecord(ev_[4], st_);
   gather_li(vx.p, li_x.p, false);
   // A_IG u_G is non-zero only on interior nodes next to the interface
@@ -553,6 +561,11 @@ int GpuSolver::step(int* iters_out) {
   record_probes(step_index);
   cudaEventRecord(ev_[5], st_);
   SGW_CUDA(cudaEventSynchronize(ev_[5]));
+  if (deferred) {
+    it = pcg_fused_finish(&conv, nullptr);
+    if (!conv)
+      throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index - 1));
+  }
   KP.collect();
   float ms_rhs = 0, ms_rec = 0, ms_all = 0;
   cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);
