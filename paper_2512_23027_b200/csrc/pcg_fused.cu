@@ -1,22 +1,25 @@
 // The whole interface PCG solve (src/pcg.cpp:7-50) with the NN2 preconditioner
 // (src/dd.cpp:199-253) as ONE persistent cooperative kernel: every CTA walks
 // the same phase sequence separated by grid barriers, so a PCG iteration costs
-// seven grid barriers instead of a dozen launches plus a host round trip for
+// eight grid barriers instead of a dozen launches plus a host round trip for
 // the convergence test.
 //
 // Per iteration (phase -> grid barrier):
-//   1. S tiles      q_tiles(S_s) on p_new = z + beta p gathered on the fly
-//   2. S scatter    q = sum_s R_s^T S_s R_s p_new, partial p.q
-//   3. update       p = p_new, x += alpha p, r -= alpha q, partial r.r, and the
+//   1. S walk       the CTA's contiguous range of S_s tiles on p_new = z + beta p
+//                   (local vectors and accumulators in shared memory)
+//   2. S scatter    q = sum_s R_s^T S_s R_s p_new from the CTA partials, p.q
+//   3. update       p = p_new, x += alpha p, r -= alpha q, r.r, and the
 //                   weighted local copies D_s R_s r (NN2 inputs f_r, f_c)
-//   4. Q tiles      Q_s f_r tiles + d_s = f_c - Psi_s^T f_r
-//   5. coarse       d = sum_s B_s^T d_s
-//   6. coarse solve u_c = F_cc^-1 d
-//   7. z scatter    z = sum_s R_s^T D_s [Q f_r - Psi u_c ; u_c], partial r.z
-// Reductions: fixed-order block sums, then every CTA sums the block partials
-// in index order itself (bitwise identical in every CTA, run to run).
-// The convergence test, the true-residual confirmation and the restart from
-// the true residual are evaluated on device exactly as src/pcg.cpp:30-40.
+//   4. Q / Psi walk Q_s f_r and Psi_s^T f_r (Psi as rectangular tiles)
+//   5. coarse       d = sum_s B_s^T (f_c - Psi_s^T f_r)
+//   6. coarse solve u_c = F_cc^-1 d; Psi walk on B_s u_c
+//   7. z scatter    z = sum_s R_s^T D_s [Q f_r - Psi u_c ; u_c], r.z
+// Every tile stream goes through a per-CTA TMA ring (evict-first); a walk
+// issues the next walk's first tiles during its tail.  Reductions: fixed-order
+// block sums, then every CTA sums the block partials in index order itself
+// (bitwise identical in every CTA, run to run).  The convergence test, the
+// true-residual confirmation and the restart from the true residual are
+// evaluated on device exactly as src/pcg.cpp:30-40.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -87,7 +90,6 @@ extern __shared__ __align__(128) double dyn_smem[];  // ring stages, local vecto
 
 struct Smem {
   double csum[8][kTile];
-  double xI[kTile], xJ[kTile];
   double red[40];
 };
 

@@ -323,7 +323,7 @@ class GpuSolver {
   int pcg_fused_finish(bool* converged, std::vector<double>* hist);
   bool fused_ok() const { return use_fused_ && !comm_ && P.precond == 0 && !P.implicit_schur; }
   double* h_fused_ = nullptr;  // pinned: persistent PCG outputs [4 ints as doubles' room][history]
-  DBuf<int> smap_, fused_out_;
+  DBuf<int> fused_out_;
   RangeBufs rs_, rq_, rp_;
   // Psi_s^T as rectangular tiles for the persistent kernel (pcg_fused.cu)
   DBuf<double> psi_tiles_;
