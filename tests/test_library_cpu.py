@@ -66,3 +66,35 @@ def test_invalid_arguments_rejected_before_device_work():
     coeff = O.lognormal_coeff(8, 8, 0.2, 1.0, 1.0, 2, 1)
     with pytest.raises(ValueError):  # mismatched tensor (test_sg.cpp "mismatched ... rejected")
         sg.SgSolver(8, 8, 2, 2, coeff, O.triple_products(2, 2, 2))
+
+
+def test_problem_struct_layout_matches_header(tmp_path):
+    # the ctypes mirror of sgw_problem must match the C layout field by field
+    import ctypes
+    import shutil
+    import subprocess
+
+    if not shutil.which("gcc"):
+        pytest.skip("no C compiler")
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "sgw.h"\n'
+                   'int main(void) { printf("%zu %zu %zu %zu\\n", sizeof(sgw_problem), '
+                   'offsetof(sgw_problem, nccl_id), offsetof(sgw_problem, precond), '
+                   'offsetof(sgw_problem, implicit_schur)); return 0; }\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    size, o_id, o_pc, o_imp = (int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                              check=True).stdout.split())
+    P = sg.sgwave._Problem
+    assert ctypes.sizeof(P) == size
+    assert (P.nccl_id.offset, P.precond.offset, P.implicit_schur.offset) == (o_id, o_pc, o_imp)
+
+
+def test_preconditioner_names():
+    # precond_from_string (dd.hpp:100); test_cli_io.cpp:65 rejects "jacobi"
+    assert [sg.precond_from_string(k) for k in ("nn2", "nn1", "lumped")] == [0, 1, 2]
+    with pytest.raises(ValueError):
+        sg.precond_from_string("jacobi")
+    coeff = O.lognormal_coeff(8, 8, 0.2, 1.0, 1.0, 1, 1)
+    with pytest.raises(ValueError):  # rejected before any device work
+        sg.SgSolver(8, 8, 2, 2, coeff, O.triple_products(1, 1, 1), options=sg.SgOptions(precond="jacobi"))
