@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--implicit-schur", action="store_true",
+                    help="reduced-memory mode (S_s not stored, applied through the interior solve)")
     ap.add_argument("--force-shard", action="store_true",
                     help="test hook: the sharded code path (NCCL communicator) even on one rank")
     ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
@@ -204,7 +206,8 @@ def main():
         kw = dict(rank=rank, world_size=world, nccl_id=ids[0])
     t0 = time.perf_counter()
     solver = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, tensor, alpha0=ALPHA0, alpha1=ALPHA1,
-                         params=sg.NewmarkParams(dt=c["dt"]), options=sg.SgOptions(tol=TOL, device=local), **kw)
+                         params=sg.NewmarkParams(dt=c["dt"]),
+                         options=sg.SgOptions(tol=TOL, device=local, implicit_schur=args.implicit_schur), **kw)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     solver.set_stream(stream.cuda_stream)
@@ -281,7 +284,9 @@ def main():
                    "parallelism": "single GPU" if world == 1 else (
                        f"{world} GPUs, subdomains sharded {[len(r) for r in sg.shard_plan(c['px'] ** 2, world)]}, "
                        "interface sums by ncclAllReduce" if shard else f"{world} independent replicas"),
-                   "l2": "inputs larger than L2: S+Q tiles stream ~2.7 GB per PCG iteration (L2 126 MB)"},
+                   "l2": "inputs larger than L2: S+Q tiles stream ~2.7 GB per PCG iteration (L2 126 MB)",
+                   **({"mode": "reduced-memory (implicit Schur: S_s applied through the interior sweep)"}
+                      if args.implicit_schur else {})},
         "s_per_newmark_step": ms / args.steps / 1e3,
         "pcg_iterations": iters_all, "mean_iterations_per_step": iters / args.steps,
         "setup_s": setup_s,
