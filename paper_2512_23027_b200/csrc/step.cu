@@ -127,8 +127,10 @@ __global__ void local_force_kernel(LocalArgs A, int n, const double* __restrict_
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     int lid, k, s;
     if (list) {
-      const int e = list[t / A.nt];
-      s = e / A.nl, lid = e % A.nl, k = int(t % A.nt);
+      // term-major: a warp's lanes share the output term k (uniform loops over
+      // its tensor entries, broadcast entry loads) and cover consecutive nodes
+      const int e = list[t % nlist];
+      s = e / A.nl, lid = e % A.nl, k = int(t / nlist);
     } else {
       lid = int(t % A.nl), k = int((t / A.nl) % A.nt), s = int(t / ((long long)A.nl * A.nt));
     }
@@ -230,6 +232,106 @@ __global__ void coupling_kernel(LocalArgs A, int mode, const double* __restrict_
       outI[interior_index(A, s, il, jl, k)] = acc;
     }
   }
+}
+
+// ----------------------------------------------------- coupling blocks ---
+// Block of the transient operator between interface node q and interior node
+// i of subdomain s (direction dir from q):  C[k][j] = ms M(q,i) d_kj +
+// ss sum_{(i', j, g) in G(k)} g K_i'(q, i)  -- symmetric, and A(i, q) = A(q, i).
+// One CTA per edge, thread = row k.
+__global__ void coupling_block_kernel(LocalArgs A, const int4* __restrict__ edge, double* __restrict__ blk) {
+  const int4 e = edge[blockIdx.x];
+  const int s = e.x, q = e.y, nb = e.z, dir = e.w, nt = A.nt;
+  const double* Ms = A.Ml + (long long)s * 4 * A.nl;
+  const double* Ks = A.Kl + (long long)s * A.nin * 3 * A.nl;
+  double* C = blk + (long long)blockIdx.x * nt * nt;
+  const double m = A.ms * mco(Ms, A.nl, q, nb, dir);
+  for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+    double* row = C + (long long)k * nt;
+    for (int j = 0; j < nt; ++j) row[j] = j == k ? m : 0.0;
+    if (dir < 5)
+      for (int g = A.g.ptr[k]; g < A.g.ptr[k + 1]; ++g)
+        row[A.g.j[g]] += (A.ss * A.g.v[g]) * kco(Ks + (long long)A.g.i[g] * 3 * A.nl, A.nl, q, nb, dir);
+  }
+}
+
+// mode 0 (A_GI y): out_LI[s][k ng + p] = fG - sum_{edges of q} C y(i)
+// mode 1 (A_IG u): out_I[s][..]      = sum_{edges of i} C u(q)
+// thread = (list entry, k), node-major: the lanes of a node share its edges
+__global__ void coupling_blk_kernel(LocalArgs A, int mode, const double* __restrict__ blk,
+                                    const int4* __restrict__ edge, const int* __restrict__ q_cls,
+                                    const int* __restrict__ ptr, const int* __restrict__ eidx,
+                                    const int* __restrict__ list, long long nlist, const double* __restrict__ yI,
+                                    const double* __restrict__ fG, const double* __restrict__ uLI,
+                                    double* __restrict__ outLI, double* __restrict__ outI) {
+  const int nt = A.nt;
+  const long long total = nlist * nt;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int a = int(t / nt), k = int(t % nt);
+    double acc = 0.0;
+    for (int c = ptr[a]; c < ptr[a + 1]; ++c) {
+      const int ed = eidx[c];
+      const int4 e = edge[ed];
+      const double* row = blk + ((long long)ed * nt + k) * nt;
+      if (mode == 0) {
+        const int i2 = e.z % (A.mx + 1), j2 = e.z / (A.mx + 1);
+        const double* y = yI + ((long long)e.x * A.H + (j2 - 1)) * A.B + (long long)(i2 - 1) * nt;
+        for (int j = 0; j < nt; ++j) acc = fma(__ldg(row + j), y[j], acc);
+      } else {
+        const double* u = uLI + A.lioff[e.x] + q_cls[ed];
+        const int ng = A.ng[e.x];
+        for (int j = 0; j < nt; ++j) acc = fma(__ldg(row + j), u[(long long)j * ng], acc);
+      }
+    }
+    const int en = list[a], s = en / A.nl, lid = en % A.nl;
+    if (mode == 0) {
+      const long long o = A.lioff[s] + (long long)k * A.ng[s] + A.lid_to_p[(long long)s * A.nl + lid];
+      outLI[o] = fG[o] - acc;
+    } else {
+      outI[interior_index(A, s, lid % (A.mx + 1), lid / (A.mx + 1), k)] = acc;
+    }
+  }
+}
+
+void GpuSolver::build_coupling_blocks() {
+  // edges from the interface list (A_GI rows) and their transposes for the
+  // interior list (A_IG rows); host copies of the lists and classes
+  std::vector<int> il(n_ilist_), al(n_alist_), cls((size_t)NS * G.nl);
+  if (n_ilist_) SGW_CUDA(cudaMemcpy(il.data(), ilist_.p, il.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  if (n_alist_) SGW_CUDA(cudaMemcpy(al.data(), alist_.p, al.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  SGW_CUDA(cudaMemcpy(cls.data(), lid_to_p.p, cls.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  static const int DI[7] = {0, 1, -1, 0, 0, 1, -1}, DJ[7] = {0, 0, 0, 1, -1, 1, -1};
+  const int w = G.mx + 1;
+  std::vector<int4> edges;
+  std::vector<int> qcls, iptr(1, 0), iedge;
+  std::vector<std::vector<int>> by_interior((size_t)NS * G.nl);
+  for (size_t a = 0; a < il.size(); ++a) {
+    const int s = il[a] / G.nl, q = il[a] % G.nl, i0 = q % w, j0 = q / w;
+    for (int dir = 1; dir < 7; ++dir) {
+      const int i2 = i0 + DI[dir], j2 = j0 + DJ[dir];
+      if (i2 < 0 || i2 > G.mx || j2 < 0 || j2 > G.my) continue;
+      const int nb = j2 * w + i2;
+      if (cls[(size_t)s * G.nl + nb] != -2) continue;
+      by_interior[(size_t)s * G.nl + nb].push_back((int)edges.size());
+      iedge.push_back((int)edges.size());
+      edges.push_back(make_int4(s, q, nb, dir));
+      qcls.push_back(cls[(size_t)s * G.nl + q]);
+    }
+    iptr.push_back((int)iedge.size());
+  }
+  std::vector<int> aptr(1, 0), aedge;
+  for (int e : al) {
+    for (int ed : by_interior[e]) aedge.push_back(ed);
+    aptr.push_back((int)aedge.size());
+  }
+  cpl_edge_.upload(edges), cpl_q_cls_.upload(qcls), cpl_iptr_.upload(iptr), cpl_iedge_.upload(iedge);
+  cpl_aptr_.upload(aptr), cpl_aedge_.upload(aedge);
+  cpl_blk_.alloc(std::max<size_t>(1, edges.size() * (size_t)NT * NT));
+  if (!edges.empty()) {
+    coupling_block_kernel<<<(unsigned)edges.size(), 32, 0, st_>>>(local_args(), cpl_edge_.p, cpl_blk_.p);
+    SGW_LAUNCHED();
+  }
+  cpl_built_ = true;
 }
 
 // --------------------------------------------------------------- Newmark ---
@@ -525,8 +627,10 @@ int GpuSolver::step(int* iters_out) {
   }
   SGW_LAUNCHED();
   sweep(yI.p);  // y = A_II^-1 f_I
-  coupling_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
-      A, 0, yI.p, fG.p, nullptr, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
+  if (!cpl_built_) build_coupling_blocks();
+  coupling_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+      A, 0, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_iptr_.p, cpl_iedge_.p, ilist_.p, n_ilist_, yI.p, fG.p,
+      nullptr, li_y.p, nullptr);
   SGW_LAUNCHED();
   scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
   allreduce(vb.p, NG);
@@ -548,8 +652,9 @@ int GpuSolver::step(int* iters_out) {
   // A_IG u_G is non-zero only on interior nodes next to the interface
   SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
   if (n_alist_ > 0) {
-    coupling_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
-        A, 1, nullptr, nullptr, li_x.p, ip_off.p, iface_lid_.p, nullptr, wI.p, NS, alist_.p, n_alist_);
+    coupling_blk_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
+        A, 1, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_aptr_.p, cpl_aedge_.p, alist_.p, n_alist_, nullptr,
+        nullptr, li_x.p, nullptr, wI.p);
     SGW_LAUNCHED();
   }
   sweep(wI.p);  // A_II^-1 A_IG u_G
