@@ -348,7 +348,7 @@ class GpuSolver {
   // interface <-> interior coupling blocks (step.cu): per edge (interface node q,
   // interior neighbour i) the (P+1)^2 block of the transient operator A(q, i) =
   // A(i, q); CSR by interface-list entry (A_GI) and by interior-list entry (A_IG)
-  DBuf<double> cpl_blk_;
+  DBuf<double> cpl_blk_, frc_blk_;  // frc: local-force stiffness blocks of the interface list
   DBuf<int4> cpl_edge_;  // {s, q lid, i lid, dir}
   DBuf<int> cpl_q_cls_, cpl_iptr_, cpl_iedge_, cpl_aptr_, cpl_aedge_;
   bool cpl_built_ = false;

@@ -293,6 +293,68 @@ __global__ void coupling_blk_kernel(LocalArgs A, int mode, const double* __restr
   }
 }
 
+// Stiffness part of the local force on the interface list, per (entry a,
+// direction d <= 4): B[k][j] = sum_{(i, j, g) in G(k)} g K_i(q, nb_d) (the
+// element-assembled stencil of q; scaled by alpha1 at use).  CTA per (a, d).
+__global__ void force_block_kernel(LocalArgs A, const int* __restrict__ list, double* __restrict__ blk) {
+  const int a = blockIdx.x / 5, dir = blockIdx.x % 5, nt = A.nt;
+  const int e = list[a], s = e / A.nl, q = e % A.nl;
+  const int il = q % (A.mx + 1), jl = q / (A.mx + 1);
+  const int i2 = il + sDI[dir], j2 = jl + sDJ[dir];
+  const bool in = i2 >= 0 && i2 <= A.mx && j2 >= 0 && j2 <= A.my;
+  const int nb = in ? j2 * (A.mx + 1) + i2 : q;
+  const double* Ks = A.Kl + (long long)s * A.nin * 3 * A.nl;
+  double* C = blk + (long long)blockIdx.x * nt * nt;
+  for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+    double* row = C + (long long)k * nt;
+    for (int j = 0; j < nt; ++j) row[j] = 0.0;
+    if (in)
+      for (int g = A.g.ptr[k]; g < A.g.ptr[k + 1]; ++g)
+        row[A.g.j[g]] += A.g.v[g] * kco(Ks + (long long)A.g.i[g] * 3 * A.nl, A.nl, q, nb, dir);
+  }
+}
+
+// local_force_kernel's interface rows with the stiffness part from the blocks
+__global__ void local_force_blk_kernel(LocalArgs A, int n, const double* __restrict__ um, const double* __restrict__ uc,
+                                       double a0, double a1, const double* __restrict__ fnext, int fdof, double fval,
+                                       const double* __restrict__ iface_w, const int* __restrict__ ip_off,
+                                       double* __restrict__ fG, const int* __restrict__ list, long long nlist,
+                                       const double* __restrict__ blk) {
+  const int nt = A.nt;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nlist * nt; t += (long long)gridDim.x * blockDim.x) {
+    const int a = int(t / nt), k = int(t % nt);
+    const int e = list[a], s = e / A.nl, lid = e % A.nl;
+    const int cls = A.lid_to_p[(long long)s * A.nl + lid];
+    const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
+    const double* Ms = A.Ml + (long long)s * 4 * A.nl;
+    double f = 0.0;
+    int nbd0 = -1;
+#pragma unroll
+    for (int dir = 0; dir < 7; ++dir) {
+      const int i2 = il + sDI[dir], j2 = jl + sDJ[dir];
+      if (i2 < 0 || i2 > A.mx || j2 < 0 || j2 > A.my) continue;
+      const int nbl = j2 * (A.mx + 1) + i2;
+      if (A.lid_to_p[(long long)s * A.nl + nbl] == -1) continue;
+      const int nbd = lid_dof(A, s, i2, j2);
+      if (dir == 0) nbd0 = nbd;
+      const long long o = (long long)k * n + nbd;
+      f += mco(Ms, A.nl, lid, nbl, dir) * (um[o] + a0 * uc[o]);
+      if (dir < 5 && a1 > 0.0) {
+        const double* row = blk + (((long long)a * 5 + dir) * nt + k) * nt;
+        double sacc = 0.0;
+        for (int j = 0; j < nt; ++j) sacc = fma(__ldg(row + j), uc[(long long)j * n + nbd], sacc);
+        f += a1 * sacc;
+      }
+    }
+    const double wgt = iface_w[ip_off[s] + cls];
+    if (k == 0) {
+      if (fnext) f += wgt * fnext[nbd0];
+      else if (nbd0 == fdof) f += wgt * fval;
+    }
+    fG[A.lioff[s] + (long long)k * A.ng[s] + cls] = f;
+  }
+}
+
 void GpuSolver::build_coupling_blocks() {
   // edges from the interface list (A_GI rows) and their transposes for the
   // interior list (A_IG rows); host copies of the lists and classes
@@ -329,6 +391,13 @@ void GpuSolver::build_coupling_blocks() {
   cpl_blk_.alloc(std::max<size_t>(1, edges.size() * (size_t)NT * NT));
   if (!edges.empty()) {
     coupling_block_kernel<<<(unsigned)edges.size(), 32, 0, st_>>>(local_args(), cpl_edge_.p, cpl_blk_.p);
+    SGW_LAUNCHED();
+  }
+  // local-force stiffness blocks of the interface list (skipped when large)
+  const size_t fb = (size_t)n_ilist_ * 5 * NT * NT;
+  if (fb > 0 && fb * sizeof(double) <= (size_t(2) << 30)) {
+    frc_blk_.alloc(fb);
+    force_block_kernel<<<(unsigned)(n_ilist_ * 5), 32, 0, st_>>>(local_args(), ilist_.p, frc_blk_.p);
     SGW_LAUNCHED();
   }
   cpl_built_ = true;
@@ -618,9 +687,15 @@ int GpuSolver::step(int* iters_out) {
     interior_from_global_kernel<<<std::min(cdiv(tI, 256), 65535), 256, 0, st_>>>(A, n, yglob_.p, Mg.p, um.p, fvec,
                                                                                    fdof, fval, yI.p, NS);
     SGW_LAUNCHED();
-    local_force_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
-        A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, yI.p, fG.p, NS, ilist_.p,
-        n_ilist_);
+    if (!cpl_built_) build_coupling_blocks();
+    if (frc_blk_.p)
+      local_force_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+          A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, fG.p, ilist_.p, n_ilist_,
+          frc_blk_.p);
+    else
+      local_force_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+          A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, yI.p, fG.p, NS, ilist_.p,
+          n_ilist_);
   } else {
     local_force_kernel<<<std::min(cdiv(tl, 256), 65535), 256, 0, st_>>>(
         A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, yI.p, fG.p, NS, nullptr, 0);
