@@ -410,7 +410,9 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
     finish_nn2(fcc);
   }
 
-  // work vectors
+  // work vectors (the step kernels use 32-bit index arithmetic)
+  if (NSTATE >= (size_t(1) << 31) || (size_t)NS * G.H * B >= (size_t(1) << 31))
+    throw Error(1, "state too large for one GPU (2^31 entries)");
   for (DBuf<double>* b : {&u, &v, &a, &um, &uc, &unext}) b->alloc(NSTATE), b->zero(st_);
   for (DBuf<double>* b : {&vb, &vx, &vr, &vz, &vp, &vq, &vrt}) b->alloc(NG), b->zero(st_);
   li_x.alloc(Sp.xlen), li_x.zero(st_);

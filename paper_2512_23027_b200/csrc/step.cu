@@ -265,9 +265,9 @@ __global__ void coupling_blk_kernel(LocalArgs A, int mode, const double* __restr
                                     const double* __restrict__ fG, const double* __restrict__ uLI,
                                     double* __restrict__ outLI, double* __restrict__ outI) {
   const int nt = A.nt;
-  const long long total = nlist * nt;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int a = int(t / nt), k = int(t % nt);
+  const int total = int(nlist) * nt;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int a = t / nt, k = t % nt;
     double acc = 0.0;
     for (int c = ptr[a]; c < ptr[a + 1]; ++c) {
       const int ed = eidx[c];
@@ -320,9 +320,9 @@ __global__ void local_force_blk_kernel(LocalArgs A, int n, const double* __restr
                                        const double* __restrict__ iface_w, const int* __restrict__ ip_off,
                                        double* __restrict__ fG, const int* __restrict__ list, long long nlist,
                                        const double* __restrict__ blk) {
-  const int nt = A.nt;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nlist * nt; t += (long long)gridDim.x * blockDim.x) {
-    const int a = int(t / nt), k = int(t % nt);
+  const int nt = A.nt, total = int(nlist) * nt;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int a = t / nt, k = t % nt;
     const int e = list[a], s = e / A.nl, lid = e % A.nl;
     const int cls = A.lid_to_p[(long long)s * A.nl + lid];
     const int il = lid % (A.mx + 1), jl = lid / (A.mx + 1);
@@ -422,10 +422,10 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
                               const double* __restrict__ wI, const int* __restrict__ iface_of_dof, int n, int nt,
                               int n_iface, int nx, int ny, int px, int py, int H, int B, int s0, int ns,
                               double dt, double zeta, double gamma) {
-  const long long N = (long long)n * nt;
+  const int N = n * nt;  // < 2^31 (GpuSolver ctor): 32-bit index arithmetic
   const double zdd = zeta * dt * dt, c1 = (1.0 - 2.0 * zeta) / (2.0 * zeta);
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
-    const int d = int(t % n), k = int(t / n);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N; t += gridDim.x * blockDim.x) {
+    const int d = t % n, k = t / n;
     const int q = iface_of_dof[d];
     double un;
     if (q >= 0) {
@@ -631,10 +631,10 @@ __global__ void interior_from_global_kernel(LocalArgs A, int n, const double* __
                                             const double* __restrict__ Mg, const double* __restrict__ um,
                                             const double* __restrict__ fnext, int fdof, double fval,
                                             double* __restrict__ yI, int ns) {
-  const long long total = (long long)ns * A.H * A.B;
+  const int total = ns * A.H * A.B;  // < 2^31 (GpuSolver ctor)
   const int rw = A.nx - 1, rh = A.ny - 1;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int row = int(t % A.B), jl = int((t / A.B) % A.H) + 1, s = int(t / ((long long)A.B * A.H));
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int row = t % A.B, jl = (t / A.B) % A.H + 1, s = t / (A.B * A.H);
     const int il = row / A.nt + 1, k = row % A.nt;
     const int lid = jl * (A.mx + 1) + il;
     if (A.lid_to_p[(long long)s * A.nl + lid] != -2) continue;  // unit row of a ragged block
