@@ -407,7 +407,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
   if (coarse) {
     // 5. one warp per coarse dof: lane group e (8 lanes) takes subdomain e
     //    (<= 4 share a cross point), its lanes split the CTA partials
-    for (long long qc = gwarp; qc < A.NC; qc += nwarps) {
+    for (long long qc = blockIdx.x + (long long)(threadIdx.x >> 5) * gridDim.x; qc < A.NC; qc += nwarps) {
       const int j = int(qc / A.n_corner), gc = int(qc % A.n_corner), e = lane >> 3, kk = lane & 7;
       double d = 0.0;
       if (e < A.cinv_cnt[gc]) {
@@ -429,7 +429,11 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
       for (int c = threadIdx.x; c < A.NC; c += blockDim.x) xs[c] = __ldcg(A.dco + c);
       __syncthreads();
     }
-    for (long long row = gwarp; row < A.NC; row += nwarps) {
+    // rows dealt round-robin over the CTAs first (row = b + (warp + 8 i) G):
+    // every SM streams its share of F_cc^-1 even when n_C < number of warps
+    const int nw = blockDim.x >> 5;
+    for (long long row = blockIdx.x + (long long)(threadIdx.x >> 5) * gridDim.x; row < A.NC;
+         row += (long long)nw * gridDim.x) {
       const double* col = A.Finv + row * A.NC;
       auto dv = [&](int c) { return dsm ? xs[c] : __ldcg(A.dco + c); };
       const int h = int((row * A.NC) & 1);  // leading element before the 16-byte aligned part
