@@ -283,6 +283,43 @@ __global__ void scatter_kernel(double* __restrict__ X, const double* __restrict_
   if (dw) finalize_sum(acc, partials, counter, dout, nullptr);
 }
 
+// scatter_kernel<true> on the CTA partials of a tile walk (walk_kernel)
+__global__ void scatter_range_kernel(double* __restrict__ X, const RangePack P, const int* __restrict__ inv_cnt,
+                                     const int* __restrict__ inv_s, const int* __restrict__ inv_p,
+                                     const int* __restrict__ ng, int n_iface, long long NG,
+                                     const double* __restrict__ dw, double* partials, unsigned* counter,
+                                     double* dout) {
+  double acc = 0.0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < NG; q += (long long)gridDim.x * blockDim.x) {
+    const int j = int(q / n_iface), g = int(q % n_iface);
+    double y = 0.0;
+    for (int e = 0; e < inv_cnt[g]; ++e) {
+      const int s = inv_s[4 * g + e], p = inv_p[4 * g + e];
+      y += range_reduce(P, s, j * ng[s] + p);
+    }
+    X[q] = y;
+    if (dw) acc += y * dw[q];
+  }
+  if (dw) finalize_sum(acc, partials, counter, dout, nullptr);
+}
+
+// S x (no exchange): the stored S tiles, by a tile walk when the ranges exist
+void GpuSolver::s_product(const double* x, double* y, const double* dot_with, double* dot_out) {
+  const int grid = red_grid(NG);
+  gather_li(x, li_x.p, false);
+  if (walk_ok_) {
+    walk_pack(0, li_x.p);
+    scatter_range_kernel<<<grid, 256, 0, st_>>>(y, range_pack(0), inv_cnt.p, inv_s.p, inv_p.p, ng_d.p, G.n_iface, NG,
+                                                dot_with, dpart.p, dcount.p, dot_out);
+  } else {
+    symv(Sp, li_x.p, nullptr);
+    scatter_kernel<true><<<grid, 256, 0, st_>>>(y, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
+                                                inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
+                                                Sp.d_tile_base.p, Sp.d_ntile.p, dot_with, dpart.p, dcount.p, dot_out);
+  }
+  SGW_LAUNCHED();
+}
+
 void GpuSolver::scatter_li(const double* li, double* glob, bool weighted, double* dot_with, double* dot_out) {
   const int grid = red_grid(NG);
   scatter_kernel<false><<<grid, 256, 0, st_>>>(glob, li, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
@@ -294,13 +331,7 @@ void GpuSolver::scatter_li(const double* li, double* glob, bool weighted, double
 // --------------------------------------------------------------- matvec ----
 void GpuSolver::schur_matvec(const double* x, double* y) {
   if (P.implicit_schur) return schur_matvec_implicit(x, y);
-  gather_li(x, li_x.p, false);
-  symv(Sp, li_x.p, nullptr);
-  const int grid = red_grid(NG);
-  scatter_kernel<true><<<grid, 256, 0, st_>>>(y, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
-                                              inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
-                                              Sp.d_tile_base.p, Sp.d_ntile.p, nullptr, nullptr, nullptr, nullptr);
-  SGW_LAUNCHED();
+  s_product(x, y, nullptr, nullptr);
   allreduce(y, NG);  // sharded: partial sums over owned subdomains
   ++T.matvecs;
 }
@@ -405,12 +436,44 @@ __global__ void nn2_local_kernel(double* __restrict__ li, const long long* __res
   }
 }
 
+// nn2_local_kernel on the CTA partials of the Q walk
+__global__ void nn2_local_range_kernel(double* __restrict__ li, const long long* __restrict__ lioff,
+                                       const int* __restrict__ ip_off, const int* __restrict__ pkind,
+                                       const int* __restrict__ ng, const int* __restrict__ nr,
+                                       const int* __restrict__ nc, int nt, const RangePack Pq,
+                                       const double* __restrict__ Psi, const long long* __restrict__ psioff,
+                                       const double* __restrict__ uc, const int* __restrict__ corner_pos_flat,
+                                       const int* __restrict__ cp_off, int n_corner, int has_coarse) {
+  const int s = blockIdx.y;
+  const int a = ng[s] * nt, rsz = nr[s] * nt, ncs = nc[s];
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < a; f += gridDim.x * blockDim.x) {
+    const int j = f / ng[s], p = f % ng[s];
+    const int k = pkind[ip_off[s] + p];
+    double v;
+    if (k >= 0) {
+      const int ar = j * nr[s] + k;
+      v = range_reduce(Pq, s, ar);
+      if (has_coarse) {
+        const double* P = Psi + psioff[s] + ar;
+        for (int jc = 0; jc < nt; ++jc)
+          for (int cc = 0; cc < ncs; ++cc)
+            v -= P[(long long)(jc * ncs + cc) * rsz] * uc[jc * n_corner + corner_pos_flat[cp_off[s] + cc]];
+      }
+    } else {
+      const int cc = -1 - k;
+      v = has_coarse ? uc[j * n_corner + corner_pos_flat[cp_off[s] + cc]] : 0.0;
+    }
+    li[lioff[s] + f] = v;
+  }
+}
+
 void GpuSolver::apply_nn2(const double* r, double* z) {
   const long long nr_tot = roff_.back(), nc_tot = coff_.back();
   nn2_gather_kernel<<<red_grid(nr_tot + nc_tot), 256, 0, st_>>>(r, r_gidx.p, r_w.p, r_x.p, nr_tot, c_gidx.p, c_w.p,
                                                                  c_f.p, nc_tot);
   SGW_LAUNCHED();
-  symv(Qp, r_x.p, nullptr);
+  if (walk_ok_) walk_pack(1, r_x.p);
+  else symv(Qp, r_x.p, nullptr);
   const bool has_coarse = NC > 0;
   if (has_coarse) {
     psi_t_kernel<<<dim3(cdiv(NT * 4, 8), NS), 256, 0, st_>>>(Psi.p, d_psioff.p, r_x.p, d_roff.p, c_f.p, d_coff.p,
@@ -423,10 +486,15 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
     symv_dense_kernel<<<cdiv(NC, 8), 256, 0, st_>>>(Finv.p, dcoarse.p, ucoarse.p, NC);
     SGW_LAUNCHED();
   }
-  nn2_local_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
-      li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, Qp.rowpart.p, Qp.colpart.p,
-      Qp.d_tile_base.p, Qp.d_ntile.p, Psi.p, d_psioff.p, ucoarse.p, cpos_flat_.p, cp_off_.p, G.n_corner,
-      has_coarse ? 1 : 0);
+  if (walk_ok_)
+    nn2_local_range_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
+        li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, range_pack(1), Psi.p, d_psioff.p,
+        ucoarse.p, cpos_flat_.p, cp_off_.p, G.n_corner, has_coarse ? 1 : 0);
+  else
+    nn2_local_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
+        li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, Qp.rowpart.p, Qp.colpart.p,
+        Qp.d_tile_base.p, Qp.d_ntile.p, Psi.p, d_psioff.p, ucoarse.p, cpos_flat_.p, cp_off_.p, G.n_corner,
+        has_coarse ? 1 : 0);
   SGW_LAUNCHED();
   scatter_li(li_y.p, z, true, nullptr, nullptr);
   allreduce(z, NG);
@@ -512,13 +580,7 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
       dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();
     } else {
-    gather_li(vp.p, li_x.p, false);
-    symv(Sp, li_x.p, nullptr);
-    scatter_kernel<true><<<grid, 256, 0, st_>>>(vq.p, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
-                                                inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
-                                                Sp.d_tile_base.p, Sp.d_ntile.p, comm_ ? nullptr : vp.p, dpart.p,
-                                                dcount.p, scal.p + PQ);
-    SGW_LAUNCHED();
+    s_product(vp.p, vq.p, comm_ ? nullptr : vp.p, scal.p + PQ);
     }
     if (comm_ && !P.implicit_schur) {
       allreduce(vq.p, NG);
@@ -595,13 +657,7 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
       dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();
     } else {
-    gather_li(vp.p, li_x.p, false);
-    symv(Sp, li_x.p, nullptr);
-    scatter_kernel<true><<<grid, 256, 0, st_>>>(vq.p, nullptr, Sp.d_xoff.p, ip_off.p, iface_w.p, inv_cnt.p, inv_s.p,
-                                                inv_p.p, ng_d.p, G.n_iface, NG, 0, Sp.rowpart.p, Sp.colpart.p,
-                                                Sp.d_tile_base.p, Sp.d_ntile.p, comm_ ? nullptr : vp.p, dpart.p,
-                                                dcount.p, scal.p + PQ);
-    SGW_LAUNCHED();
+    s_product(vp.p, vq.p, comm_ ? nullptr : vp.p, scal.p + PQ);
     }
     if (comm_ && !P.implicit_schur) {  // sharded: q is complete only after the sum over ranks
       allreduce(vq.p, NG);

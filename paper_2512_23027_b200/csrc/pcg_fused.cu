@@ -33,35 +33,6 @@ namespace cg = cooperative_groups;
 
 namespace sgw {
 
-// A tile pack walked in contiguous tile ranges, one per CTA.  Two kinds:
-//  * symmetric (S_s, Q_s): lower 64x64 tiles (I, J <= I), row-major over the
-//    tiles of a matrix, diagonal tiles full, 32 KB each;
-//  * rectangular (Psi_s^T): tiles (I, J), I over 64-wide corner-column chunks,
-//    J over 64-row blocks of the remaining dofs, row-major; tile (I, J) is the
-//    column-major 64 x w chunk of Psi_s (w = the chunk's valid columns, rows
-//    past r_s stored as zeros), i.e. row-major Psi^T rows of stride 64, w x 512
-//    bytes, so one bulk copy moves only stored data.
-// A CTA keeps the local input vector of its current matrix and a local
-// accumulator in shared memory, adds every tile's row and column products
-// into it (tile_acc), and at a matrix boundary writes the accumulator as its
-// partial of that matrix: y_s = sum over the CTAs covering s of their
-// partials, in CTA order.  Local vectors: symmetric [64 nt]; rectangular
-// [64 nI (corner chunks) | 64 nJ (remaining-dof blocks)].
-struct RangePack {
-  const double* tiles;
-  const long long* toff;      // per tile: offset in doubles (null: t * 4096)
-  const int* tbytes;          // per tile: bytes (null: 32 KB)
-  const int* nI;              // per matrix: tile rows (symmetric: tiles per side)
-  const int* nJ;              // per matrix: tile columns (rectangular only)
-  int rect;
-  const long long* t_first;   // [G + 1] first tile of each CTA's range
-  const int4* start;          // [G] {matrix, I, J} of each CTA's first tile
-  const int* c0;              // per matrix: first CTA covering it
-  const int* ncta;            // per matrix: CTAs covering it
-  const long long* pbase;     // per matrix: offset of its partials in part
-  double* part;               // partials [pbase[s] + (c - c0[s]) len_s + i]
-};
-
 struct FusedPcg {
   long long NG;
   int n_iface, NT, NS, n_corner, NC, max_iter, hist_cap;
@@ -330,28 +301,6 @@ __device__ void range_phase(Ring& R, int kind, const RangePack& P, const RangePa
   range_flush(P, cur, len, acc);
 }
 
-// sum of the n CTA partials p[k len] of one local entry, k ascending
-__device__ __forceinline__ double partial_sum(const double* p, int len, int n) {
-  double y = 0.0;
-  int k = 0;
-  for (; k + 4 <= n; k += 4) {
-    const double a = __ldcg(p + (long long)k * len), b = __ldcg(p + (long long)(k + 1) * len),
-                 c = __ldcg(p + (long long)(k + 2) * len), d = __ldcg(p + (long long)(k + 3) * len);
-    y += a, y += b, y += c, y += d;
-  }
-  for (; k < n; ++k) y += __ldcg(p + (long long)k * len);
-  return y;
-}
-// y_s[i] from the partials of the CTAs covering symmetric matrix s
-__device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i) {
-  return partial_sum(P.part + P.pbase[s] + i, kTile * P.nI[s], P.ncta[s]);
-}
-// Psi^T x (corner part, i < 64 nI) or Psi x (remaining-dof part, offset 64 nI)
-// of rectangular matrix s
-__device__ __forceinline__ double rect_reduce(const RangePack& P, int s, int i) {
-  return partial_sum(P.part + P.pbase[s] + i, kTile * (P.nI[s] + P.nJ[s]), P.ncta[s]);
-}
-
 // mode 0: x vector = first ? z : z + beta p (lazy p update); mode 1: x
 __device__ void s_tiles_phase(const FusedPcg& A, Ring& R, Smem& sm, double* xs, double* acc, int mode, bool first,
                               double beta) {
@@ -617,6 +566,28 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   __syncthreads();
 }
 
+// One tile walk as a standalone (non-cooperative) launch, for the host-driven
+// PCG of sharded runs: every CTA walks its range of P on the local vector x
+// (layout xoff) and writes its partials; consumers use range_reduce.
+__global__ void __launch_bounds__(256) walk_kernel(RangePack P, const double* __restrict__ x,
+                                                   const long long* __restrict__ xoff, int nst, int maxlen) {
+  __shared__ Smem sm;
+  __shared__ unsigned long long ring_bar[kMaxRing];
+  Ring R{dyn_smem, ring_bar, nst, 0, 0, 0};
+  double* xs = dyn_smem + (size_t)nst * kTile * kTile;
+  for (int i = threadIdx.x; i < nst * kTile * kTile; i += blockDim.x) dyn_smem[i] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) mb_init(&ring_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  range_phase(R, 1, P, nullptr, xs, xs + maxlen, sm, [&](int s, int i) { return __ldg(x + xoff[s] + i); });
+  if (threadIdx.x == 0)
+    for (int c = R.consumed; c < R.issued; ++c) mb_wait(&R.full[c % R.nst], (c / R.nst) & 1);
+  __syncthreads();
+}
+
 // --------------------------------------------------------------- host ----
 // Contiguous tile ranges per CTA over a pack whose matrix s holds tiles
 // [tile_base[s], tile_base[s + 1]) in row-major order: lower tiles of an
@@ -709,7 +680,7 @@ void GpuSolver::build_psi_tiles() {
 
 void GpuSolver::setup_fused_pcg() {
   tphase_.alloc(8), tphase_.zero(st_);
-  if (comm_ || P.implicit_schur) {  // sharded / reduced-memory: the host-driven loop
+  if (P.implicit_schur) {  // reduced-memory: the host-driven loop without S tiles
     use_fused_ = false;
     return;
   }
@@ -744,8 +715,15 @@ void GpuSolver::setup_fused_pcg() {
                                 (int)fused_smem_));
   SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pcg_fused_kernel, 256, fused_smem_));
   fused_grid_ = std::max(1, std::min(nb, bps)) * sms;
+  SGW_CUDA(cudaFuncSetAttribute((const void*)walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused_smem_));
   rs_.plan(Sp.tile_base, Sp.ntile, {}, fused_grid_);
   rq_.plan(Qp.tile_base, Qp.ntile, {}, fused_grid_);
+  walk_ok_ = true;  // the host-driven loop streams S / Q with walk_kernel too
+  if (comm_) {      // sharded: the host-driven loop with a sum over ranks after each scatter
+    use_fused_ = false;
+    return;
+  }
   build_psi_tiles();
   fused_part_.alloc(size_t(8) * fused_grid_);
   fused_out_.alloc(4);
@@ -754,6 +732,23 @@ void GpuSolver::setup_fused_pcg() {
   ucl_.alloc(std::max<long long>(1, coff_.back())), ucl_.zero(st_);
   const char* e = std::getenv("SGW_PCG");
   use_fused_ = !(e && std::string(e) == "host");
+}
+
+RangePack GpuSolver::range_pack(int which) const {
+  const TilePack& tp = which == 0 ? Sp : Qp;
+  const RangeBufs& rb = which == 0 ? rs_ : rq_;
+  return RangePack{tp.tiles.p, nullptr, nullptr, tp.d_ntile.p, nullptr, 0, rb.t_first.p, rb.start.p, rb.c0.p,
+                   rb.ncta.p, rb.pbase.p, rb.part.p};
+}
+
+void GpuSolver::walk_pack(int which, const double* x) {
+  const TilePack& tp = which == 0 ? Sp : Qp;
+  if (!tp.n_tiles) return;
+  cudaEvent_t e0;
+  KP.begin(which == 0 ? K_SYMV_S : K_SYMV_Q, st_, &e0);
+  walk_kernel<<<fused_grid_, 256, fused_smem_, st_>>>(range_pack(which), x, tp.d_xoff.p, fused_nst_, fused_maxlen_);
+  SGW_LAUNCHED();
+  KP.end(st_);
 }
 
 int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist) {

@@ -194,6 +194,8 @@ class GpuSolver {
   // S x without stored S tiles (Problem::implicit_schur): per subdomain
   // A_GG x - A_GI A_II^-1 A_IG x through the local stencils and one interior sweep
   void schur_matvec_implicit(const double* x, double* y);
+  // S x over this rank's subdomains (no exchange), optional x.(S x) partial dot
+  void s_product(const double* x, double* y, const double* dot_with, double* dot_out);
   void apply_nn2(const double* r, double* z);                           // K2-K4
   // make_preconditioner(schur, kind) (dd.cpp:159-253): 0 nn2, 1 nn1, 2 lumped
   // (nn1 / lumped need Problem::precond == kind: their local operators are
@@ -325,6 +327,9 @@ class GpuSolver {
   double* h_fused_ = nullptr;  // pinned: persistent PCG outputs [4 ints as doubles' room][history]
   DBuf<int> fused_out_;
   RangeBufs rs_, rq_, rp_;
+  bool walk_ok_ = false;  // ranges built: the host-driven loop uses walk_kernel
+  void walk_pack(int which, const double* x);  // 0: S, 1: Q
+  struct RangePack range_pack(int which) const;
   // Psi_s^T as rectangular tiles for the persistent kernel (pcg_fused.cu)
   DBuf<double> psi_tiles_;
   DBuf<long long> psi_toff_;

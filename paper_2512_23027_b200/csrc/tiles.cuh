@@ -98,4 +98,55 @@ __device__ __forceinline__ double tile_reduce(const double* __restrict__ rowpart
   return s;
 }
 
+// A tile pack walked in contiguous tile ranges, one per CTA.  Two kinds:
+//  * symmetric (S_s, Q_s): lower 64x64 tiles (I, J <= I), row-major over the
+//    tiles of a matrix, diagonal tiles full, 32 KB each;
+//  * rectangular (Psi_s^T): tiles (I, J), I over 64-wide corner-column chunks,
+//    J over 64-row blocks of the remaining dofs, row-major; tile (I, J) is the
+//    column-major 64 x w chunk of Psi_s (w = the chunk's valid columns, rows
+//    past r_s stored as zeros), i.e. row-major Psi^T rows of stride 64, w x 512
+//    bytes, so one bulk copy moves only stored data.
+// A CTA keeps the local input vector of its current matrix and a local
+// accumulator in shared memory, adds every tile's row and column products
+// into it (tile_acc), and at a matrix boundary writes the accumulator as its
+// partial of that matrix: y_s = sum over the CTAs covering s of their
+// partials, in CTA order.  Local vectors: symmetric [64 nt]; rectangular
+// [64 nI (corner chunks) | 64 nJ (remaining-dof blocks)].
+struct RangePack {
+  const double* tiles;
+  const long long* toff;      // per tile: offset in doubles (null: t * 4096)
+  const int* tbytes;          // per tile: bytes (null: 32 KB)
+  const int* nI;              // per matrix: tile rows (symmetric: tiles per side)
+  const int* nJ;              // per matrix: tile columns (rectangular only)
+  int rect;
+  const long long* t_first;   // [G + 1] first tile of each CTA's range
+  const int4* start;          // [G] {matrix, I, J} of each CTA's first tile
+  const int* c0;              // per matrix: first CTA covering it
+  const int* ncta;            // per matrix: CTAs covering it
+  const long long* pbase;     // per matrix: offset of its partials in part
+  double* part;               // partials [pbase[s] + (c - c0[s]) len_s + i]
+};
+
+// sum of the n CTA partials p[k len] of one local entry, k ascending
+__device__ __forceinline__ double partial_sum(const double* p, int len, int n) {
+  double y = 0.0;
+  int k = 0;
+  for (; k + 4 <= n; k += 4) {
+    const double a = __ldcg(p + (long long)k * len), b = __ldcg(p + (long long)(k + 1) * len),
+                 c = __ldcg(p + (long long)(k + 2) * len), d = __ldcg(p + (long long)(k + 3) * len);
+    y += a, y += b, y += c, y += d;
+  }
+  for (; k < n; ++k) y += __ldcg(p + (long long)k * len);
+  return y;
+}
+// y_s[i] from the partials of the CTAs covering symmetric matrix s
+__device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i) {
+  return partial_sum(P.part + P.pbase[s] + i, kTile * P.nI[s], P.ncta[s]);
+}
+// Psi^T x (corner part, i < 64 nI) or Psi x (remaining-dof part, offset 64 nI)
+// of rectangular matrix s
+__device__ __forceinline__ double rect_reduce(const RangePack& P, int s, int i) {
+  return partial_sum(P.part + P.pbase[s] + i, kTile * (P.nI[s] + P.nJ[s]), P.ncta[s]);
+}
+
 }  // namespace sgw
