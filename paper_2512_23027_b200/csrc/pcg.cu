@@ -436,16 +436,33 @@ __global__ void nn2_local_kernel(double* __restrict__ li, const long long* __res
   }
 }
 
-// nn2_local_kernel on the CTA partials of the Q walk
-__global__ void nn2_local_range_kernel(double* __restrict__ li, const long long* __restrict__ lioff,
-                                       const int* __restrict__ ip_off, const int* __restrict__ pkind,
-                                       const int* __restrict__ ng, const int* __restrict__ nr,
-                                       const int* __restrict__ nc, int nt, const RangePack Pq,
-                                       const double* __restrict__ Psi, const long long* __restrict__ psioff,
-                                       const double* __restrict__ uc, const int* __restrict__ corner_pos_flat,
-                                       const int* __restrict__ cp_off, int n_corner, int has_coarse) {
+// d_s = f_c - Psi_s^T f_r from the Psi^T walk's corner partials (c-space, padded per subdomain)
+__global__ void psi_t_range_kernel(const RangePack Pp, const double* __restrict__ fc, const long long* __restrict__ coff,
+                                   const int* __restrict__ ncs, double* __restrict__ dsub, int ns) {
   const int s = blockIdx.y;
-  const int a = ng[s] * nt, rsz = nr[s] * nt, ncs = nc[s];
+  if (s >= ns) return;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncs[s]; c += gridDim.x * blockDim.x)
+    dsub[coff[s] + c] = fc[coff[s] + c] - rect_reduce(Pp, s, c);
+}
+// B_s u_c per subdomain (c-space, compact)
+__global__ void ucl_kernel(const double* __restrict__ uc, const long long* __restrict__ coff,
+                           const int* __restrict__ nc, const int* __restrict__ corner_pos_flat,
+                           const int* __restrict__ cp_off, int nt, int n_corner, double* __restrict__ ucl) {
+  const int s = blockIdx.y;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nt * nc[s]; c += gridDim.x * blockDim.x) {
+    const int j = c / nc[s], cc = c % nc[s];
+    ucl[coff[s] + c] = uc[j * n_corner + corner_pos_flat[cp_off[s] + cc]];
+  }
+}
+// z_s from the Q walk and the second Psi^T walk (remaining-dof part of its partials)
+__global__ void nn2_local_walk_kernel(double* __restrict__ li, const long long* __restrict__ lioff,
+                                      const int* __restrict__ ip_off, const int* __restrict__ pkind,
+                                      const int* __restrict__ ng, const int* __restrict__ nr,
+                                      const int* __restrict__ nc, int nt, const RangePack Pq, const RangePack Pp,
+                                      const double* __restrict__ ucl, const long long* __restrict__ coff,
+                                      int has_coarse) {
+  const int s = blockIdx.y;
+  const int a = ng[s] * nt;
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < a; f += gridDim.x * blockDim.x) {
     const int j = f / ng[s], p = f % ng[s];
     const int k = pkind[ip_off[s] + p];
@@ -453,15 +470,9 @@ __global__ void nn2_local_range_kernel(double* __restrict__ li, const long long*
     if (k >= 0) {
       const int ar = j * nr[s] + k;
       v = range_reduce(Pq, s, ar);
-      if (has_coarse) {
-        const double* P = Psi + psioff[s] + ar;
-        for (int jc = 0; jc < nt; ++jc)
-          for (int cc = 0; cc < ncs; ++cc)
-            v -= P[(long long)(jc * ncs + cc) * rsz] * uc[jc * n_corner + corner_pos_flat[cp_off[s] + cc]];
-      }
+      if (has_coarse) v -= rect_reduce(Pp, s, kTile * Pp.nI[s] + ar);
     } else {
-      const int cc = -1 - k;
-      v = has_coarse ? uc[j * n_corner + corner_pos_flat[cp_off[s] + cc]] : 0.0;
+      v = has_coarse ? ucl[coff[s] + (long long)j * nc[s] + (-1 - k)] : 0.0;
     }
     li[lioff[s] + f] = v;
   }
@@ -472,9 +483,35 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
   nn2_gather_kernel<<<red_grid(nr_tot + nc_tot), 256, 0, st_>>>(r, r_gidx.p, r_w.p, r_x.p, nr_tot, c_gidx.p, c_w.p,
                                                                  c_f.p, nc_tot);
   SGW_LAUNCHED();
-  if (walk_ok_) walk_pack(1, r_x.p);
-  else symv(Qp, r_x.p, nullptr);
   const bool has_coarse = NC > 0;
+  if (walk_ok_) {  // Q, Psi^T f_r, F_cc^-1, Psi u_c as tile walks (pcg_fused.cu)
+    walk_pack(1, r_x.p);
+    if (has_coarse) {
+      walk_psi(1, r_x.p);
+      psi_t_range_kernel<<<dim3(cdiv(NT * 4, 128), NS), 128, 0, st_>>>(psi_pack(), c_f.p, d_coff.p, psi_ncs_.p, c_d.p,
+                                                                     NS);
+      SGW_LAUNCHED();
+      coarse_assemble_kernel<<<cdiv(NC, 256), 256, 0, st_>>>(c_d.p, d_coff.p, cinv_cnt.p, cinv_s.p, cinv_c.p, nc_d.p,
+                                                             G.n_corner, NC, dcoarse.p);
+      SGW_LAUNCHED();
+      allreduce(dcoarse.p, NC);
+      symv_dense_kernel<<<cdiv(NC, 8), 256, 0, st_>>>(Finv.p, dcoarse.p, ucoarse.p, NC);
+      SGW_LAUNCHED();
+      ucl_kernel<<<dim3(cdiv(NT * 4, 128), NS), 128, 0, st_>>>(ucoarse.p, d_coff.p, nc_d.p, cpos_flat_.p, cp_off_.p,
+                                                             NT, G.n_corner, ucl_.p);
+      SGW_LAUNCHED();
+      walk_psi(2, ucl_.p);
+    }
+    nn2_local_walk_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
+        li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, range_pack(1), psi_pack(), ucl_.p,
+        d_coff.p, has_coarse ? 1 : 0);
+    SGW_LAUNCHED();
+    scatter_li(li_y.p, z, true, nullptr, nullptr);
+    allreduce(z, NG);
+    ++T.nn2s;
+    return;
+  }
+  symv(Qp, r_x.p, nullptr);
   if (has_coarse) {
     psi_t_kernel<<<dim3(cdiv(NT * 4, 8), NS), 256, 0, st_>>>(Psi.p, d_psioff.p, r_x.p, d_roff.p, c_f.p, d_coff.p,
                                                               c_d.p, nr_d.p, nc_d.p, NT, NS);
@@ -486,12 +523,7 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
     symv_dense_kernel<<<cdiv(NC, 8), 256, 0, st_>>>(Finv.p, dcoarse.p, ucoarse.p, NC);
     SGW_LAUNCHED();
   }
-  if (walk_ok_)
-    nn2_local_range_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
-        li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, range_pack(1), Psi.p, d_psioff.p,
-        ucoarse.p, cpos_flat_.p, cp_off_.p, G.n_corner, has_coarse ? 1 : 0);
-  else
-    nn2_local_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
+  nn2_local_kernel<<<dim3(cdiv(NT * 4 * (G.mx + G.my), 256), NS), 256, 0, st_>>>(
         li_y.p, Sp.d_xoff.p, ip_off.p, pkind_.p, ng_d.p, nr_d.p, nc_d.p, NT, Qp.rowpart.p, Qp.colpart.p,
         Qp.d_tile_base.p, Qp.d_ntile.p, Psi.p, d_psioff.p, ucoarse.p, cpos_flat_.p, cp_off_.p, G.n_corner,
         has_coarse ? 1 : 0);

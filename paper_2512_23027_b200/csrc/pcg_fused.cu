@@ -570,7 +570,8 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
 // PCG of sharded runs: every CTA walks its range of P on the local vector x
 // (layout xoff) and writes its partials; consumers use range_reduce.
 __global__ void __launch_bounds__(256) walk_kernel(RangePack P, const double* __restrict__ x,
-                                                   const long long* __restrict__ xoff, int nst, int maxlen) {
+                                                   const long long* __restrict__ xoff, int nst, int maxlen,
+                                                   int xmode, const int* __restrict__ ncs) {
   __shared__ Smem sm;
   __shared__ unsigned long long ring_bar[kMaxRing];
   Ring R{dyn_smem, ring_bar, nst, 0, 0, 0};
@@ -582,7 +583,14 @@ __global__ void __launch_bounds__(256) walk_kernel(RangePack P, const double* __
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  range_phase(R, 1, P, nullptr, xs, xs + maxlen, sm, [&](int s, int i) { return __ldg(x + xoff[s] + i); });
+  // xmode 0: x[xoff[s] + i]; Psi^T tiles: 1 = [0 | f_r] (xoff = r-space offsets),
+  // 2 = [B_s u_c | 0] (xoff = c-space offsets, ncs = corner columns per matrix)
+  range_phase(R, 1, P, nullptr, xs, xs + maxlen, sm, [&](int s, int i) {
+    if (xmode == 0) return __ldg(x + xoff[s] + i);
+    const int o = i - kTile * P.nI[s];
+    if (xmode == 1) return o >= 0 ? __ldcg(x + xoff[s] + o) : 0.0;
+    return i < ncs[s] ? __ldcg(x + xoff[s] + i) : 0.0;
+  });
   if (threadIdx.x == 0)
     for (int c = R.consumed; c < R.issued; ++c) mb_wait(&R.full[c % R.nst], (c / R.nst) & 1);
   __syncthreads();
@@ -719,17 +727,22 @@ void GpuSolver::setup_fused_pcg() {
                                 (int)fused_smem_));
   rs_.plan(Sp.tile_base, Sp.ntile, {}, fused_grid_);
   rq_.plan(Qp.tile_base, Qp.ntile, {}, fused_grid_);
-  walk_ok_ = true;  // the host-driven loop streams S / Q with walk_kernel too
+  walk_ok_ = true;  // the host-driven loop streams S / Q / Psi with walk_kernel too
+  build_psi_tiles();
+  {
+    std::vector<int> ncs(NS);
+    for (int s = 0; s < NS; ++s) ncs[s] = NT * nc_[s];
+    psi_ncs_.upload(ncs);
+  }
+  ucl_.alloc(std::max<long long>(1, coff_.back())), ucl_.zero(st_);
   if (comm_) {      // sharded: the host-driven loop with a sum over ranks after each scatter
     use_fused_ = false;
     return;
   }
-  build_psi_tiles();
   fused_part_.alloc(size_t(8) * fused_grid_);
   fused_out_.alloc(4);
   fused_hist_.alloc(P.max_iter + 8);
   for (DBuf<double>* b : {&li_z_, &li_p_, &li_xx_}) b->alloc(Sp.xlen), b->zero(st_);  // padding stays 0
-  ucl_.alloc(std::max<long long>(1, coff_.back())), ucl_.zero(st_);
   const char* e = std::getenv("SGW_PCG");
   use_fused_ = !(e && std::string(e) == "host");
 }
@@ -741,12 +754,28 @@ RangePack GpuSolver::range_pack(int which) const {
                    rb.ncta.p, rb.pbase.p, rb.part.p};
 }
 
+// the Psi^T tile walk for the host-driven NN2: pass 1 on [0 | f_r], pass 2 on [B_s u_c | 0]
+void GpuSolver::walk_psi(int pass, const double* x) {
+  if (!rp_.t_first.p) return;
+  const RangePack P{psi_tiles_.p, psi_toff_.p, psi_tbytes_.p, psi_dnI_.p, psi_dnJ_.p, 1, rp_.t_first.p, rp_.start.p,
+                    rp_.c0.p, rp_.ncta.p, rp_.pbase.p, rp_.part.p};
+  walk_kernel<<<fused_grid_, 256, fused_smem_, st_>>>(P, x, pass == 1 ? d_roff.p : d_coff.p, fused_nst_, fused_maxlen_,
+                                                      pass, psi_ncs_.p);
+  SGW_LAUNCHED();
+}
+
+RangePack GpuSolver::psi_pack() const {
+  return RangePack{psi_tiles_.p, psi_toff_.p, psi_tbytes_.p, psi_dnI_.p, psi_dnJ_.p, 1, rp_.t_first.p, rp_.start.p,
+                   rp_.c0.p, rp_.ncta.p, rp_.pbase.p, rp_.part.p};
+}
+
 void GpuSolver::walk_pack(int which, const double* x) {
   const TilePack& tp = which == 0 ? Sp : Qp;
   if (!tp.n_tiles) return;
   cudaEvent_t e0;
   KP.begin(which == 0 ? K_SYMV_S : K_SYMV_Q, st_, &e0);
-  walk_kernel<<<fused_grid_, 256, fused_smem_, st_>>>(range_pack(which), x, tp.d_xoff.p, fused_nst_, fused_maxlen_);
+  walk_kernel<<<fused_grid_, 256, fused_smem_, st_>>>(range_pack(which), x, tp.d_xoff.p, fused_nst_, fused_maxlen_, 0,
+                                                      nullptr);
   SGW_LAUNCHED();
   KP.end(st_);
 }

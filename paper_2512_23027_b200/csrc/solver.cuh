@@ -329,6 +329,9 @@ class GpuSolver {
   RangeBufs rs_, rq_, rp_;
   bool walk_ok_ = false;  // ranges built: the host-driven loop uses walk_kernel
   void walk_pack(int which, const double* x);  // 0: S, 1: Q
+  void walk_psi(int pass, const double* x);     // Psi^T tiles: 1 on [0 | f_r], 2 on [B_s u_c | 0]
+  struct RangePack psi_pack() const;
+  DBuf<int> psi_ncs_;                            // NT nc_s per subdomain
   struct RangePack range_pack(int which) const;
   // Psi_s^T as rectangular tiles for the persistent kernel (pcg_fused.cu)
   DBuf<double> psi_tiles_;
