@@ -185,7 +185,7 @@ __device__ __forceinline__ void issue_k_now(const SgOpArgs& A, int q, int nst) {
 // mid-tile), then every warp waits for its chunk
 #define STAGE_IN(ch)                                                   \
   if (warp == 0) {                                                     \
-    issue_k(A, s + S - 2, nst, lane);                                  \
+    issue_k(A, s + AHEAD, nst, lane);                                  \
     if ((ch) == NCHUNK / 2 && t + 1 < mytiles) load_xm(A, t + 1, lane); \
     __syncwarp();                                                      \
   }                                                                    \
@@ -249,7 +249,7 @@ extern "C" __global__ void __launch_bounds__(NTHR, CPS) sgop_kernel(const SgOpAr
   }
 #else
   if (warp == 0) {
-    for (int q = 0; q < S - 2; ++q) issue_k(A, q, nst, lane);
+    for (int q = 0; q < AHEAD; ++q) issue_k(A, q, nst, lane);
     load_xm(A, 0, lane);
     __syncwarp();
   }
@@ -595,7 +595,9 @@ std::string sgop_source(int NT, int NIN, const TensorHost& T, SgOpJit* J) {
   if (const char* e = std::getenv("SGW_SGOP_PF")) pf = std::max(0, std::atoi(e));  // tuning hook
   int ef = 1;
   if (const char* e = std::getenv("SGW_SGOP_EF")) ef = std::atoi(e);  // tuning hook
-  std::string src = "#define CPS " + std::to_string(J->cps) + "\n#define EF " + std::to_string(ef) + "\n#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
+  int ahead = J->S - 2;  // chunks in flight ahead of the one being consumed (warp 0 refills)
+  if (const char* e = std::getenv("SGW_SGOP_AHEAD")) ahead = std::max(1, std::min(J->S - 1, std::atoi(e)));  // tuning hook
+  std::string src = "#define AHEAD " + std::to_string(ahead) + "\n#define CPS " + std::to_string(J->cps) + "\n#define EF " + std::to_string(ef) + "\n#define PF " + std::to_string(pf) + "\n#define PROD " + std::to_string(J->prod) + "\n#define LA " + std::to_string(J->la) + "\n#define XG " + std::to_string(int(J->xg)) + "\n" + std::string("#define RED_ALIAS ") + (J->red_alias ? "1" : "0") + "\n#define NCOEF " + std::to_string(std::max<size_t>(1, J->coef.size())) +
                     "\n#define NT " + std::to_string(NT) + "\n#define NIN " + std::to_string(NIN) +
                     "\n#define R " + std::to_string(R) + "\n#define G " + std::to_string(G) + "\n#define IC " +
                     std::to_string(IC) + "\n#define S " + std::to_string(J->S) + "\n#define NCHUNK " +
