@@ -782,13 +782,13 @@ void GpuSolver::walk_pack(int which, const double* x) {
 
 int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vector<double>* hist) {
   pcg_fused_launch(b, x);
-  SGW_CUDA(cudaEventSynchronize(ev_[1]));
+  SGW_CUDA(cudaEventSynchronize(ev_[6]));
   return pcg_fused_finish(converged, hist);
 }
 
 // Asynchronous half: the kernel, then its outputs (iterations, convergence,
 // residual history) copied into pinned host memory; pcg_fused_finish reads them
-// once the stream has passed ev_[1] (step() launches the recovery first).
+// once the stream has passed ev_[6] (step() launches the recovery first).
 void GpuSolver::pcg_fused_launch(const double* b, double* x) {
   if (!h_fused_) SGW_CUDA(cudaMallocHost(&h_fused_, (4 + fused_hist_.n) * sizeof(double)));
   cudaEventRecord(ev_[0], st_);
@@ -818,9 +818,10 @@ void GpuSolver::pcg_fused_launch(const double* b, double* x) {
   SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_fused_kernel, dim3(fused_grid_), dim3(256), args,
                                        fused_smem_, st_));
   SGW_LAUNCHED();
+  cudaEventRecord(ev_[1], st_);  // end of the solve (the PCG time)
   SGW_CUDA(cudaMemcpyAsync(h_fused_, fused_out_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st_));
   SGW_CUDA(cudaMemcpyAsync(h_fused_ + 4, fused_hist_.p, fused_hist_.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  cudaEventRecord(ev_[1], st_);
+  cudaEventRecord(ev_[6], st_);  // outputs in pinned memory
 }
 
 int GpuSolver::pcg_fused_finish(bool* converged, std::vector<double>* hist) {
