@@ -395,7 +395,7 @@ void GpuSolver::build_coupling_blocks() {
   }
   // local-force stiffness blocks of the interface list (skipped when large)
   const size_t fb = (size_t)n_ilist_ * 5 * NT * NT;
-  if (fb > 0 && fb * sizeof(double) <= (size_t(2) << 30)) {
+  if (fb > 0 && fb * sizeof(double) <= (size_t(4) << 30)) {
     frc_blk_.alloc(fb);
     force_block_kernel<<<(unsigned)(n_ilist_ * 5), 32, 0, st_>>>(local_args(), ilist_.p, frc_blk_.p);
     SGW_LAUNCHED();
