@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   double* zv = CS > 1 ? red + VL : red;        // D^-1 output, owned rows
   double* slots = zv + VL;                     // [source rank][owned row] partials (CS > 1)
   double* tpart = CS > 1 ? slots + CS * L.slot_len : red + VL;  // band partials [rank segments]
+  // second half of the CTA reduction tree, 16-byte aligned (double2 accesses)
+  double* red2 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tpart + L.tpart_len) + 15) & ~uintptr_t(15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* Fs = F + (long long)s * L.per_sub;
   double* xs = x + (long long)s * H * B;
@@ -358,22 +360,28 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
         }
         e = en;
       }
-      // CTA sum in warp order, then to the row owners
-#pragma unroll 1
-      for (int w = 0; w < kSwWarps; ++w) {
-        if (warp == w) {
+      // CTA sum as a fixed tree (w0 + w1) + (w2 + w3): odd warps store, even
+      // warps add theirs, then one pass adds the two halves; then to the owners
+      static_assert(kSwWarps == 4, "the CTA reduction tree assumes four consumer warps");
+      {
+        double* half = (warp >> 1) ? red2 : red;
+        if (warp & 1) {
+#pragma unroll
+          for (int q = 0; q < NBM; ++q)
+            if (q < nb) reinterpret_cast<double2*>(half + q * kTile)[lane] = make_double2(cx[q], cy[q]);
+        }
+        consumers_sync();
+        if (!(warp & 1)) {
 #pragma unroll
           for (int q = 0; q < NBM; ++q)
             if (q < nb) {
-              double2* dq = reinterpret_cast<double2*>(red + q * kTile) + lane;
-              double2 v = make_double2(cx[q], cy[q]);
-              if (w > 0) {
-                const double2 o = *dq;
-                v.x = o.x + v.x, v.y = o.y + v.y;
-              }
-              *dq = v;
+              double2* dq = reinterpret_cast<double2*>(half + q * kTile) + lane;
+              const double2 o = *dq;
+              *dq = make_double2(cx[q] + o.x, cy[q] + o.y);
             }
         }
+        consumers_sync();
+        for (int i = tid; i < nb * kTile; i += kSwWarps * 32) red[i] += red2[i];
         consumers_sync();
       }
       if (CS > 1) {
@@ -547,7 +555,7 @@ static SweepFn sweep_fn(int cs, int nbm) {
 }
 
 static size_t smem_bytes(int stages, int VL, int CS, int slot_len, int tpart_len) {
-  const size_t vec = 2 * (size_t)VL + (CS > 1 ? (size_t)VL + (size_t)CS * slot_len : 0) + (size_t)tpart_len;
+  const size_t vec = 3 * (size_t)VL + (CS > 1 ? (size_t)VL + (size_t)CS * slot_len : 0) + (size_t)tpart_len + 2;
   return (size_t)stages * kTileD * 8 + 256 + vec * 8;
 }
 
