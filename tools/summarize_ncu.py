@@ -62,7 +62,10 @@ def launch_shares(tag):
 def full_captures(tag, config):
     summary_path = os.path.join(PROF, "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
-    for rep in sorted(glob.glob(os.path.join(OUT, "prof_*.ncu-rep"))):
+    # only the captures tools/gpu_round.sh makes for this config (other prof_*
+    # files, e.g. C3 captures from tools/ncu_one.sh, must not feed the C2 traffic)
+    reps = [os.path.join(OUT, f"prof_{n}.ncu-rep") for n in ("sweep", "pcg", "sgop")]
+    for rep in [r for r in reps if os.path.exists(r)]:
         name = os.path.basename(rep)[5:-8]
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
