@@ -53,7 +53,8 @@ typedef struct sgw_solver sgw_solver;
 
 /* SgSolver constructor arguments.  The mesh is build_unit_square_mesh(nx, ny)
  * (src/mesh.cpp:15-58) and the partition partition_structured(mesh, px, py)
- * (src/partition.cpp:48-133); the GPU path requires px | nx and py | ny. */
+ * (src/partition.cpp:48-133), floor-division cell ownership: px need not
+ * divide nx (ragged blocks of two widths are supported).                   */
 typedef struct sgw_problem {
   int nx, ny, px, py;
   int n_input;          /* CoefficientField terms                              */
@@ -140,6 +141,12 @@ int sgw_apply_precond(sgw_solver* s, int kind, const double* r, double* z);
 /* PCG on S u = rhs with NN2 (src/pcg.cpp:7-50).  history: >= max_iter + 2. */
 int sgw_pcg(sgw_solver* s, const double* rhs, double* x, int* iterations, int* converged,
             double* residual_history, int history_cap);
+/* Verification hook (test_dd.cpp:77-96 at full size): dense copy of global
+ * subdomain `sub`'s local operator, column-major: which 0 = S_s (a x a),
+ * 1 = S_rr^-1 (r x r), 2 = Psi_s = S_rr^-1 S_rc (r x c).  dims (optional) =
+ * {a, r, c}; gmap (optional, a entries) = make_flat_maps' gmap (dd.cpp:78-96).
+ * out = gmap = NULL: sizes only.  The subdomain must be owned by this rank. */
+int sgw_local_block(sgw_solver* s, int sub, int which, double* out, long long* gmap, long long* dims);
 /* F_cc (n_corner flat)^2, column-major. */
 int sgw_coarse_operator(sgw_solver* s, double* out);
 

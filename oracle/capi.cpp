@@ -183,6 +183,27 @@ int orc_coarse_operator(void* hp, double* out) {
   return 0;
 }
 
+// pcg(matvec, apply_nn2 / make_preconditioner, rhs, tol, max_iter) on the
+// solver's Schur system (src/pcg.cpp:7-50); hist: >= max_iter + 2 entries.
+int orc_pcg(void* hp, const double* rhs, double* x, int* iters, int* converged, double* hist, int hist_cap,
+            int precond, double tol, int max_iter) {
+  try {
+    const SgSolver& s = *static_cast<Handle*>(hp)->solver;
+    const SchurSystem& sys = s.schur();
+    const Vec b(rhs, rhs + sys.n_global);
+    PcgReport rep;
+    const Vec xv = pcg([&](const Vec& v) { return sys.matvec(v); }, [&](const Vec& v) { return sys.apply(precond, v); },
+                       b, tol, max_iter, &rep);
+    std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+    *iters = rep.iterations;
+    *converged = rep.converged ? 1 : 0;
+    for (int i = 0; i < hist_cap; ++i) hist[i] = i < int(rep.residual_history.size()) ? rep.residual_history[i] : -1.0;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // Local Schur S_s (column-major a x a) and its flat gmap.
 int orc_local_schur(void* hp, int s, double* S, long long* gmap, long long* a_out) {
   const SgSolver& sv = *static_cast<Handle*>(hp)->solver;
@@ -275,6 +296,67 @@ int orc_single_block_nn2(int n, const double* a, const double* r, double* z, dou
     return fail(e);
   }
 }
+
+// One subdomain's local operators without building the whole solver
+// (SgSolver::local_blocks): for checking the GPU tiles at sizes where the full
+// oracle does not fit in host memory.  sizes_out = {a, r, c}.
+int orc_local_blocks_create(int nx, int ny, int px, int py, int n_in, const double* coeff, int n_out, int n_ent,
+                            const int* ei, const int* ej, const int* ek, const double* ev, double density,
+                            double alpha0, double alpha1, double gamma, double zeta, double dt, int s, int threads,
+                            long long* sizes_out, void** out) {
+  try {
+    const Mesh mesh = build_unit_square_mesh(nx, ny);
+    const Partition part = partition_structured(mesh, px, py);
+    CoefficientField f;
+    for (int i = 0; i < n_in; ++i)
+      f.terms.emplace_back(coeff + size_t(i) * mesh.n_nodes(), coeff + size_t(i + 1) * mesh.n_nodes());
+    TripleTensor t;
+    t.n_input = n_in;
+    t.n_output = n_out;
+    t.by_input.resize(n_in);
+    for (int c = 0; c < n_ent; ++c) t.by_input.at(ei[c]).push_back({ej[c], ek[c], ev[c]});
+    NewmarkParams p;
+    p.gamma = gamma, p.zeta = zeta, p.dt = dt;
+    auto ls = std::make_unique<LocalSchur>(SgSolver::local_blocks(mesh, part, f, t, density, alpha0, alpha1, p, s,
+                                                                  threads));
+    sizes_out[0] = ls->n_flat();
+    sizes_out[1] = Index(ls->r_idx.size());
+    sizes_out[2] = Index(ls->c_idx.size());
+    *out = ls.release();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// S (a x a column-major) and gmap (a); qv = S_rr^{-1} v for m vectors v
+// (r x m column-major); psi = S_rr^{-1} S_rc (r x c column-major).  Any
+// output may be null.
+int orc_local_blocks_get(void* hp, double* S, long long* gmap, const double* v, int m, double* qv, double* psi) {
+  try {
+    const LocalSchur& ls = *static_cast<LocalSchur*>(hp);
+    const Index r = Index(ls.r_idx.size()), c = Index(ls.c_idx.size());
+    if (S) std::memcpy(S, ls.S.a.data(), sizeof(double) * ls.S.a.size());
+    if (gmap)
+      for (Index k = 0; k < ls.n_flat(); ++k) gmap[k] = ls.gmap[k];
+    if (qv)
+      for (int q = 0; q < m; ++q) {
+        std::memcpy(qv + size_t(q) * r, v + size_t(q) * r, sizeof(double) * r);
+        ls.Srr_llt.solve_in_place(qv + size_t(q) * r);
+      }
+    if (psi)
+      parallel_for(c, 8, [&](int b) {
+        double* col = psi + size_t(b) * r;
+        for (Index a = 0; a < r; ++a) col[a] = ls.S_rc(a, b);
+        ls.Srr_llt.solve_in_place(col);
+      });
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+void orc_local_blocks_destroy(void* hp) { delete static_cast<LocalSchur*>(hp); }
 
 void orc_timing(void* hp, double* out) {
   const SgSolver& s = *static_cast<Handle*>(hp)->solver;

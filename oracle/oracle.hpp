@@ -258,6 +258,9 @@ class SgSolver {  // include/sgwave/sg.hpp:43-98
   Vec apply_block_mass(const Vec& flat) const;
   Vec apply_block_stiffness(const Vec& flat) const;
   Vec apply_block_transient(const Vec& flat) const;
+  static LocalSchur local_blocks(const Mesh& mesh, const Partition& part, const CoefficientField& coeff,
+                                 const TripleTensor& tensor, double density, double alpha0, double alpha1,
+                                 NewmarkParams params, int s, int threads);
 
   // per-phase timing of the last run (seconds)
   double t_setup = 0.0, t_pcg = 0.0, t_steps = 0.0;
@@ -277,6 +280,17 @@ class SgSolver {  // include/sgwave/sg.hpp:43-98
     std::vector<Index> perm;  // term-major flat interior index -> band index
     bool has_interior = false;
   };
+  struct Ctx {
+    const Mesh& mesh;
+    const Partition& part;
+    const DirichletReduction& red;
+    const InterfaceLayout& layout;
+    const CoefficientField& coeff;
+    const TripleTensor& tensor;
+    double density, mass_scale, stiff_scale;
+    int nt, precond;
+  };
+  static void build_local(const Ctx& cx, int s, int panel_threads, Local& loc, LocalSchur& ls);
   void assemble_subdomains();
   Vec local_force(int s, const Vec& um, const Vec& uc, const Vec& f_next) const;
   Vec step_rhs_and_solve(const StateTriple& st, const Vec& f_next, PcgReport* rep);

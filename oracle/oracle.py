@@ -53,6 +53,15 @@ def lib():
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_residual_history.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int]
         L.orc_timing.argtypes = [C.c_void_p, _dp]
+        L.orc_local_blocks_create.argtypes = ([C.c_int] * 5 + [_dp, C.c_int, C.c_int, _ip, _ip, _ip, _dp]
+                                              + [C.c_double] * 6 + [C.c_int, C.c_int,
+                                                                    np.ctypeslib.ndpointer(dtype=np.int64),
+                                                                    C.POINTER(C.c_void_p)])
+        L.orc_local_blocks_get.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                           C.c_void_p]
+        L.orc_pcg.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_int, C.c_int,
+                              C.c_double, C.c_int]
+        L.orc_local_blocks_destroy.argtypes = [C.c_void_p]
         L.orc_single_block_nn2.argtypes = [C.c_int, _dp, _dp, _dp, C.c_double, C.POINTER(C.c_int)]
         _lib = L
     return _lib
@@ -156,6 +165,7 @@ class SgSolver:
                                        tensor.i, tensor.j, tensor.k, tensor.v, density, alpha0, alpha1, gamma,
                                        zeta, dt, tol, max_iter, threads, PRECONDS[precond], C.byref(h)))
         self._h = h
+        self.tol = tol
         s = np.zeros(6, np.int64)
         lib().orc_solver_sizes(self._h, s)
         self.n_dofs, self.n_terms, self.n_iface, self.n_corner, self.n_global, direct = (int(v) for v in s)
@@ -202,6 +212,17 @@ class SgSolver:
         _check(lib().orc_schur_apply(self._h, which, r, z))
         return z
 
+    def pcg(self, rhs, tol=None, max_iter=500, precond="nn2"):
+        """pcg(matvec, precond, rhs, tol, max_iter) (src/pcg.cpp:7-50) -> (x, report dict)."""
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.zeros(self.n_global)
+        it, cv = C.c_int(), C.c_int()
+        hist = np.zeros(max_iter + 2)
+        _check(lib().orc_pcg(self._h, rhs, x, C.byref(it), C.byref(cv), hist, len(hist), PRECONDS[precond],
+                             self.tol if tol is None else tol, max_iter))
+        h = hist[hist >= 0]
+        return x, {"iterations": it.value, "converged": bool(cv.value), "residual_history": h}
+
     def coarse_operator(self):
         out = np.zeros(self.n_corner * self.n_terms * self.n_corner * self.n_terms)
         lib().orc_coarse_operator(self._h, out)
@@ -242,6 +263,46 @@ class SgSolver:
         buf = np.zeros(1024)
         n = lib().orc_residual_history(self._h, k, buf, len(buf))
         return buf[:n].copy()
+
+
+class LocalBlocks:
+    """One subdomain's S_s, S_rr^{-1} and Psi_s = S_rr^{-1} S_rc built alone
+    (SgSolver::local_blocks, src/sg.cpp:186-246 + src/dd.cpp:112-120), for
+    per-subdomain checks at sizes where the whole oracle exceeds host RAM."""
+
+    def __init__(self, nx, ny, px, py, coeff, tensor: Tensor, s, density=1.0, alpha0=0.5445, alpha1=0.0174,
+                 dt=1e-3, gamma=0.5, zeta=0.25, threads=None):
+        coeff = np.ascontiguousarray(coeff, np.float64)
+        sz = np.zeros(3, np.int64)
+        h = C.c_void_p()
+        _check(lib().orc_local_blocks_create(nx, ny, px, py, coeff.shape[0], coeff, tensor.n_output, len(tensor.v),
+                                             tensor.i, tensor.j, tensor.k, tensor.v, density, alpha0, alpha1, gamma,
+                                             zeta, dt, s, threads or os.cpu_count() or 1, sz, C.byref(h)))
+        self._h = h
+        self.a, self.r, self.c = (int(v) for v in sz)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_local_blocks_destroy(self._h)
+            self._h = None
+
+    def schur(self):
+        S = np.zeros(self.a * self.a)
+        g = np.zeros(self.a, np.int64)
+        _check(lib().orc_local_blocks_get(self._h, _ptr(S), _ptr(g), None, 0, None, None))
+        return S.reshape(self.a, self.a).T.copy(), g
+
+    def srr_solve(self, V):
+        """S_rr^{-1} V for V of shape (r, m)."""
+        Vt = np.ascontiguousarray(np.asarray(V, np.float64).T)
+        out = np.zeros_like(Vt)
+        _check(lib().orc_local_blocks_get(self._h, None, None, _ptr(Vt), Vt.shape[0], _ptr(out), None))
+        return out.T.copy()
+
+    def psi(self):
+        P = np.zeros(self.r * self.c)
+        _check(lib().orc_local_blocks_get(self._h, None, None, None, 0, None, _ptr(P)))
+        return P.reshape(self.c, self.r).T.copy()
 
 
 def single_block_nn2(a, r, tol=1e-10):

@@ -461,98 +461,133 @@ void SgSolver::assemble_subdomains() {
   schur_.n_corner = nt * layout_.n_corner();
   schur_.n_threads = opt_.threads;
   schur_.locals.resize(ns);
-  parallel_for(ns, opt_.threads, [&](int s) {
-    const SubdomainDofs& sd = layout_.sub[s];
-    Local& loc = locals_[s];
-    assemble_local_terms(mesh_, part_, red_, sd, coeff_, density_, s, loc.mass, loc.k_terms);
-    const Index ni = sd.n_interior(), ng = sd.n_iface();
-    // flattened interior block and interior x iface coupling (src/sg.cpp:203-217)
-    std::vector<Triplet> t_ii, t_ig;
-    for (int j = 0; j < nt; ++j) {
-      block_triplets(loc.mass, 0, ni, 0, ni, j * ni, j * ni, mass_scale_, t_ii);
-      block_triplets(loc.mass, 0, ni, ni, ng, j * ni, j * ng, mass_scale_, t_ig);
-    }
-    for (int i = 0; i < tensor_.n_input; ++i)
-      tensor_.for_each(i, [&](int j, int k, double g) {
-        block_triplets(loc.k_terms[i], 0, ni, 0, ni, k * ni, j * ni, stiff_scale_ * g, t_ii);
-        block_triplets(loc.k_terms[i], 0, ni, ni, ng, k * ni, j * ng, stiff_scale_ * g, t_ig);
-      });
-    loc.a_ig = Csr::from_triplets(nt * ni, nt * ng, std::move(t_ig));
-    if (ni > 0) {
-      // node band of the interior block
-      Index nbw = 0;
-      for (Index r = 0; r < ni; ++r)
-        for (Index p = loc.mass.ptr[r]; p < loc.mass.ptr[r + 1]; ++p)
-          if (loc.mass.col[p] < ni) nbw = std::max(nbw, std::abs(r - loc.mass.col[p]));
-      for (const Csr& kt : loc.k_terms)
-        for (Index r = 0; r < ni; ++r)
-          for (Index p = kt.ptr[r]; p < kt.ptr[r + 1]; ++p)
-            if (kt.col[p] < ni) nbw = std::max(nbw, std::abs(r - kt.col[p]));
-      if (!factor_flattened(t_ii, ni, nt, nbw, loc.ii))
-        throw std::runtime_error("stochastic interior factorization failed (subdomain " + std::to_string(s) + ")");
-      loc.has_interior = true;
-    }
-    // dense flattened local Schur (src/sg.cpp:227-245)
-    LocalSchur ls = make_flat_maps(sd, nt, layout_.n_iface(), layout_.n_corner());
-    const Index a = nt * ng;
-    ls.S = Dense(a, a);
-    for (int j = 0; j < nt; ++j)
-      for (Index r = 0; r < ng; ++r)
-        for (Index p = loc.mass.ptr[ni + r]; p < loc.mass.ptr[ni + r + 1]; ++p) {
-          const Index c = loc.mass.col[p];
-          if (c >= ni) ls.S(j * ng + r, j * ng + c - ni) += mass_scale_ * loc.mass.val[p];
-        }
-    for (int i = 0; i < tensor_.n_input; ++i) {
-      const Csr& kt = loc.k_terms[i];
-      tensor_.for_each(i, [&](int j, int k, double g) {
-        const double sg = stiff_scale_ * g;
-        for (Index r = 0; r < ng; ++r)
-          for (Index p = kt.ptr[ni + r]; p < kt.ptr[ni + r + 1]; ++p) {
-            const Index c = kt.col[p];
-            if (c >= ni) ls.S(k * ng + r, j * ng + c - ni) += sg * kt.val[p];
-          }
-      });
-    }
-    if (opt_.precond == 2) ls.Kgg = ls.S;  // A_GG before the elimination
-    if (ni > 0 && ng > 0) {
-      // S -= A_IG^T A_II^{-1} A_IG, panels of RHS in band index space, columns
-      // ordered by their first non-zero band row so panels skip leading zeros.
-      const Index nb = nt * ni;
-      std::vector<std::vector<std::pair<Index, double>>> cols(a);  // band-row entries per column
-      for (Index fr = 0; fr < nb; ++fr)
-        for (Index p = loc.a_ig.ptr[fr]; p < loc.a_ig.ptr[fr + 1]; ++p) {
-          const Index br = (fr % ni) * nt + fr / ni;
-          cols[loc.a_ig.col[p]].push_back({br, loc.a_ig.val[p]});
-        }
-      std::vector<Index> order(a), first(a, nb);
-      for (Index c = 0; c < a; ++c) {
-        order[c] = c;
-        for (auto& e : cols[c]) first[c] = std::min(first[c], e.first);
-      }
-      std::stable_sort(order.begin(), order.end(), [&](Index x, Index y) { return first[x] < first[y]; });
-      const Index P = 32;
-      std::vector<double> panel;
-      for (Index c0 = 0; c0 < a; c0 += P) {
-        const Index w = std::min(P, a - c0);
-        panel.assign(size_t(nb) * w, 0.0);
-        for (Index q = 0; q < w; ++q)
-          for (auto& e : cols[order[c0 + q]]) panel[size_t(e.first) * w + q] = e.second;
-        loc.ii.solve_many(panel.data(), w);
-        // S(c', order[c0+q]) -= sum_r A_IG(r, c') X(r, q)
-        for (Index fr = 0; fr < nb; ++fr) {
-          const Index br = (fr % ni) * nt + fr / ni;
-          const double* xr = &panel[size_t(br) * w];
-          for (Index p = loc.a_ig.ptr[fr]; p < loc.a_ig.ptr[fr + 1]; ++p) {
-            const Index cp = loc.a_ig.col[p];
-            const double v = loc.a_ig.val[p];
-            for (Index q = 0; q < w; ++q) ls.S(cp, order[c0 + q]) -= v * xr[q];
-          }
-        }
-      }
-    }
-    schur_.locals[s] = std::move(ls);
-  });
+  const Ctx cx{mesh_, part_, red_, layout_, coeff_, tensor_, density_, mass_scale_, stiff_scale_, nt, opt_.precond};
+  parallel_for(ns, opt_.threads, [&](int s) { build_local(cx, s, 1, locals_[s], schur_.locals[s]); });
   schur_.finalize(opt_.precond == 1);
+}
+
+// The body of assemble_subdomains' per-subdomain loop (src/sg.cpp:186-246):
+// local terms, flattened A_II / A_IG, the interior factor and the dense local
+// Schur S = A_GG - A_IG^T A_II^-1 A_IG.  panel_threads > 1 splits the
+// right-hand-side panels of the elimination over threads (independent columns).
+void SgSolver::build_local(const Ctx& cx, int s, int panel_threads, Local& loc, LocalSchur& ls) {
+  const int nt = cx.nt;
+  const SubdomainDofs& sd = cx.layout.sub[s];
+  assemble_local_terms(cx.mesh, cx.part, cx.red, sd, cx.coeff, cx.density, s, loc.mass, loc.k_terms);
+  const Index ni = sd.n_interior(), ng = sd.n_iface();
+  // flattened interior block and interior x iface coupling (src/sg.cpp:203-217)
+  std::vector<Triplet> t_ii, t_ig;
+  for (int j = 0; j < nt; ++j) {
+    block_triplets(loc.mass, 0, ni, 0, ni, j * ni, j * ni, cx.mass_scale, t_ii);
+    block_triplets(loc.mass, 0, ni, ni, ng, j * ni, j * ng, cx.mass_scale, t_ig);
+  }
+  for (int i = 0; i < cx.tensor.n_input; ++i)
+    cx.tensor.for_each(i, [&](int j, int k, double g) {
+      block_triplets(loc.k_terms[i], 0, ni, 0, ni, k * ni, j * ni, cx.stiff_scale * g, t_ii);
+      block_triplets(loc.k_terms[i], 0, ni, ni, ng, k * ni, j * ng, cx.stiff_scale * g, t_ig);
+    });
+  loc.a_ig = Csr::from_triplets(nt * ni, nt * ng, std::move(t_ig));
+  if (ni > 0) {
+    // node band of the interior block
+    Index nbw = 0;
+    for (Index r = 0; r < ni; ++r)
+      for (Index p = loc.mass.ptr[r]; p < loc.mass.ptr[r + 1]; ++p)
+        if (loc.mass.col[p] < ni) nbw = std::max(nbw, std::abs(r - loc.mass.col[p]));
+    for (const Csr& kt : loc.k_terms)
+      for (Index r = 0; r < ni; ++r)
+        for (Index p = kt.ptr[r]; p < kt.ptr[r + 1]; ++p)
+          if (kt.col[p] < ni) nbw = std::max(nbw, std::abs(r - kt.col[p]));
+    if (!factor_flattened(t_ii, ni, nt, nbw, loc.ii))
+      throw std::runtime_error("stochastic interior factorization failed (subdomain " + std::to_string(s) + ")");
+    loc.has_interior = true;
+  }
+  // dense flattened local Schur (src/sg.cpp:227-245)
+  ls = make_flat_maps(sd, nt, cx.layout.n_iface(), cx.layout.n_corner());
+  const Index a = nt * ng;
+  ls.S = Dense(a, a);
+  for (int j = 0; j < nt; ++j)
+    for (Index r = 0; r < ng; ++r)
+      for (Index p = loc.mass.ptr[ni + r]; p < loc.mass.ptr[ni + r + 1]; ++p) {
+        const Index c = loc.mass.col[p];
+        if (c >= ni) ls.S(j * ng + r, j * ng + c - ni) += cx.mass_scale * loc.mass.val[p];
+      }
+  for (int i = 0; i < cx.tensor.n_input; ++i) {
+    const Csr& kt = loc.k_terms[i];
+    cx.tensor.for_each(i, [&](int j, int k, double g) {
+      const double sg = cx.stiff_scale * g;
+      for (Index r = 0; r < ng; ++r)
+        for (Index p = kt.ptr[ni + r]; p < kt.ptr[ni + r + 1]; ++p) {
+          const Index c = kt.col[p];
+          if (c >= ni) ls.S(k * ng + r, j * ng + c - ni) += sg * kt.val[p];
+        }
+    });
+  }
+  if (cx.precond == 2) ls.Kgg = ls.S;  // A_GG before the elimination
+  if (ni > 0 && ng > 0) {
+    // S -= A_IG^T A_II^{-1} A_IG, panels of RHS in band index space, columns
+    // ordered by their first non-zero band row so panels skip leading zeros.
+    const Index nb = nt * ni;
+    std::vector<std::vector<std::pair<Index, double>>> cols(a);  // band-row entries per column
+    for (Index fr = 0; fr < nb; ++fr)
+      for (Index p = loc.a_ig.ptr[fr]; p < loc.a_ig.ptr[fr + 1]; ++p) {
+        const Index br = (fr % ni) * nt + fr / ni;
+        cols[loc.a_ig.col[p]].push_back({br, loc.a_ig.val[p]});
+      }
+    std::vector<Index> order(a), first(a, nb);
+    for (Index c = 0; c < a; ++c) {
+      order[c] = c;
+      for (auto& e : cols[c]) first[c] = std::min(first[c], e.first);
+    }
+    std::stable_sort(order.begin(), order.end(), [&](Index x, Index y) { return first[x] < first[y]; });
+    const Index P = 32;
+    const int n_panels = int((a + P - 1) / P);
+    // each panel updates only its own columns of S: panels are independent
+    parallel_for(n_panels, panel_threads, [&](int pi) {
+      const Index c0 = Index(pi) * P;
+      const Index w = std::min(P, a - c0);
+      std::vector<double> panel(size_t(nb) * w, 0.0);
+      for (Index q = 0; q < w; ++q)
+        for (auto& e : cols[order[c0 + q]]) panel[size_t(e.first) * w + q] = e.second;
+      loc.ii.solve_many(panel.data(), w);
+      // S(c', order[c0+q]) -= sum_r A_IG(r, c') X(r, q)
+      for (Index fr = 0; fr < nb; ++fr) {
+        const Index br = (fr % ni) * nt + fr / ni;
+        const double* xr = &panel[size_t(br) * w];
+        for (Index p = loc.a_ig.ptr[fr]; p < loc.a_ig.ptr[fr + 1]; ++p) {
+          const Index cp = loc.a_ig.col[p];
+          const double v = loc.a_ig.val[p];
+          for (Index q = 0; q < w; ++q) ls.S(cp, order[c0 + q]) -= v * xr[q];
+        }
+      }
+    });
+  }
+}
+
+// One subdomain's local operators without the rest of the solver: S_s (as
+// assemble_subdomains builds it), S_rr^{-1} V for caller vectors V, and
+// Psi = S_rr^{-1} S_rc (src/dd.cpp:112-120).  Used to check the GPU's
+// per-subdomain tiles at sizes where the whole oracle exceeds host memory.
+LocalSchur SgSolver::local_blocks(const Mesh& mesh, const Partition& part, const CoefficientField& coeff,
+                                  const TripleTensor& tensor, double density, double alpha0, double alpha1,
+                                  NewmarkParams params, int s, int threads) {
+  const DirichletReduction red = make_dirichlet_reduction(mesh);
+  const InterfaceLayout layout = build_interface_layout(part, red);
+  if (s < 0 || s >= part.n_sub) throw std::invalid_argument("subdomain out of range");
+  const double ms = params.mass_factor() + params.damping_factor() * alpha0;
+  const double ss = 1.0 + params.damping_factor() * alpha1;
+  const Ctx cx{mesh, part, red, layout, coeff, tensor, density, ms, ss, tensor.n_output, 0};
+  Local loc;
+  LocalSchur ls;
+  build_local(cx, s, threads, loc, ls);
+  const Index nr = Index(ls.r_idx.size()), nc = Index(ls.c_idx.size());
+  Dense srr(nr, nr);
+  ls.S_rc = Dense(nr, nc);
+  for (Index b = 0; b < nr; ++b)
+    for (Index a = 0; a < nr; ++a) srr(a, b) = ls.S(ls.r_idx[a], ls.r_idx[b]);
+  for (Index b = 0; b < nc; ++b)
+    for (Index a = 0; a < nr; ++a) ls.S_rc(a, b) = ls.S(ls.r_idx[a], ls.c_idx[b]);
+  ls.Srr_llt = llt_regularized(srr);
+  return ls;
 }
 
 void SgSolver::interior_solve(int s, double* flat) const {

@@ -229,6 +229,21 @@ int sgw_coarse_operator(sgw_solver* s, double* out) {
   });
 }
 
+int sgw_local_block(sgw_solver* s, int sub, int which, double* out, long long* gmap, long long* dims) {
+  return guard([&] {
+    GpuSolver& g = *s->g;
+    const int sl = g.local_sub(sub);
+    if (sl < 0 || sl >= g.NS) throw Error(SGW_EINVAL, "subdomain is not owned by this rank");
+    if (which < 0 || which > 2) throw Error(SGW_EINVAL, "which must be 0 (S), 1 (S_rr^-1) or 2 (Psi)");
+    if (dims) g.local_dims(sl, dims);
+    if (!out && !gmap) return;
+    std::vector<long long> gm;
+    const std::vector<double> v = g.local_block(sl, which, gmap ? &gm : nullptr);
+    if (out) std::memcpy(out, v.data(), v.size() * sizeof(double));
+    if (gmap) std::memcpy(gmap, gm.data(), gm.size() * sizeof(long long));
+  });
+}
+
 int sgw_init_state(sgw_solver* s, const double* u0, const double* v0, const sgw_force* force) {
   return guard([&] {
     GpuSolver& g = *s->g;

@@ -187,6 +187,59 @@ void pack_tiles_range(TilePack& tp, int s, const double* src, int ld, cudaStream
   SGW_LAUNCHED();
 }
 
+// Inverse of pack_tiles_kernel: lower tiles of matrix s -> dense column-major
+// n x n (both triangles).  One CTA per tile.
+__global__ void unpack_tiles_kernel(const int4* __restrict__ desc, int n, const double* __restrict__ tiles,
+                                    double* __restrict__ A) {
+  const long long t = blockIdx.x;
+  const int4 d = desc[t];
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int r = e / kTile, c = e % kTile, R = d.y * kTile + r, Cc = d.z * kTile + c;
+    if (R >= n || Cc >= n || Cc > R) continue;
+    const double v = tiles[t * kTile * kTile + e];
+    A[(size_t)Cc * n + R] = v;
+    A[(size_t)R * n + Cc] = v;
+  }
+}
+
+// Dense copy of subdomain s's local operator (verification hook): which 0 =
+// S_s (a x a), 1 = Q_s = S_rr^-1 (r x r), 2 = Psi_s (r x c), column-major.
+std::vector<double> GpuSolver::local_block(int s, int which, std::vector<long long>* gmap) {
+  if (s < 0 || s >= NS) throw Error(1, "local_block: subdomain not on this rank");
+  std::vector<double> out;
+  const int a = NT * ng_[s], r = NT * nr_[s], c = NT * nc_[s];
+  if (which == 0 || which == 1) {
+    TilePack& tp = which == 0 ? Sp : Qp;
+    if (!tp.tiles.p) throw Error(1, "local_block: S tiles are not stored (reduced-memory mode)");
+    const int dim = which == 0 ? a : r;
+    DBuf<double> d;
+    d.alloc(std::max<size_t>(1, (size_t)dim * dim));
+    const long long tb = tp.tile_base[s], te = tp.tile_base[s + 1];
+    if (te > tb) {
+      unpack_tiles_kernel<<<(unsigned)(te - tb), 256, 0, st_>>>(tp.desc.p + tb, dim, tp.tiles.p + tb * kTile * kTile,
+                                                               d.p);
+      SGW_LAUNCHED();
+    }
+    out.resize((size_t)dim * dim);
+    SGW_CUDA(cudaMemcpyAsync(out.data(), d.p, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  } else if (which == 2) {
+    out.resize((size_t)r * c);
+    if (!out.empty())
+      SGW_CUDA(cudaMemcpyAsync(out.data(), Psi.p + psioff_[s], out.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                               st_));
+  } else {
+    throw Error(1, "local_block: which must be 0 (S), 1 (S_rr^-1) or 2 (Psi)");
+  }
+  SGW_CUDA(cudaStreamSynchronize(st_));
+  if (gmap) {  // flat local index j*ng + p -> global flat interface index (make_flat_maps, dd.cpp:78-96)
+    const auto& sd = G.sub[s];
+    gmap->resize(a);
+    for (int j = 0; j < NT; ++j)
+      for (int p = 0; p < ng_[s]; ++p) (*gmap)[(size_t)j * ng_[s] + p] = (long long)j * G.n_iface + sd.iface_pos[p];
+  }
+  return out;
+}
+
 // One CTA (8 warps) per 64x64 lower tile (tiles.cuh): row / column partials.
 __global__ void __launch_bounds__(256) symv_tiles_kernel(const int4* __restrict__ desc,
                                                          const double* __restrict__ tiles,

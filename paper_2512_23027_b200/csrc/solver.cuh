@@ -207,6 +207,10 @@ class GpuSolver {
   void set_force_table(const double* table_host, int n_rows);
   int step(int* iters_out);  // one Newmark step on device
   std::vector<double> coarse_operator_host() const { return fcc_host_; }
+  // dense S_s / S_rr^-1 / Psi_s of local subdomain s (verification hook)
+  std::vector<double> local_block(int s, int which, std::vector<long long>* gmap);
+  int local_sub(int s_global) const { return s_global - G.s0; }  // caller checks 0 <= . < NS
+  void local_dims(int s, long long* d) const { d[0] = NT * ng_[s], d[1] = NT * nr_[s], d[2] = NT * nc_[s]; }
   // full state on every rank (sharded runs: owners' values summed across ranks)
   void gather_state(double* dst_dev);
   int rank() const { return comm_ ? comm_->rank() : 0; }

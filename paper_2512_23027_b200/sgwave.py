@@ -83,6 +83,7 @@ def load_library():
     L.sgw_apply_precond.argtypes = [vp, C.c_int, vp, vp]
     L.sgw_pcg.argtypes = [vp, vp, vp, vp, vp, vp, ip]
     L.sgw_coarse_operator.argtypes = [vp, vp]
+    L.sgw_local_block.argtypes = [vp, ip, ip, vp, vp, vp]
     L.sgw_run.argtypes = [vp, vp, vp, ip, C.POINTER(_Force), C.POINTER(_History)]
     L.sgw_init_state.argtypes = [vp, vp, vp, C.POINTER(_Force)]
     L.sgw_advance.argtypes = [vp, ip, vp]
@@ -321,6 +322,20 @@ class SchurSystem:
         z = np.zeros(self._s.n_global)
         _check(load_library().sgw_apply_precond(self._s._h, precond_from_string(kind), _p(r), _p(z)))
         return z
+
+    def local_block(self, sub, which="S"):
+        """Dense copy of subdomain `sub`'s local operator (verification hook):
+        "S" = S_s, "Q" = S_rr^-1, "Psi" = S_rr^-1 S_rc; returns (matrix, gmap)."""
+        w = {"S": 0, "Q": 1, "Psi": 2}[which]
+        d = np.zeros(3, np.int64)
+        L = load_library()
+        _check(L.sgw_local_block(self._s._h, sub, w, None, None, _p(d)))
+        a, r, c = (int(v) for v in d)
+        rows, cols = {0: (a, a), 1: (r, r), 2: (r, c)}[w]
+        out = np.zeros(rows * cols)
+        g = np.zeros(a, np.int64)
+        _check(L.sgw_local_block(self._s._h, sub, w, _p(out), _p(g), None))
+        return out.reshape(cols, rows).T.copy(), g
 
     def coarse_operator(self):
         n = self.n_corner

@@ -67,13 +67,24 @@ def test_nn2_symmetric_and_schur_spd(gpu):
     assert r1 @ g.schur().matvec(r1) > 0
 
 
-def test_pcg_matches_oracle_iterations(gpu):
-    g, c = pair(16, 4, 4, 0.3, 0.5, 2, 4, 2, 1e-3)
+@pytest.mark.parametrize("cfg", [(16, 4, 4, 2, 4, 2), (24, 3, 2, 3, 2, 3), (26, 4, 3, 2, 3, 2)])
+def test_pcg_matches_oracle_iterations(gpu, cfg):
+    # pcg(matvec, apply_nn2) (src/pcg.cpp:7-50) on the same right-hand side:
+    # iteration count within +-1, residual history and solution against the
+    # oracle's own pcg
+    nx, px, py, L, pin, pout = cfg
+    g, c = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 1e-3)
     b = c.schur_matvec(rand(g.n_global, 3))
     x, rep = g.pcg(b)
-    assert rep["converged"]
+    xc, repc = c.pcg(b)
+    assert rep["converged"] and repc["converged"]
+    assert abs(rep["iterations"] - repc["iterations"]) <= 1
+    if rep["iterations"] == repc["iterations"]:
+        h, hc = np.asarray(rep["residual_history"]), repc["residual_history"]
+        assert len(h) == len(hc) and np.allclose(h, hc, rtol=1e-6, atol=1e-14)
     res = np.linalg.norm(c.schur_matvec(x) - b) / np.linalg.norm(b)
     assert res <= 1e-10
+    assert np.linalg.norm(x - xc) / np.linalg.norm(xc) <= 1e-8
 
 
 @pytest.mark.parametrize("mode", ["fused", "host"])
