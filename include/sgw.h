@@ -71,11 +71,13 @@ typedef struct sgw_problem {
   int max_iter;           /* SgOptions::max_iter                               */
   int device;             /* CUDA device ordinal                                */
   /* Multi-GPU sharding (one process per GPU); world_size 1 = single GPU.
-   * Rank r owns subdomains [n_sub r / W, n_sub (r+1) / W) (row-major ids);
-   * interface vectors are replicated and every subdomain sum becomes a local
-   * partial sum + ncclAllReduce.  Every entry point is collective: all ranks
-   * call it with the same arguments.  Results (state, probes, PCG output)
-   * are identical on all ranks.
+   * The ranks form an rx x ry grid (sgw_shard_plan) and each owns a 2D block
+   * of subdomains and the interface nodes they touch; interface sums are
+   * completed by point-to-point halo exchanges (ncclSend/ncclRecv) with the
+   * neighbouring ranks, the coarse vector and the CG scalars by
+   * ncclAllReduce.  Every entry point is collective: all ranks call it with
+   * the same arguments.  Results (state, probes, PCG output) are identical on
+   * all ranks; interface vectors at this boundary are always global.
    * nccl_id: 128-byte ncclUniqueId from sgw_nccl_unique_id on rank 0,
    * broadcast by the caller (e.g. torch.distributed).  A non-NULL id with
    * world_size 1 runs the sharded code path on a 1-rank communicator.      */
@@ -184,6 +186,15 @@ int sgw_triple_products(int n_vars, int p_in, int p_out, int* n_in, int* n_out, 
                         int* ei, int* ej, int* ek, double* ev, long long cap);
 int sgw_nearest_node(int nx, int ny, double x, double y);
 
+/* Sharding plan (host only, no GPU needed): the rx x ry rank grid and rank
+ * `rank`'s halo.  info[7] = {rx, ry, owned subdomains, local interface nodes,
+ * peers, shared entries (sum over peers), global interface nodes}.  Optional
+ * outputs: sub_owner[px py] (rank of every subdomain), iface_gpos[local
+ * nodes] (global interface position of each local node, ascending), peers[],
+ * peer_off[peers + 1] and peer_idx[shared entries] (per peer, the shared
+ * local nodes in ascending global position).  Call with NULLs to size.       */
+int sgw_shard_plan(int nx, int ny, int px, int py, int world, int rank, long long* info, int* sub_owner,
+                   int* iface_gpos, int* peers, int* peer_off, int* peer_idx);
 /* NCCL unique id for multi-GPU runs (128 bytes), generated on rank 0. */
 int sgw_nccl_unique_id(void* out128);
 

@@ -61,6 +61,17 @@ void set_force(GpuSolver& g, const sgw_force* f, int rows) {
     throw Error(SGW_EINVAL, "unknown force kind");
   }
 }
+// global interface vectors in and out (every rank passes and gets the whole vector)
+template <typename F>
+void iface_op(GpuSolver& g, const double* x, double* y, F&& op) {
+  DBuf<double> gx, lx, ly, gy;
+  h2d(gx, x, g.NGG, g.stream());
+  lx.alloc(g.NG), ly.alloc(g.NG), gy.alloc(g.NGG);
+  g.iface_to_local(gx.p, lx.p);
+  op(lx.p, ly.p);
+  g.iface_to_global(ly.p, gy.p);
+  d2h(y, gy.p, g.NGG, g.stream());
+}
 }  // namespace
 
 extern "C" {
@@ -145,9 +156,9 @@ int sgw_sizes(sgw_solver* s, long long* o) {
     GpuSolver& g = *s->g;
     o[0] = g.n;
     o[1] = g.NT;
-    o[2] = g.G.n_iface;
+    o[2] = g.G.n_iface_global;
     o[3] = g.G.n_corner;
-    o[4] = g.NG;
+    o[4] = g.NGG;
     o[5] = g.G.ns_total;
     o[6] = 0;
     o[7] = g.device_bytes();
@@ -173,22 +184,14 @@ int sgw_apply_block(sgw_solver* s, int op, const double* x, double* y) {
 int sgw_schur_matvec(sgw_solver* s, const double* x, double* y) {
   return guard([&] {
     GpuSolver& g = *s->g;
-    DBuf<double> dx, dy;
-    h2d(dx, x, g.NG, g.stream());
-    dy.alloc(g.NG);
-    g.schur_matvec(dx.p, dy.p);
-    d2h(y, dy.p, g.NG, g.stream());
+    iface_op(g, x, y, [&](const double* a, double* b) { g.schur_matvec(a, b); });
   });
 }
 
 int sgw_apply_nn2(sgw_solver* s, const double* r, double* z) {
   return guard([&] {
     GpuSolver& g = *s->g;
-    DBuf<double> dx, dy;
-    h2d(dx, r, g.NG, g.stream());
-    dy.alloc(g.NG);
-    g.apply_nn2(dx.p, dy.p);
-    d2h(z, dy.p, g.NG, g.stream());
+    iface_op(g, r, z, [&](const double* a, double* b) { g.apply_nn2(a, b); });
   });
 }
 
@@ -196,11 +199,7 @@ int sgw_apply_precond(sgw_solver* s, int kind, const double* r, double* z) {
   return guard([&] {
     GpuSolver& g = *s->g;
     if (kind < 0 || kind > 2) throw Error(SGW_EINVAL, "unknown preconditioner");
-    DBuf<double> dx, dy;
-    h2d(dx, r, g.NG, g.stream());
-    dy.alloc(g.NG);
-    g.apply_precond(kind, dx.p, dy.p);
-    d2h(z, dy.p, g.NG, g.stream());
+    iface_op(g, r, z, [&](const double* a, double* b) { g.apply_precond(kind, a, b); });
   });
 }
 
@@ -208,13 +207,10 @@ int sgw_pcg(sgw_solver* s, const double* rhs, double* x, int* iterations, int* c
             int cap) {
   return guard([&] {
     GpuSolver& g = *s->g;
-    DBuf<double> db, dx;
-    h2d(db, rhs, g.NG, g.stream());
-    dx.alloc(g.NG);
     bool conv = false;
     std::vector<double> h;
-    const int it = g.pcg(db.p, dx.p, &conv, &h);
-    d2h(x, dx.p, g.NG, g.stream());
+    int it = 0;
+    iface_op(g, rhs, x, [&](const double* b, double* xx) { it = g.pcg(b, xx, &conv, &h); });
     if (iterations) *iterations = it;
     if (converged) *converged = conv ? 1 : 0;
     if (hist)
@@ -462,6 +458,23 @@ int sgw_triple_products(int n_vars, int p_in, int p_out, int* n_in, int* n_out, 
 }
 
 int sgw_nearest_node(int nx, int ny, double x, double y) { return nearest_node(nx, ny, x, y); }
+
+int sgw_shard_plan(int nx, int ny, int px, int py, int world, int rank, long long* info, int* sub_owner,
+                   int* iface_gpos, int* peers, int* peer_off, int* peer_idx) {
+  return guard([&] {
+    if (!info) throw Error(SGW_EINVAL, "null argument");
+    const Geometry g = build_geometry(nx, ny, px, py, rank, world);
+    const Halo& h = g.halo;
+    info[0] = g.rx, info[1] = g.ry, info[2] = g.ns, info[3] = g.n_iface, info[4] = (long long)h.peers.size();
+    info[5] = (long long)h.idx.size(), info[6] = g.n_iface_global;
+    if (sub_owner)
+      for (int s2 = 0; s2 < g.ns_total; ++s2) sub_owner[s2] = g.rank_of_sub(s2);
+    if (iface_gpos) std::memcpy(iface_gpos, g.iface_gpos.data(), g.iface_gpos.size() * sizeof(int));
+    if (peers) std::memcpy(peers, h.peers.data(), h.peers.size() * sizeof(int));
+    if (peer_off) std::memcpy(peer_off, h.peer_off.data(), h.peer_off.size() * sizeof(int));
+    if (peer_idx) std::memcpy(peer_idx, h.idx.data(), h.idx.size() * sizeof(int));
+  });
+}
 
 int sgw_nccl_unique_id(void* out128) {
   return guard([&] {

@@ -46,6 +46,28 @@ class NcclComm final : public Comm {
     if (n == 0) return;
     SGW_NCCL(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, comm_, st));
   }
+  void exchange(const std::vector<int>& peers, const std::vector<size_t>& off, const std::vector<size_t>& cnt,
+                const double* send, double* recv, cudaStream_t st) override {
+    if (peers.empty()) return;
+    SGW_NCCL(ncclGroupStart());
+    for (size_t i = 0; i < peers.size(); ++i) {
+      SGW_NCCL(ncclSend(send + off[i], cnt[i], ncclDouble, peers[i], comm_, st));
+      SGW_NCCL(ncclRecv(recv + off[i], cnt[i], ncclDouble, peers[i], comm_, st));
+    }
+    SGW_NCCL(ncclGroupEnd());
+  }
+  // ncclCommGetAsyncError: a peer that died or a failed transfer surfaces
+  // here; abort the communicator so no later call blocks on it
+  void poll() override {
+    if (!comm_) throw Error(5, "NCCL communicator was aborted");
+    ncclResult_t async = ncclSuccess;
+    SGW_NCCL(ncclCommGetAsyncError(comm_, &async));
+    if (async != ncclSuccess && async != ncclInProgress) {
+      ncclCommAbort(comm_);
+      comm_ = nullptr;
+      throw Error(5, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
+    }
+  }
 
  private:
   ncclComm_t comm_ = nullptr;
@@ -62,9 +84,13 @@ __global__ void sum_ranks_kernel(const double* const* __restrict__ src, int worl
 }  // namespace
 
 struct ThreadGroup {
-  explicit ThreadGroup(int w) : world(w), slot(w, nullptr) {}
+  explicit ThreadGroup(int w) : world(w), slot(w, nullptr), xsend(w, nullptr), xpeers(w), xoff(w) {}
   int world;
   std::vector<double*> slot;
+  // exchange(): every rank's send buffer and its (peer, offset) blocks
+  std::vector<const double*> xsend;
+  std::vector<std::vector<int>> xpeers;
+  std::vector<std::vector<size_t>> xoff;
   std::mutex mu;
   std::condition_variable cv;
   int arrived = 0;
@@ -113,6 +139,24 @@ class ThreadComm final : public Comm {
     g_->barrier();  // nobody overwrites its partial while another rank still reads it
     SGW_CUDA(cudaMemcpyAsync(buf, tmp_, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
+  void exchange(const std::vector<int>& peers, const std::vector<size_t>& off, const std::vector<size_t>& cnt,
+                const double* send, double* recv, cudaStream_t st) override {
+    SGW_CUDA(cudaStreamSynchronize(st));  // this rank's send blocks are final
+    g_->xsend[rank_] = send;
+    g_->xpeers[rank_] = peers;
+    g_->xoff[rank_] = off;
+    g_->barrier();
+    for (size_t i = 0; i < peers.size(); ++i) {  // the block peer i packed for this rank
+      const int pr = peers[i];
+      const auto& pp = g_->xpeers[pr];
+      const size_t k = size_t(std::find(pp.begin(), pp.end(), rank_) - pp.begin());
+      if (k == pp.size()) throw Error(1, "halo plan is not symmetric");
+      SGW_CUDA(cudaMemcpyAsync(recv + off[i], g_->xsend[pr] + g_->xoff[pr][k], cnt[i] * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    SGW_CUDA(cudaStreamSynchronize(st));
+    g_->barrier();  // nobody overwrites its send buffer while a peer still reads it
+  }
 
  private:
   std::shared_ptr<ThreadGroup> g_;
@@ -122,6 +166,28 @@ class ThreadComm final : public Comm {
   size_t cap_ = 0;
 };
 }  // namespace
+
+namespace {
+class SoloComm final : public Comm {
+ public:
+  SoloComm(int rank, int world) : rank_(rank), world_(world) {}
+  int rank() const override { return rank_; }
+  int size() const override { return world_; }
+  bool capturable() const override { return true; }
+  bool solo() const override { return true; }
+  void allreduce_sum(double*, size_t, cudaStream_t) override {}
+  void exchange(const std::vector<int>&, const std::vector<size_t>& off, const std::vector<size_t>& cnt, const double*,
+                double* recv, cudaStream_t st) override {
+    for (size_t i = 0; i < off.size(); ++i)
+      if (cnt[i]) SGW_CUDA(cudaMemsetAsync(recv + off[i], 0, cnt[i] * sizeof(double), st));
+  }
+
+ private:
+  int rank_, world_;
+};
+}  // namespace
+
+std::unique_ptr<Comm> make_solo_comm(int rank, int world) { return std::make_unique<SoloComm>(rank, world); }
 
 std::unique_ptr<Comm> make_nccl_comm(const void* id128, int rank, int world, int device) {
   return std::make_unique<NcclComm>(id128, rank, world, device);

@@ -14,6 +14,26 @@
 namespace sgw {
 
 // ----------------------------------------------------------- geometry ------
+bool rank_grid(int nx, int ny, int px, int py, int world, int* rx, int* ry) {
+  long long best = -1;
+  for (int a = 1; a <= world; ++a) {
+    if (world % a) continue;
+    const int b = world / a;
+    if (a > px || b > py) continue;
+    const long long cut = (long long)(a - 1) * ny + (long long)(b - 1) * nx;
+    if (best < 0 || cut < best || (cut == best && a > *rx)) best = cut, *rx = a, *ry = b;
+  }
+  return best >= 0;
+}
+
+int Geometry::rank_of_sub(int gid) const {
+  const int sx = gid % px, sy = gid / px;
+  int bx = 0, by = 0;
+  while (bx + 1 < rx && origin(bx + 1, px, rx) <= sx) ++bx;
+  while (by + 1 < ry && origin(by + 1, py, ry) <= sy) ++by;
+  return by * rx + bx;
+}
+
 // Structured restatement of partition_structured (src/partition.cpp:48-133,
 // floor-division cell ownership, so ragged splits are allowed) and
 // build_interface_layout / make_flat_maps (src/dd.cpp:10-96): interface =
@@ -26,38 +46,105 @@ Geometry build_geometry(int nx, int ny, int px, int py, int rank, int world) {
   g.nx = nx, g.ny = ny, g.px = px, g.py = py;
   g.mx = (nx + px - 1) / px, g.my = (ny + py - 1) / py;  // widest block (partition.cpp:70-76)
   g.n = (nx - 1) * (ny - 1);
+  g.ns_total = px * py;
+  if (world < 1 || rank < 0 || rank >= world) throw Error(1, "bad rank / world_size");
+  if (world > g.ns_total) throw Error(1, "more ranks than subdomains");
+  if (!rank_grid(nx, ny, px, py, world, &g.rx, &g.ry))
+    throw Error(1, "world_size " + std::to_string(world) + " does not factor into a rank grid rx x ry with rx <= px, "
+                   "ry <= py");
+  g.world = world, g.rank = rank;
+  g.bx0 = Geometry::origin(rank % g.rx, px, g.rx), g.bx1 = Geometry::origin(rank % g.rx + 1, px, g.rx);
+  g.by0 = Geometry::origin(rank / g.rx, py, g.ry), g.by1 = Geometry::origin(rank / g.rx + 1, py, g.ry);
+  g.gid_to_local.assign(g.ns_total, -1);
+  for (int sy = g.by0; sy < g.by1; ++sy)
+    for (int sx = g.bx0; sx < g.bx1; ++sx) {
+      g.gid_to_local[sy * px + sx] = int(g.sub_gid.size());
+      g.sub_gid.push_back(sy * px + sx);
+    }
+  g.ns = int(g.sub_gid.size());
   std::vector<char> vl(nx + 1, 0), hl(ny + 1, 0);
   for (int s = 1; s < px; ++s) vl[Geometry::origin(s, nx, px)] = 1;
   for (int s = 1; s < py; ++s) hl[Geometry::origin(s, ny, py)] = 1;
+  // ranks touching node (gi, gj): owners of the subdomains of its <= 4 cells
+  auto ranks_at = [&](int gi, int gj, int* out) {
+    int c = 0;
+    for (int cj = gj - 1; cj <= gj; ++cj)
+      for (int ci = gi - 1; ci <= gi; ++ci) {
+        if (ci < 0 || cj < 0 || ci >= nx || cj >= ny) continue;
+        const int r = g.rank_of_sub((cj * py / ny) * px + ci * px / nx);
+        bool seen = false;
+        for (int k = 0; k < c; ++k) seen |= out[k] == r;
+        if (!seen) out[c++] = r;
+      }
+    for (int a = 1; a < c; ++a)  // insertion sort of <= 4 ranks
+      for (int b = a; b > 0 && out[b - 1] > out[b]; --b) std::swap(out[b - 1], out[b]);
+    return c;
+  };
   g.iface_pos_of_dof.assign(g.n, -1);
+  g.iface_gpos_of_dof.assign(g.n, -1);
   g.corner_pos_of_dof.assign(g.n, -1);
+  std::vector<std::vector<int>> shared_with;  // per local interface node: ranks touching it
   for (int gj = 1; gj < ny; ++gj)
     for (int gi = 1; gi < nx; ++gi) {
       const bool vline = vl[gi], hline = hl[gj];
       if (!(vline || hline)) continue;
       const int d = g.dof(gi, gj);
-      g.iface_pos_of_dof[d] = static_cast<int>(g.iface_dofs.size());
-      g.iface_dofs.push_back(d);
+      g.iface_gpos_of_dof[d] = g.n_iface_global++;
       if (vline && hline) {
         g.corner_pos_of_dof[d] = static_cast<int>(g.corner_dofs.size());
         g.corner_dofs.push_back(d);
       }
+      int rk[4];
+      const int c = ranks_at(gi, gj, rk);
+      if (!std::binary_search(rk, rk + c, rank)) continue;
+      g.iface_pos_of_dof[d] = static_cast<int>(g.iface_dofs.size());
+      g.iface_dofs.push_back(d);
+      g.iface_gpos.push_back(g.iface_gpos_of_dof[d]);
+      g.iface_owner.push_back(rk[0]);
+      shared_with.emplace_back(rk, rk + c);
     }
   g.n_iface = static_cast<int>(g.iface_dofs.size());
   g.n_corner = static_cast<int>(g.corner_dofs.size());
-  g.ns_total = px * py;
-  if (world < 1 || rank < 0 || rank >= world) throw Error(1, "bad rank / world_size");
-  if (world > g.ns_total) throw Error(1, "more ranks than subdomains");
-  g.world = world;
-  g.s0 = Geometry::first_sub(rank, g.ns_total, world);
-  g.ns = Geometry::first_sub(rank + 1, g.ns_total, world) - g.s0;
+  // halo plan: per peer the shared nodes (ascending global position = local order)
+  {
+    Halo& h = g.halo;
+    std::vector<std::vector<int>> by_peer(world);
+    for (int q = 0; q < g.n_iface; ++q)
+      for (int r : shared_with[q])
+        if (r != rank) by_peer[r].push_back(q);
+    std::vector<int> pos_in_peer(world, -1);
+    h.peer_off.push_back(0);
+    for (int r = 0; r < world; ++r) {
+      if (by_peer[r].empty()) continue;
+      pos_in_peer[r] = int(h.peers.size());
+      h.peers.push_back(r);
+      h.idx.insert(h.idx.end(), by_peer[r].begin(), by_peer[r].end());
+      h.peer_off.push_back(int(h.idx.size()));
+    }
+    h.src_ptr.push_back(0);
+    std::vector<int> cursor(h.peers.size(), 0);
+    for (int q = 0; q < g.n_iface; ++q) {
+      if (shared_with[q].size() < 2) continue;
+      h.node.push_back(q);
+      for (int r : shared_with[q]) {
+        h.src_rank.push_back(r);
+        if (r == rank) {
+          h.src_pos.push_back(-1);
+        } else {  // q is the cursor-th shared node of this peer (both lists ascend)
+          const int pi = pos_in_peer[r];
+          h.src_pos.push_back(cursor[pi]++);
+        }
+      }
+      h.src_ptr.push_back(int(h.src_rank.size()));
+    }
+  }
   g.W = g.mx - 1;
   g.H = g.my - 1;
   g.nl = (g.mx + 1) * (g.my + 1);
   g.sub.resize(g.ns);
   for (int sl = 0; sl < g.ns; ++sl) {
     Geometry::Sub& sd = g.sub[sl];
-    const int s = g.s0 + sl;
+    const int s = g.sub_gid[sl];
     sd.sx = s % px;
     sd.sy = s / px;
     sd.ox = Geometry::origin(sd.sx, nx, px), sd.oy = Geometry::origin(sd.sy, ny, py);
@@ -91,9 +178,17 @@ Geometry build_geometry(int nx, int ny, int px, int py, int rank, int world) {
 }
 
 int Geometry::owner_of_dof(int d) const {
-  if (world == 1 || iface_pos_of_dof[d] >= 0) return 0;
+  if (world == 1) return 0;
+  if (iface_gpos_of_dof[d] >= 0) {  // interface: the lowest rank touching it
+    const int gi = d % (nx - 1) + 1, gj = d / (nx - 1) + 1;
+    int lo = world;
+    for (int cj = gj - 1; cj <= gj; ++cj)
+      for (int ci = gi - 1; ci <= gi; ++ci)
+        lo = std::min(lo, rank_of_sub((cj * py / ny) * px + ci * px / nx));
+    return lo;
+  }
   const int gi = d % (nx - 1) + 1, gj = d / (nx - 1) + 1;
-  return owner_of_sub((gj * py / ny) * px + gi * px / nx);  // interior: the block of cell (gi, gj)
+  return rank_of_sub((gj * py / ny) * px + gi * px / nx);  // interior: the block of cell (gi, gj)
 }
 
 // ----------------------------------------------------------- stencils ------

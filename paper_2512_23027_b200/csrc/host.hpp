@@ -36,37 +36,59 @@ struct Problem {
 // nodes beyond are inert (class -1, like Dirichlet nodes).  Interior nodes:
 // 0<il<mxs, 0<jl<mys (block row jl-1, position il-1).  Interface nodes: the
 // block boundary minus Dirichlet nodes, ordered by reduced dof id.
+//
+// Multi-GPU sharding: the ranks form an rx x ry grid and rank
+// (bx, by) owns the 2D block of subdomains [ceil(bx px/rx), ceil((bx+1) px/rx))
+// x [ceil(by py/ry), ...), which keeps the cut interface short.  Each rank
+// numbers only the interface nodes its subdomains touch ("local interface",
+// ascending global position); nodes on a rank-block boundary are held by every
+// rank that touches them (<= 4, diagonal neighbours included) and their sums
+// are completed by a point-to-point halo exchange (Halo).  World size 1: the
+// local interface is the global one.
+struct Halo {
+  std::vector<int> peers;      // ranks sharing >= 1 interface node, ascending
+  std::vector<int> peer_off;   // peers.size() + 1: blocks of `idx`
+  std::vector<int> idx;        // per peer: shared local interface positions, ascending global position
+  // per shared local node (ascending local position): the ranks touching it
+  // (ascending, this rank included) as sources of its sum
+  std::vector<int> node, src_ptr, src_rank, src_pos;  // src_pos: position in that peer's block (-1 = own)
+};
+
 struct Geometry {
   int nx = 0, ny = 0, px = 0, py = 0, mx = 0, my = 0;
   int n = 0;  // reduced dofs (nx-1)(ny-1), row-major over interior mesh nodes
-  int n_iface = 0, n_corner = 0;
-  std::vector<int> iface_dofs, corner_dofs;
-  std::vector<int> iface_pos_of_dof, corner_pos_of_dof;
-  // multi-GPU sharding: this rank owns subdomains [s0, s0 + ns) of ns_total
-  // (contiguous row-major ranges, owner_of_sub); sub[] holds the owned ones.
-  int ns = 0, s0 = 0, ns_total = 0, world = 1;
+  // n_iface: LOCAL interface nodes (all of them on one rank); n_corner: global cross points
+  int n_iface = 0, n_iface_global = 0, n_corner = 0;
+  std::vector<int> iface_dofs;        // local interface position -> reduced dof
+  std::vector<int> iface_gpos;        // local interface position -> global interface position
+  std::vector<int> iface_owner;       // local interface position -> lowest rank touching it
+  std::vector<int> iface_pos_of_dof;  // reduced dof -> local interface position or -1
+  std::vector<int> iface_gpos_of_dof; // reduced dof -> global interface position or -1
+  std::vector<int> corner_dofs, corner_pos_of_dof;  // global cross points
+  int ns = 0, ns_total = 0, world = 1, rank = 0;
+  int rx = 1, ry = 1, bx0 = 0, bx1 = 0, by0 = 0, by1 = 0;  // rank grid, this rank's block of subdomains
+  std::vector<int> sub_gid;        // owned subdomain (local index) -> global id (row-major), ascending
+  std::vector<int> gid_to_local;   // global id -> local index or -1
   int W = 0, H = 0, nl = 0;  // padded interior grid W x H, local nodes
   struct Sub {
     int sx = 0, sy = 0, ox = 0, oy = 0, mxs = 0, mys = 0;  // origin node, real cell extent
-    std::vector<int> iface_lid, iface_pos, r_local, c_local, corner_pos;
+    std::vector<int> iface_lid, iface_pos, r_local, c_local, corner_pos;  // iface_pos: local interface position
     std::vector<double> w;
     std::vector<int> lid_to_p;  // -2 interior, -1 Dirichlet, else local interface index
   };
   std::vector<Sub> sub;
+  Halo halo;
 
   static int origin(int s, int n, int p) { return (s * n + p - 1) / p; }  // ceil(s n / p)
-  static int first_sub(int r, int ns_total, int world) { return int((long long)ns_total * r / world); }
-  int owner_of_sub(int s) const {
-    int r = 0;
-    while (r + 1 < world && first_sub(r + 1, ns_total, world) <= s) ++r;
-    return r;
-  }
-  // rank holding the authoritative value of reduced dof d (interface: rank 0)
-  int owner_of_dof(int d) const;
+  int rank_of_sub(int gid) const;   // owner rank of a global subdomain
+  int owner_of_dof(int d) const;    // rank holding the authoritative value of reduced dof d
   int dof(int gi, int gj) const {
     return (gi >= 1 && gi <= nx - 1 && gj >= 1 && gj <= ny - 1) ? (gj - 1) * (nx - 1) + gi - 1 : -1;
   }
 };
+// rank grid rx x ry for `world` ranks on px x py subdomains: the factor pair
+// (rx <= px, ry <= py) with the shortest cut, (rx - 1) ny + (ry - 1) nx
+bool rank_grid(int nx, int ny, int px, int py, int world, int* rx, int* ry);
 Geometry build_geometry(int nx, int ny, int px, int py, int rank = 0, int world = 1);
 
 // P1 stencils.  K: 3 components per node (diag, E, N); the NE coupling of the

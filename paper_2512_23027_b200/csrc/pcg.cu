@@ -50,25 +50,26 @@ __device__ void finalize_sum(double v, double* partials, unsigned* counter, doub
 
 inline int red_grid(long long len) { return std::max(1, std::min<int>(kRedBlocks, cdiv(len, 256))); }
 
-__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
-                           double* partials, unsigned* counter, double* out, double* out_prev) {
+// sum_i a_i b_i (w_i): w = the ownership mask of a sharded interface vector
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ w,
+                           long long n, double* partials, unsigned* counter, double* out, double* out_prev) {
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    s += a[i] * b[i];
+    s += w ? a[i] * b[i] * w[i] : a[i] * b[i];
   finalize_sum(s, partials, counter, out, out_prev);
 }
 
 // x += alpha p ; r -= alpha q ; rr = r.r   with alpha = scal[RZN] / scal[PQ]
 __global__ void cg_xr_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                             const double* __restrict__ q, long long n, double* scal, double* partials,
-                             unsigned* counter) {
+                             const double* __restrict__ q, const double* __restrict__ w, long long n, double* scal,
+                             double* partials, unsigned* counter) {
   const double alpha = scal[RZN] / scal[PQ];
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     x[i] += alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
-    s += ri * ri;
+    s += w ? ri * ri * w[i] : ri * ri;
   }
   finalize_sum(s, partials, counter, scal + RR, nullptr);
 }
@@ -83,12 +84,13 @@ __global__ void cg_p_kernel(double* __restrict__ p, const double* __restrict__ z
 
 // rt = b - ax ; scal[RT] = rt.rt
 __global__ void residual_kernel(double* __restrict__ rt, const double* __restrict__ b, const double* __restrict__ ax,
-                                long long n, double* scal, double* partials, unsigned* counter) {
+                                const double* __restrict__ w, long long n, double* scal, double* partials,
+                                unsigned* counter) {
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double v = b[i] - ax[i];
     rt[i] = v;
-    s += v * v;
+    s += w ? v * v * w[i] : v * v;
   }
   finalize_sum(s, partials, counter, scal + RT, nullptr);
 }
@@ -104,19 +106,19 @@ void GpuSolver::mass_solve(double* x, const double* b) {
   SGW_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st_));
   SGW_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
   SGW_CUDA(cudaMemcpyAsync(p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
-  const double bb = dot_host(b, b, N);
+  const double bb = dot_host(b, b, N, false);
   if (bb == 0.0) return;
   const int grid = red_grid(N);
-  dot_kernel<<<grid, 256, 0, st_>>>(r, r, N, dpart.p, dcount.p, scal.p + RZN, nullptr);  // rz = r.r
+  dot_kernel<<<grid, 256, 0, st_>>>(r, r, nullptr, N, dpart.p, dcount.p, scal.p + RZN, nullptr);  // rz = r.r
   SGW_LAUNCHED();
   for (int it = 0; it < 500;) {
     for (int u = 0; u < 4; ++u, ++it) {
       apply_block(0, p, q);
-      dot_kernel<<<grid, 256, 0, st_>>>(p, q, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      dot_kernel<<<grid, 256, 0, st_>>>(p, q, nullptr, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();
-      cg_xr_kernel<<<grid, 256, 0, st_>>>(x, r, p, q, N, scal.p, dpart.p, dcount.p);  // alpha = rz / pq
+      cg_xr_kernel<<<grid, 256, 0, st_>>>(x, r, p, q, nullptr, N, scal.p, dpart.p, dcount.p);  // alpha = rz / pq
       SGW_LAUNCHED();
-      dot_kernel<<<grid, 256, 0, st_>>>(r, r, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
+      dot_kernel<<<grid, 256, 0, st_>>>(r, r, nullptr, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
       SGW_LAUNCHED();
       cg_p_kernel<<<grid, 256, 0, st_>>>(p, r, N, scal.p, 0);  // p = r + (rz_new / rz) p
       SGW_LAUNCHED();
@@ -235,7 +237,8 @@ std::vector<double> GpuSolver::local_block(int s, int which, std::vector<long lo
     const auto& sd = G.sub[s];
     gmap->resize(a);
     for (int j = 0; j < NT; ++j)
-      for (int p = 0; p < ng_[s]; ++p) (*gmap)[(size_t)j * ng_[s] + p] = (long long)j * G.n_iface + sd.iface_pos[p];
+      for (int p = 0; p < ng_[s]; ++p)
+        (*gmap)[(size_t)j * ng_[s] + p] = (long long)j * G.n_iface_global + G.iface_gpos[sd.iface_pos[p]];
   }
   return out;
 }
@@ -385,7 +388,7 @@ void GpuSolver::scatter_li(const double* li, double* glob, bool weighted, double
 void GpuSolver::schur_matvec(const double* x, double* y) {
   if (P.implicit_schur) return schur_matvec_implicit(x, y);
   s_product(x, y, nullptr, nullptr);
-  allreduce(y, NG);  // sharded: partial sums over owned subdomains
+  halo_sum(y);  // sharded: partial sums over owned subdomains -> full sums
   ++T.matvecs;
 }
 
@@ -560,7 +563,7 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
         d_coff.p, has_coarse ? 1 : 0);
     SGW_LAUNCHED();
     scatter_li(li_y.p, z, true, nullptr, nullptr);
-    allreduce(z, NG);
+    halo_sum(z);
     ++T.nn2s;
     return;
   }
@@ -582,7 +585,7 @@ void GpuSolver::apply_nn2(const double* r, double* z) {
         has_coarse ? 1 : 0);
   SGW_LAUNCHED();
   scatter_li(li_y.p, z, true, nullptr, nullptr);
-  allreduce(z, NG);
+  halo_sum(z);
   ++T.nn2s;
 }
 
@@ -597,7 +600,7 @@ void GpuSolver::apply_one_level(TilePack& tp, const double* r, double* z) {
                                               inv_p.p, ng_d.p, G.n_iface, NG, 1, tp.rowpart.p, tp.colpart.p,
                                               tp.d_tile_base.p, tp.d_ntile.p, nullptr, nullptr, nullptr, nullptr);
   SGW_LAUNCHED();
-  allreduce(z, NG);
+  halo_sum(z);
   ++T.nn2s;
 }
 
@@ -610,13 +613,15 @@ void GpuSolver::apply_precond(int kind, const double* r, double* z) {
 }
 
 // -------------------------------------------------------------- vectors ----
-void GpuSolver::dot_dev(const double* a, const double* b, long long len, double* out) {
-  dot_kernel<<<red_grid(len), 256, 0, st_>>>(a, b, len, dpart.p, dcount.p, out, nullptr);
+// iface: a, b are (sharded) interface vectors: owned entries only, summed over ranks
+void GpuSolver::dot_dev(const double* a, const double* b, long long len, double* out, bool iface) {
+  dot_kernel<<<red_grid(len), 256, 0, st_>>>(a, b, iface ? dot_mask() : nullptr, len, dpart.p, dcount.p, out, nullptr);
   SGW_LAUNCHED();
+  if (iface) allreduce(out, 1);
 }
 
-double GpuSolver::dot_host(const double* a, const double* b, long long len) {
-  dot_dev(a, b, len, scal.p + TMP);
+double GpuSolver::dot_host(const double* a, const double* b, long long len, bool iface) {
+  dot_dev(a, b, len, scal.p + TMP, iface);
   double h = 0;
   SGW_CUDA(cudaMemcpyAsync(&h, scal.p + TMP, sizeof(double), cudaMemcpyDeviceToHost, st_));
   SGW_CUDA(cudaStreamSynchronize(st_));
@@ -632,7 +637,7 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
   const long long N = NG;
   const int grid = red_grid(N);
   SGW_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), st_));
-  const double bb = dot_host(b, b, N);
+  const double bb = dot_host(b, b, N, true);
   const double bnorm = std::sqrt(bb);
   int iters = 0;
   *converged = false;
@@ -648,38 +653,45 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     T.pcg_ms += ms;
     return 0;
   }
+  const double* w = dot_mask();  // sharded: owned interface entries (global dots)
+  // r.z -> scal[RZN] (previous in scal[RZ]), summed over ranks
+  auto rz_dot = [&]() {
+    dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, w, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
+    SGW_LAUNCHED();
+    allreduce(scal.p + RZN, 1);
+  };
   SGW_CUDA(cudaMemcpyAsync(vr.p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
   apply_precond(P.precond, vr.p, vz.p);
-  dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
-  SGW_LAUNCHED();
+  rz_dot();
   cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 1);
   SGW_LAUNCHED();
   if (hist) hist->push_back(1.0);
   // The two halves of an iteration (S p ... x, r, ||r||; NN2 ... p) as CUDA
   // graphs when the exchange can be captured (no exchange, or NCCL): two
-  // launches per iteration instead of ~15 kernels and 3 collectives.
+  // launches per iteration instead of ~15 kernels and the collectives.
   const bool graphs = !comm_ || comm_->capturable();
   auto matvec_half = [&]() {
     if (P.implicit_schur) {
-      schur_matvec_implicit(vp.p, vq.p);  // sum over ranks included
-      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      schur_matvec_implicit(vp.p, vq.p);  // halo included
+      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, w, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();
+    } else if (!comm_) {
+      s_product(vp.p, vq.p, vp.p, scal.p + PQ);  // p.q fused into the scatter
     } else {
-    s_product(vp.p, vq.p, comm_ ? nullptr : vp.p, scal.p + PQ);
-    }
-    if (comm_ && !P.implicit_schur) {
-      allreduce(vq.p, NG);
-      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
+      s_product(vp.p, vq.p, nullptr, nullptr);
+      halo_sum(vq.p);
+      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, w, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
       SGW_LAUNCHED();
     }
-    cg_xr_kernel<<<grid, 256, 0, st_>>>(x, vr.p, vp.p, vq.p, N, scal.p, dpart.p, dcount.p);
+    allreduce(scal.p + PQ, 1);
+    cg_xr_kernel<<<grid, 256, 0, st_>>>(x, vr.p, vp.p, vq.p, w, N, scal.p, dpart.p, dcount.p);
     SGW_LAUNCHED();
+    allreduce(scal.p + RR, 1);
     SGW_CUDA(cudaMemcpyAsync(h_scal_, scal.p + RR, sizeof(double), cudaMemcpyDeviceToHost, st_));
   };
   auto precond_half = [&]() {
     apply_precond(P.precond, vr.p, vz.p);
-    dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
-    SGW_LAUNCHED();
+    rz_dot();
     cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 0);
     SGW_LAUNCHED();
   };
@@ -705,63 +717,24 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     graph_x_ = x;
   }
   for (int it = 0; it < P.max_iter; ++it) {
-    if (graphs) {  // q = S p, p.q, x, r, ||r||^2 -> host
+    // q = S p, p.q, x, r, ||r||^2 -> host
+    if (graphs) {
       SGW_CUDA(cudaGraphLaunch(graph_mv_, st_));
       g_launches += graph_mv_launches_;
-      ++T.matvecs;
-      ++iters;
-      SGW_CUDA(cudaStreamSynchronize(st_));
-      double rel = std::sqrt(*h_scal_) / bnorm;
-      last_rel = rel;
-      if (rel <= P.tol) {
-        schur_matvec(x, vq.p);
-        residual_kernel<<<grid, 256, 0, st_>>>(vrt.p, b, vq.p, N, scal.p, dpart.p, dcount.p);
-        SGW_LAUNCHED();
-        double rt = 0;
-        SGW_CUDA(cudaMemcpyAsync(&rt, scal.p + RT, sizeof(double), cudaMemcpyDeviceToHost, st_));
-        SGW_CUDA(cudaStreamSynchronize(st_));
-        rel = std::sqrt(rt) / bnorm;
-        last_rel = rel;
-        if (hist) hist->push_back(rel);
-        if (rel <= P.tol) {
-          *converged = true;
-          break;
-        }
-        SGW_CUDA(cudaMemcpyAsync(vr.p, vrt.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st_));
-      } else if (hist) {
-        hist->push_back(rel);
-      }
-      SGW_CUDA(cudaGraphLaunch(graph_pc_, st_));
-      g_launches += graph_pc_launches_;
-      T.nn2s += 1;
-      continue;
-    }
-    // q = S p with p.q fused into the scatter
-    if (P.implicit_schur) {
-      schur_matvec_implicit(vp.p, vq.p);
-      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
-      SGW_LAUNCHED();
     } else {
-    s_product(vp.p, vq.p, comm_ ? nullptr : vp.p, scal.p + PQ);
-    }
-    if (comm_ && !P.implicit_schur) {  // sharded: q is complete only after the sum over ranks
-      allreduce(vq.p, NG);
-      dot_kernel<<<grid, 256, 0, st_>>>(vp.p, vq.p, N, dpart.p, dcount.p, scal.p + PQ, nullptr);
-      SGW_LAUNCHED();
+      matvec_half();
     }
     ++T.matvecs;
-    cg_xr_kernel<<<grid, 256, 0, st_>>>(x, vr.p, vp.p, vq.p, N, scal.p, dpart.p, dcount.p);
-    SGW_LAUNCHED();
     ++iters;
-    double rr = 0;
-    SGW_CUDA(cudaMemcpyAsync(&rr, scal.p + RR, sizeof(double), cudaMemcpyDeviceToHost, st_));
     SGW_CUDA(cudaStreamSynchronize(st_));
-    double rel = std::sqrt(rr) / bnorm;
+    if (comm_) comm_->poll();
+    double rel = std::sqrt(*h_scal_) / bnorm;
     last_rel = rel;
     if (rel <= P.tol) {
       schur_matvec(x, vq.p);
-      residual_kernel<<<grid, 256, 0, st_>>>(vrt.p, b, vq.p, N, scal.p, dpart.p, dcount.p);
+      residual_kernel<<<grid, 256, 0, st_>>>(vrt.p, b, vq.p, w, N, scal.p, dpart.p, dcount.p);
       SGW_LAUNCHED();
+      allreduce(scal.p + RT, 1);
       double rt = 0;
       SGW_CUDA(cudaMemcpyAsync(&rt, scal.p + RT, sizeof(double), cudaMemcpyDeviceToHost, st_));
       SGW_CUDA(cudaStreamSynchronize(st_));
@@ -776,11 +749,13 @@ int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<doub
     } else if (hist) {
       hist->push_back(rel);
     }
-    apply_precond(P.precond, vr.p, vz.p);
-    dot_kernel<<<grid, 256, 0, st_>>>(vr.p, vz.p, N, dpart.p, dcount.p, scal.p + RZN, scal.p + RZ);
-    SGW_LAUNCHED();
-    cg_p_kernel<<<grid, 256, 0, st_>>>(vp.p, vz.p, N, scal.p, 0);
-    SGW_LAUNCHED();
+    if (graphs) {
+      SGW_CUDA(cudaGraphLaunch(graph_pc_, st_));
+      g_launches += graph_pc_launches_;
+    } else {
+      precond_half();
+    }
+    T.nn2s += 1;
   }
   cudaEventRecord(ev_[1], st_);
   SGW_CUDA(cudaEventSynchronize(ev_[1]));

@@ -354,6 +354,9 @@ void GpuSolver::build_maps() {
   c_gidx.upload(cg);
   c_w.upload(cw);
   d_coff.upload(coff_);
+  sub_gid_d_.upload(G.sub_gid);
+  gid_local_d_.upload(G.gid_to_local);
+  build_halo();
 }
 
 // ---------------------------------------------------------- constructor ----
@@ -372,6 +375,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   NS = G.ns;
   n = G.n;
   NG = NT * G.n_iface;
+  NGG = (long long)NT * G.n_iface_global;
   NC = NT * G.n_corner;
   NSTATE = size_t(NT) * n;
   SGW_CUDA(cudaSetDevice(P.device));
@@ -568,7 +572,7 @@ void GpuSolver::setup_interior_and_schur(int b0, int nb) {
     for (int k = 0; k < H; ++k)
       for (int q = 0; q < ns; ++q)
         if (h[size_t(k) * ns + q] != 0)
-          throw Error(2, "stochastic interior factorization failed (subdomain " + std::to_string(G.s0 + b0 + q) + ")");
+          throw Error(2, "stochastic interior factorization failed (subdomain " + std::to_string(G.sub_gid[b0 + q]) + ")");
   }
   // S_s = A_GG - Y^T Y, Y = L^-1 A_IG by rolling block forward substitution
   Sdense_.alloc(size_t(ns) * amax * amax);

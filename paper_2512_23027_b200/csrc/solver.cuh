@@ -25,6 +25,7 @@
 #include "comm.hpp"
 #include "common.cuh"
 #include "host.hpp"
+#include "tiles.cuh"
 
 namespace sgw {
 
@@ -129,7 +130,8 @@ struct LocalArgs {
   const int* lid_to_p;
   const long long* lioff;
   const int* ng;
-  int nl, nin, nt, mx, my, px, nx, py, ny, H, B, s0;
+  const int* sub_gid;  // local subdomain -> global id (row-major)
+  int nl, nin, nt, mx, my, px, nx, py, ny, H, B;
   double ms, ss;
 };
 
@@ -209,7 +211,9 @@ class GpuSolver {
   std::vector<double> coarse_operator_host() const { return fcc_host_; }
   // dense S_s / S_rr^-1 / Psi_s of local subdomain s (verification hook)
   std::vector<double> local_block(int s, int which, std::vector<long long>* gmap);
-  int local_sub(int s_global) const { return s_global - G.s0; }  // caller checks 0 <= . < NS
+  int local_sub(int s_global) const {
+    return s_global >= 0 && s_global < G.ns_total ? G.gid_to_local[s_global] : -1;
+  }
   void local_dims(int s, long long* d) const { d[0] = NT * ng_[s], d[1] = NT * nr_[s], d[2] = NT * nc_[s]; }
   // full state on every rank (sharded runs: owners' values summed across ranks)
   void gather_state(double* dst_dev);
@@ -221,7 +225,13 @@ class GpuSolver {
 
   Problem P;
   Geometry G;
-  int NT = 0, NIN = 0, NS = 0, n = 0, NG = 0, NC = 0;  // NG = NT*n_iface, NC = NT*n_corner
+  // NG = NT * local interface nodes, NGG = NT * global interface nodes (equal
+  // on one GPU), NC = NT * cross points
+  int NT = 0, NIN = 0, NS = 0, n = 0, NG = 0, NC = 0;
+  long long NGG = 0;
+  // C-ABI interface vectors are global; the solver works on the rank's local numbering
+  void iface_to_local(const double* glob_dev, double* loc_dev);
+  void iface_to_global(const double* loc_dev, double* glob_dev);
   size_t NSTATE = 0;
   double setup_s = 0;
   Timers T;
@@ -252,6 +262,19 @@ class GpuSolver {
     if (comm_) comm_->allreduce_sum(buf, n, st_);
   }
   DBuf<double> own_mask_;  // sharded: 1 on dofs this rank owns (Geometry::owner_of_dof), per term
+  // sharded interface halo (host.hpp Halo, tiles.cuh HaloDev; shard.cu)
+  DBuf<int> hx_pk_ptr_, hx_cnode_, hx_cptr_;
+  DBuf<int2> hx_pk_, hx_csrc_;
+  DBuf<double> hx_send_, hx_recv_;
+  std::vector<size_t> hx_off_, hx_cnt_;  // per peer block, doubles
+  int hx_nshared_ = 0;
+  DBuf<double> own_w_;  // NG: 1 on the interface entries this rank owns (dots); sharded only
+  DBuf<int> sub_gid_d_, gid_local_d_, iface_gpos_d_;
+  void build_halo();
+  HaloDev halo_dev() const;
+  void halo_exchange();
+  void halo_sum(double* y);  // complete a local partial interface vector (no-op unsharded)
+  const double* dot_mask() const { return comm_ ? own_w_.p : nullptr; }
   void build_device_inputs(const Stencils& st);
   void setup_interior_and_schur(int b0, int nb);
   void plan_nn2();
@@ -262,8 +285,8 @@ class GpuSolver {
   void gather_li(const double* glob, double* li, bool weighted);
   void scatter_li(const double* li, double* glob, bool weighted, double* dot_with, double* dot_out);
   void symv(TilePack& tp, const double* xloc, double* yloc_or_null);
-  double dot_host(const double* a, const double* b, long long len);
-  void dot_dev(const double* a, const double* b, long long len, double* out);
+  double dot_host(const double* a, const double* b, long long len, bool iface);
+  void dot_dev(const double* a, const double* b, long long len, double* out, bool iface);
   void local_force(double fext);
   void mass_solve(double* x, const double* b);
   LocalArgs local_args() const;

@@ -105,7 +105,7 @@ void GpuSolver::apply_block(int op, const double* x, double* y) {
 // non-Dirichlet nodes (lid_to_p != -1)
 __device__ __forceinline__ int block_origin(int s, int n, int p) { return (s * n + p - 1) / p; }
 __device__ __forceinline__ int lid_dof(const LocalArgs& A, int s, int il, int jl) {
-  const int sg = A.s0 + s;  // global subdomain id
+  const int sg = A.sub_gid[s];  // global subdomain id
   const int gi = block_origin(sg % A.px, A.nx, A.px) + il, gj = block_origin(sg / A.px, A.ny, A.py) + jl;
   return (gj - 1) * (A.nx - 1) + gi - 1;
 }
@@ -420,8 +420,8 @@ __global__ void predictor_kernel(const double* __restrict__ u, const double* __r
 __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, double* __restrict__ a,
                               const double* __restrict__ ug, const double* __restrict__ yI,
                               const double* __restrict__ wI, const int* __restrict__ iface_of_dof, int n, int nt,
-                              int n_iface, int nx, int ny, int px, int py, int H, int B, int s0, int ns,
-                              double dt, double zeta, double gamma) {
+                              int n_iface, int nx, int ny, int px, int py, int H, int B,
+                              const int* __restrict__ gid_local, double dt, double zeta, double gamma) {
   const int N = n * nt;  // < 2^31 (GpuSolver ctor): 32-bit index arithmetic
   const double zdd = zeta * dt * dt, c1 = (1.0 - 2.0 * zeta) / (2.0 * zeta);
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N; t += gridDim.x * blockDim.x) {
@@ -435,8 +435,8 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
       // interior node: cell gi lies in the same block (partition.cpp:70-76)
       const int sx = gi * px / nx, sy = gj * py / ny;
       const int il = gi - block_origin(sx, nx, px), jl = gj - block_origin(sy, ny, py);
-      const int sl = sy * px + sx - s0;
-      if (sl < 0 || sl >= ns) continue;  // sharded: interior of another rank's subdomain
+      const int sl = gid_local[sy * px + sx];
+      if (sl < 0) continue;  // sharded: interior of another rank's subdomain
       const long long idx = ((long long)sl * H + (jl - 1)) * B + (long long)(il - 1) * nt + k;
       un = yI[idx] - wI[idx];
     }
@@ -515,7 +515,7 @@ void GpuSolver::schur_matvec_implicit(const double* x, double* y) {
       A, 2, wI.p, nullptr, li_x.p, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
   SGW_LAUNCHED();
   scatter_li(li_y.p, y, false, nullptr, nullptr);
-  allreduce(y, NG);
+  halo_sum(y);
 }
 
 // ---------------------------------------------------------------- driver ---
@@ -559,8 +559,8 @@ const double* GpuSolver::force_at(double t, int row, double* fval) {
 }
 
 LocalArgs GpuSolver::local_args() const {
-  return LocalArgs{Kl.p, Ml.p, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, lid_to_p.p, Sp.d_xoff.p, ng_d.p, G.nl, NIN,
-                   NT, G.mx, G.my, G.px, P.nx, G.py, P.ny, G.H, B, G.s0, P.mass_scale, P.stiff_scale};
+  return LocalArgs{Kl.p, Ml.p, GList{gk_ptr.p, gk_i.p, gk_j.p, gk_v.p}, lid_to_p.p, Sp.d_xoff.p, ng_d.p, sub_gid_d_.p,
+                   G.nl, NIN, NT, G.mx, G.my, G.px, P.nx, G.py, P.ny, G.H, B, P.mass_scale, P.stiff_scale};
 }
 
 // src/sg.cpp:358-376: u, v in block 0, a = M^-1 (f0 - a0 M v - a1 K v - K u).
@@ -708,7 +708,7 @@ int GpuSolver::step(int* iters_out) {
       nullptr, li_y.p, nullptr);
   SGW_LAUNCHED();
   scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
-  allreduce(vb.p, NG);
+  halo_sum(vb.p);
   cudaEventRecord(ev_[3], st_);
   bool conv = false;
   // persistent PCG: its convergence is read after the recovery is launched
@@ -734,7 +734,7 @@ int GpuSolver::step(int* iters_out) {
   }
   sweep(wI.p);  // A_II^-1 A_IG u_G
   update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
-                                       P.ny, G.px, G.py, G.H, B, G.s0, NS, P.dt, P.zeta, P.gamma);
+                                       P.ny, G.px, G.py, G.H, B, gid_local_d_.p, P.dt, P.zeta, P.gamma);
   SGW_LAUNCHED();
   t_now = t_now + P.dt;
   ++step_index;

@@ -149,4 +149,42 @@ __device__ __forceinline__ double rect_reduce(const RangePack& P, int s, int i) 
   return partial_sum(P.part + P.pbase[s] + i, kTile * (P.nI[s] + P.nJ[s]), P.ncta[s]);
 }
 
+// Halo of the shared interface nodes (host.hpp Halo) on the device.  Send /
+// receive buffers hold one block per peer, term-major inside a block
+// ([j * cnt + i], cnt = the peer's shared nodes).
+//  * pack: node q's partial of term j goes to send[e.x + j * e.y] for every
+//    entry e of pk[pk_ptr[q] .. pk_ptr[q + 1]) (one per peer sharing q);
+//  * combine: shared node cnode[c] = sum over its sources in ascending rank,
+//    csrc[..] = {offset in recv (or -1: this rank's own partial), stride}.
+// Every holder of a node sums the same values in the same order, so the
+// completed vectors are bitwise identical on all ranks.
+struct HaloDev {
+  int nloc;              // local interface nodes (vector stride per term)
+  int n_shared;          // shared nodes
+  const int* pk_ptr;     // nloc + 1
+  const int2* pk;        // {base + i, cnt}
+  const int* cnode;      // n_shared
+  const int* cptr;       // n_shared + 1
+  const int2* csrc;      // {recv offset | -1, stride}
+  double* send;
+  const double* recv;
+};
+
+// partial y (term j, local node gq) into the send blocks of the peers sharing gq
+__device__ __forceinline__ void halo_pack_one(const HaloDev& H, int j, int gq, double y) {
+  for (int e = H.pk_ptr[gq]; e < H.pk_ptr[gq + 1]; ++e) {
+    const int2 d = H.pk[e];
+    H.send[d.x + (long long)j * d.y] = y;
+  }
+}
+// completed value of shared node c (term j) from the own partial `own`
+__device__ __forceinline__ double halo_combine_one(const HaloDev& H, int c, int j, double own) {
+  double acc = 0.0;
+  for (int e = H.cptr[c]; e < H.cptr[c + 1]; ++e) {
+    const int2 d = H.csrc[e];
+    acc += d.x < 0 ? own : __ldcg(H.recv + d.x + (long long)j * d.y);
+  }
+  return acc;
+}
+
 }  // namespace sgw

@@ -97,6 +97,7 @@ def load_library():
                                       C.c_longlong]
     L.sgw_nearest_node.argtypes = [ip, ip, dp, dp]
     L.sgw_nccl_unique_id.argtypes = [vp]
+    L.sgw_shard_plan.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp]
     L.sgw_local_group_new.argtypes = [ip, C.POINTER(vp)]
     L.sgw_local_group_free.argtypes = [vp]
     L.sgw_create_local_group.argtypes = [C.POINTER(_Problem), ip, ip, vp, C.POINTER(vp)]
@@ -354,12 +355,38 @@ def precond_from_string(name) -> int:
     return PRECONDS.index(name)
 
 
-def shard_plan(n_sub: int, world_size: int) -> list[range]:
-    """Subdomains owned by each rank: contiguous row-major ranges
-    [n_sub r / W, n_sub (r+1) / W) (Geometry::first_sub in csrc/host.hpp)."""
-    if not 1 <= world_size <= n_sub:
+class ShardPlan:
+    """Rank `rank`'s share of a `world`-rank decomposition (host.hpp Geometry,
+    computed by libsgw_b200 on the host): the rx x ry rank grid, the owner of
+    every subdomain, the rank's local interface nodes (global positions) and
+    its halo (per peer, the shared local nodes in ascending global order)."""
+
+    def __init__(self, nx, ny, px, py, world, rank):
+        L = load_library()
+        info = np.zeros(7, np.int64)
+        _check(L.sgw_shard_plan(nx, ny, px, py, world, rank, _p(info), None, None, None, None, None))
+        self.rx, self.ry, self.n_sub_owned, self.n_iface, n_peers, n_idx, self.n_iface_global = (int(v) for v in info)
+        self.sub_owner = np.zeros(px * py, np.int32)
+        self.iface_gpos = np.zeros(self.n_iface, np.int32)
+        self.peers = np.zeros(n_peers, np.int32)
+        self.peer_off = np.zeros(n_peers + 1, np.int32)
+        self.peer_idx = np.zeros(n_idx, np.int32)
+        _check(L.sgw_shard_plan(nx, ny, px, py, world, rank, _p(info), _p(self.sub_owner), _p(self.iface_gpos),
+                                _p(self.peers), _p(self.peer_off), _p(self.peer_idx)))
+        self.owned = np.flatnonzero(self.sub_owner == rank)
+
+    def shared_with(self, i):
+        """local interface nodes shared with peers[i]"""
+        return self.peer_idx[self.peer_off[i]:self.peer_off[i + 1]]
+
+
+def shard_plan(px: int, py: int, world_size: int, nx: int | None = None, ny: int | None = None) -> list[list[int]]:
+    """Subdomains (row-major ids) owned by each rank: 2D blocks of the rx x ry
+    rank grid with the shortest cut (host.hpp rank_grid)."""
+    if not 1 <= world_size <= px * py:
         raise SgInvalidArgument(SGW_EINVAL, "need 1 <= world_size <= number of subdomains")
-    return [range(n_sub * r // world_size, n_sub * (r + 1) // world_size) for r in range(world_size)]
+    owner = ShardPlan(nx or 8 * px, ny or 8 * py, px, py, world_size, 0).sub_owner
+    return [list(np.flatnonzero(owner == r)) for r in range(world_size)]
 
 
 def nccl_unique_id() -> bytes:
