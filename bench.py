@@ -162,6 +162,39 @@ def run_reference(args, c, name):
     print(json.dumps(line), flush=True)
 
 
+def run_solo(args, c, name, sg):
+    """One rank of a W-rank decomposition built alone on this GPU (sgw_create_solo):
+    per-rank device memory, setup time and the shard's PCG iteration time
+    (phase-split kernels, exchanges deliver zeros).  Unmeasured on hardware as
+    a multi-GPU run: it times one shard's kernels, not the NVLink exchanges."""
+    import torch
+
+    nx = c["nx"]
+    coeff = sg.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
+    tensor = sg.triple_products(c["L"], c["p_in"], c["p_out"])
+    t0 = time.perf_counter()
+    solver = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, tensor, alpha0=ALPHA0, alpha1=ALPHA1,
+                         params=sg.NewmarkParams(dt=c["dt"]),
+                         options=sg.SgOptions(tol=1e-30, max_iter=args.steps), rank=args.solo_rank,
+                         world_size=args.solo_world, solo=True)
+    setup_s = time.perf_counter() - t0
+    rhs = np.sin(0.001 * np.arange(solver.n_global) + 0.3)
+    solver.pcg(rhs)  # warm-up (graph capture)
+    solver.reset_stats()
+    _, rep = solver.pcg(rhs)
+    st = solver.stats()
+    torch.cuda.synchronize()
+    plan = sg.ShardPlan(nx, nx, c["px"], c["px"], args.solo_world, args.solo_rank)
+    line = {"mode": "solo-rank loopback (one shard on one GPU; exchanges deliver zeros; not a multi-GPU measurement)",
+            "config": {"workload": workload_desc(name, c), "world": args.solo_world, "rank": args.solo_rank,
+                       "rank_grid": [plan.rx, plan.ry], "owned_subdomains": int(plan.n_sub_owned),
+                       "local_interface_nodes": int(plan.n_iface), "halo_peers": plan.peers.tolist(),
+                       "halo_doubles_per_exchange": int(len(plan.peer_idx)) * solver.n_terms},
+            "device_bytes": solver.device_bytes, "setup_s": setup_s, "pcg_iterations": rep["iterations"],
+            "ms_per_pcg_iteration": st["pcg_ms"] / max(rep["iterations"], 1)}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -176,6 +209,9 @@ def main():
                     help="reduced-memory mode (S_s not stored, applied through the interior solve)")
     ap.add_argument("--force-shard", action="store_true",
                     help="test hook: the sharded code path (NCCL communicator) even on one rank")
+    ap.add_argument("--solo-rank", type=int, default=None,
+                    help="loopback: construct only this rank of a --solo-world decomposition on one GPU")
+    ap.add_argument("--solo-world", type=int, default=2)
     ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
                     help="N>1: shard the subdomains over the ranks (one problem, NCCL sums) or run N replicas")
     args = ap.parse_args()
@@ -187,6 +223,8 @@ def main():
     import torch
     import paper_2512_23027_b200 as sg
 
+    if args.solo_rank is not None:
+        return run_solo(args, c, args.config, sg)
     rank, world, local = dist_env()
     if world > 1 or args.force_shard:
         import torch.distributed as dist
@@ -200,7 +238,7 @@ def main():
     node = sg.nearest_node(nx, nx, 0.5, 0.5)
     shard = (world > 1 and args.mode == "shard") or args.force_shard
     kw = {}
-    if shard:  # rank r owns subdomains shard_plan(n_sub, N)[r]; the NCCL id travels over torch.distributed
+    if shard:  # rank r owns a 2D block of subdomains (sgw_shard_plan); the NCCL id travels over torch.distributed
         ids = [sg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(ids, src=0)
         kw = dict(rank=rank, world_size=world, nccl_id=ids[0])
@@ -282,8 +320,9 @@ def main():
         "data": "synthetic (deterministic KLE/PCE inputs of the config; seeds have no effect on the SG solve)",
         "config": {"workload": workload_desc(args.config, c), "GDOF": gdof / 1e9,
                    "parallelism": "single GPU" if world == 1 else (
-                       f"{world} GPUs, subdomains sharded {[len(r) for r in sg.shard_plan(c['px'] ** 2, world)]}, "
-                       "interface sums by ncclAllReduce" if shard else f"{world} independent replicas"),
+                       f"{world} GPUs, 2D blocks of subdomains {[len(r) for r in sg.shard_plan(c['px'], c['px'], world)]}, "
+                       "interface halo by ncclSend/ncclRecv, coarse vector + CG scalars by ncclAllReduce, "
+                       "phase-split PCG in a CUDA graph (WHILE node)" if shard else f"{world} independent replicas"),
                    "l2": "inputs larger than L2: S+Q tiles stream ~2.7 GB per PCG iteration (L2 126 MB)",
                    **({"mode": "reduced-memory (implicit Schur: S_s applied through the interior sweep)"}
                       if args.implicit_schur else {})},

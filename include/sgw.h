@@ -202,6 +202,11 @@ int sgw_nccl_unique_id(void* out128);
  * by its own host thread, exchange through a host-synchronised group
  * instead of NCCL.  Same ownership and results as the NCCL path.           */
 int sgw_local_group_new(int world_size, void** group);
+/* One rank of a world_size-rank decomposition constructed alone on one device
+ * (no peers: every exchange delivers zeros, the coarse matrix holds only this
+ * rank's subdomains).  For per-rank memory and shard-kernel timing of
+ * configurations that need several GPUs (C4); results are not physical.     */
+int sgw_create_solo(const sgw_problem* problem, int world_size, int rank, sgw_solver** out);
 int sgw_local_group_free(void* group);
 int sgw_create_local_group(const sgw_problem* problem, int world_size, int rank, void* group,
                            sgw_solver** out);

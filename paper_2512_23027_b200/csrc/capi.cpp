@@ -136,6 +136,19 @@ int sgw_create_local_group(const sgw_problem* p, int world_size, int rank, void*
   });
 }
 
+int sgw_create_solo(const sgw_problem* p, int world_size, int rank, sgw_solver** out) {
+  return guard([&] {
+    if (!out) throw Error(SGW_EINVAL, "null argument");
+    Problem P = problem_from(p);
+    P.rank = rank, P.world = world_size;
+    if (rank < 0 || rank >= world_size || world_size > P.px * P.py)
+      throw Error(SGW_EINVAL, "rank / world_size out of range");
+    auto s = std::make_unique<sgw_solver>();
+    s->g = std::make_unique<GpuSolver>(std::move(P), make_solo_comm(rank, world_size));
+    *out = s.release();
+  });
+}
+
 int sgw_local_group_new(int world_size, void** group) {
   return guard([&] {
     if (!group || world_size < 1) throw Error(SGW_EINVAL, "bad argument");

@@ -633,6 +633,7 @@ double GpuSolver::dot_host(const double* a, const double* b, long long len, bool
 // true residual, restart from it (without resetting p) if the check fails.
 int GpuSolver::pcg(const double* b, double* x, bool* converged, std::vector<double>* hist) {
   if (fused_ok()) return pcg_fused(b, x, converged, hist);
+  if (phase_ok()) return pcg_phase(b, x, converged, hist);
   cudaEventRecord(ev_[0], st_);
   const long long N = NG;
   const int grid = red_grid(N);

@@ -55,7 +55,23 @@ struct FusedPcg {
   double* tphase;                // 8 accumulated phase times (ns), CTA 0
   RangePack rs, rq, rp;          // contiguous tile ranges per CTA of S, Q and Psi^T
   int nst, maxlen;               // ring stages; longest local vector (doubles)
+  // phase-split PCG (sharded runs, pcg_phase_kernel): halo of the shared
+  // interface nodes, ownership mask of the dots, the buffer the collectives
+  // reduce ([0, NC) coarse d, then XR rr | b.b, XPQ p.q, XRZ r.z, XRT rt.rt)
+  // and the device-resident CG state
+  HaloDev H;
+  const double* own;             // NG, null: every entry owned
+  double* xch;
+  double* sc;                    // [SC_RZ] r.z, [SC_BNORM] ||b||, [SC_BETA]
+  int* st;                       // [ST_IT], [ST_HL], [ST_EXIT], [ST_FIRST], [ST_PFIRST]
+  unsigned long long cond;       // conditional handle of the graph's WHILE loop
+  int use_cond;
 };
+enum { SC_RZ = 0, SC_BNORM = 1, SC_BETA = 2 };
+enum { ST_IT = 0, ST_HL = 1, ST_EXIT = 2, ST_FIRST = 3, ST_PFIRST = 4 };
+// ST_EXIT: 0 running, 1 recurrence residual <= tol (confirm), 2 max_iter,
+// 3 b = 0, 4 converged (true residual), 5 true residual failed (restart)
+enum { EX_RUN = 0, EX_CHECK = 1, EX_MAXIT = 2, EX_ZERO = 3, EX_CONV = 4, EX_RESTART = 5 };
 
 extern __shared__ __align__(128) double dyn_smem[];  // ring stages, local vector, accumulator
 
@@ -596,6 +612,305 @@ __global__ void __launch_bounds__(256) walk_kernel(RangePack P, const double* __
   __syncthreads();
 }
 
+// ------------------------------------------------- phase-split PCG -------
+// The persistent kernel's iteration cut at its three cross-rank sums, for
+// sharded runs.  One iteration = three cooperative launches with
+// the exchanges between them (captured with them in one CUDA graph whose
+// WHILE conditional node keeps the convergence test on the device):
+//   A  combine z's shared nodes; beta; q_partial = sum_{s owned} R_s^T S_s R_s p
+//      (tile walk + scatter), p.q partial, pack q      -> halo(q), allreduce(p.q)
+//   B  combine q; alpha; p, x, r updates; r.r partial (owned nodes); NN2 up to
+//      the coarse partial d                            -> allreduce(d, r.r)
+//   C  convergence test (loop condition); u_c = F_cc^-1 d; Psi u_c; z partial,
+//      r.z partial, pack z                             -> halo(z), allreduce(r.z)
+// p.q and r.z are sums of per-subdomain dots (p.q = sum_s (R_s p).(S_s R_s p),
+// r.z = sum_s (R_s r).(D_s zeta_s)), so their partials need no halo.
+enum { PH_INIT = 0, PH_C0, PH_A, PH_B, PH_C, PH_T1, PH_T2, PH_R, PH_RC0 };
+
+__device__ __forceinline__ bool owned(const FusedPcg& A, long long q) { return !A.own || A.own[q] != 0.0; }
+
+// Q_s f_r, Psi_s^T f_r tile walks, then the coarse partial d -> xch[0, NC)
+__device__ void ph_nn2a(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_group& g, double* xs, double* acc) {
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (long long)gridDim.x * blockDim.x >> 5;
+  const bool coarse = A.NC > 0;
+  range_phase(R, 2, A.rq, coarse ? &A.rp : nullptr, xs, acc, sm,
+              [&](int s, int i) { return __ldcg(A.fr + A.q_xoff[s] + i); });
+  if (coarse) {
+    R.pre_kind = 3;
+    range_phase(R, 3, A.rp, nullptr, xs, acc, sm, [&](int s, int i) {
+      const int o = i - kTile * A.rp.nI[s];
+      return o >= 0 ? __ldcg(A.fr + A.roff[s] + o) : 0.0;
+    });
+  }
+  g.sync();
+  if (!coarse) return;
+  for (long long qc = blockIdx.x + (long long)(threadIdx.x >> 5) * gridDim.x; qc < A.NC; qc += nwarps) {
+    const int j = int(qc / A.n_corner), gc = int(qc % A.n_corner), e = lane >> 3, kk = lane & 7;
+    double d = 0.0;
+    if (e < A.cinv_cnt[gc]) {
+      const int s = A.cinv_s[4 * gc + e], c = j * A.nc[s] + A.cinv_c[4 * gc + e];
+      const int len = kTile * (A.rp.nI[s] + A.rp.nJ[s]), n = A.rp.ncta[s];
+      const double* pp = A.rp.part + A.rp.pbase[s] + c;
+      for (int k = kk; k < n; k += 8) d -= __ldcg(pp + (long long)k * len);
+      if (kk == 0) d += __ldcg(A.fc + A.coff[s] + c);
+    }
+    d = warp_sum(d);
+    if (lane == 0) A.xch[qc] = d;  // this rank's partial of B^T d
+  }
+}
+
+// u_c = F_cc^-1 d (d summed over ranks in xch), Psi_s B_s u_c, then the local
+// partial z = sum_{s owned} R_s^T D_s zeta_s (packed for the halo); returns the
+// grid total of the partial r.z (valid in every thread)
+__device__ double ph_nn2b(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_group& g, double* xs, double* acc) {
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const bool coarse = A.NC > 0;
+  if (coarse) {
+    const bool dsm = A.NC <= 2 * A.maxlen;
+    if (dsm) {
+      for (int c = threadIdx.x; c < A.NC; c += blockDim.x) xs[c] = __ldcg(A.xch + c);
+      __syncthreads();
+    }
+    const int nw = blockDim.x >> 5;
+    for (long long row = blockIdx.x + (long long)(threadIdx.x >> 5) * gridDim.x; row < A.NC;
+         row += (long long)nw * gridDim.x) {
+      const double* col = A.Finv + row * A.NC;
+      auto dv = [&](int c) { return dsm ? xs[c] : __ldcg(A.xch + c); };
+      const int h = int((row * A.NC) & 1);
+      const int n2 = (A.NC - h) >> 1;
+      const double2* c2 = reinterpret_cast<const double2*>(col + h);
+      double a = 0.0;
+#pragma unroll kUnroll
+      for (int k = lane; k < n2; k += 32) {
+        const double2 v = __ldg(c2 + k);
+        a += v.x * dv(h + 2 * k) + v.y * dv(h + 2 * k + 1);
+      }
+      if (lane == 0) {
+        if (h) a += __ldg(col) * dv(0);
+        if ((A.NC - h) & 1) a += __ldg(col + A.NC - 1) * dv(A.NC - 1);
+      }
+      a = warp_sum(a);
+      if (lane == 0) {
+        A.uco[row] = a;
+        const int j = int(row / A.n_corner), gc = int(row % A.n_corner);
+        for (int e = 0; e < A.cinv_cnt[gc]; ++e) {
+          const int s = A.cinv_s[4 * gc + e];
+          A.ucl[A.coff[s] + (long long)j * A.nc[s] + A.cinv_c[4 * gc + e]] = a;
+        }
+      }
+    }
+    g.sync();
+    range_phase(R, 3, A.rp, nullptr, xs, acc, sm, [&](int s, int i) {
+      return i < A.NT * A.nc[s] ? __ldcg(A.ucl + A.coff[s] + i) : 0.0;
+    });
+    g.sync();
+  }
+  double rz = 0.0;
+  for (long long q = gtid; q < A.NG; q += gstride) {
+    const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
+    double zq = 0.0;
+    for (int e = 0; e < A.inv_cnt[gq]; ++e) {
+      const int s = A.inv_s[4 * gq + e], pp = A.inv_p[4 * gq + e];
+      const int kind = A.pkind[A.ip_off[s] + pp];
+      const double wgt = A.iface_w[A.ip_off[s] + pp];
+      double v;
+      if (kind >= 0) {
+        const int ar = j * A.nr[s] + kind;
+        v = range_reduce(A.rq, s, ar);
+        if (coarse) v -= rect_reduce(A.rp, s, kTile * A.rp.nI[s] + ar);
+      } else {
+        v = coarse ? __ldcg(A.ucl + A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)) : 0.0;
+      }
+      zq += wgt * v;
+    }
+    A.z[q] = zq;
+    write_local_s(A, A.li_z, q, zq);  // shared nodes are rewritten after their halo
+    halo_pack_one(A.H, j, gq, zq);
+    rz += A.r[q] * zq;
+  }
+  return grid_sum(rz, A.part, 4, g, sm);
+}
+
+__global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
+  cg::grid_group g = cg::this_grid();
+  __shared__ Smem sm;
+  __shared__ unsigned long long ring_bar[kMaxRing];
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
+  const bool leader = gtid == 0;
+  Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0};
+  double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;
+  double* xacc = xs + A.maxlen;
+  for (int i = threadIdx.x; i < A.nst * kTile * kTile; i += blockDim.x) dyn_smem[i] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < A.nst; ++i) mb_init(&ring_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int NC = A.NC;
+  switch (which) {
+    case PH_INIT: {  // x = 0, r = b, NN2 inputs of b, b.b; NN2 up to d
+      double acc = 0.0;
+      for (long long q = gtid; q < A.NG; q += gstride) {
+        const double bv = A.b[q];
+        A.x[q] = 0.0;
+        A.r[q] = bv;
+        if (owned(A, q)) acc += bv * bv;
+        write_local(A, q, bv);
+      }
+      const double bb = grid_sum(acc, A.part, 0, g, sm);
+      if (leader) {
+        A.xch[NC] = bb;
+        A.st[ST_IT] = 0, A.st[ST_HL] = 0, A.st[ST_EXIT] = EX_RUN, A.st[ST_FIRST] = 1, A.st[ST_PFIRST] = 1;
+      }
+      ph_nn2a(A, R, sm, g, xs, xacc);
+      break;
+    }
+    case PH_C0:
+    case PH_RC0: {  // (start: ||b|| from the sums) then the rest of NN2
+      if (which == PH_C0) {
+        const double bnorm = sqrt(__ldcg(A.xch + NC));
+        g.sync();
+        if (leader) {
+          A.sc[SC_BNORM] = bnorm;
+          A.hist[0] = bnorm == 0.0 ? 0.0 : 1.0;
+          A.st[ST_HL] = 1;
+          if (bnorm == 0.0) A.st[ST_EXIT] = EX_ZERO;
+        }
+        if (bnorm == 0.0) break;
+      }
+      const double rz = ph_nn2b(A, R, sm, g, xs, xacc);
+      if (leader) A.xch[NC + 2] = rz;
+      break;
+    }
+    case PH_A: {  // complete z, beta, q_partial = S p_new, p.q partial
+      for (long long t = gtid; t < (long long)A.H.n_shared * A.NT; t += gstride) {
+        const int c = int(t % A.H.n_shared), j = int(t / A.H.n_shared);
+        const long long q = (long long)j * A.n_iface + A.H.cnode[c];
+        const double zq = halo_combine_one(A.H, c, j, A.z[q]);
+        A.z[q] = zq;
+        write_local_s(A, A.li_z, q, zq);
+      }
+      const double rz_new = __ldcg(A.xch + NC + 2);
+      const bool first = A.st[ST_FIRST] != 0;
+      const double beta = first ? 0.0 : rz_new / A.sc[SC_RZ];
+      g.sync();
+      if (leader) A.sc[SC_RZ] = rz_new, A.sc[SC_BETA] = beta, A.st[ST_PFIRST] = first, A.st[ST_FIRST] = 0;
+      s_tiles_phase(A, R, sm, xs, xacc, 0, first, beta);
+      g.sync();
+      double acc = 0.0;
+      for (long long q = gtid; q < A.NG; q += gstride) {
+        const double y = s_reduce(A, q);
+        A.q[q] = y;
+        halo_pack_one(A.H, int(q / A.n_iface), int(q % A.n_iface), y);
+        acc += y * (first ? A.z[q] : A.z[q] + beta * A.p[q]);
+      }
+      const double pq = grid_sum(acc, A.part, 1, g, sm);
+      if (leader) A.xch[NC + 1] = pq;
+      break;
+    }
+    case PH_B: {  // complete q; p, x, r updates; r.r; NN2 up to d
+      for (long long t = gtid; t < (long long)A.H.n_shared * A.NT; t += gstride) {
+        const int c = int(t % A.H.n_shared), j = int(t / A.H.n_shared);
+        const long long q = (long long)j * A.n_iface + A.H.cnode[c];
+        A.q[q] = halo_combine_one(A.H, c, j, A.q[q]);
+      }
+      const bool first = A.st[ST_PFIRST] != 0;
+      const double beta = A.sc[SC_BETA], alpha = A.sc[SC_RZ] / __ldcg(A.xch + NC + 1);
+      g.sync();
+      double acc = 0.0;
+      for (long long q = gtid; q < A.NG; q += gstride) {
+        const double pn = first ? A.z[q] : A.z[q] + beta * A.p[q];
+        A.p[q] = pn;
+        write_local_s(A, A.li_p, q, pn);
+        A.x[q] += alpha * pn;
+        const double rn = A.r[q] - alpha * __ldcg(A.q + q);
+        A.r[q] = rn;
+        if (owned(A, q)) acc += rn * rn;
+        write_local(A, q, rn);
+      }
+      const double rr = grid_sum(acc, A.part, 2, g, sm);
+      if (leader) A.xch[NC] = rr;
+      ph_nn2a(A, R, sm, g, xs, xacc);
+      break;
+    }
+    case PH_C: {  // convergence test (the loop condition), then the rest of NN2
+      const int it = A.st[ST_IT] + 1, hl = A.st[ST_HL];
+      const double rel = sqrt(__ldcg(A.xch + NC)) / A.sc[SC_BNORM];
+      const int ex = rel <= A.tol ? EX_CHECK : (it >= A.max_iter ? EX_MAXIT : EX_RUN);
+      g.sync();
+      if (leader) {
+        A.st[ST_IT] = it;
+        if (hl < A.hist_cap) A.hist[hl] = rel;
+        A.st[ST_HL] = hl + 1;
+        A.st[ST_EXIT] = ex;
+        if (ex != EX_RUN && A.use_cond) cudaGraphSetConditional(A.cond, 0);
+      }
+      if (ex != EX_RUN) break;
+      const double rz = ph_nn2b(A, R, sm, g, xs, xacc);
+      if (leader) A.xch[NC + 2] = rz;
+      break;
+    }
+    case PH_T1: {  // q_partial = S x (true residual, src/pcg.cpp:31-40)
+      for (long long q = gtid; q < A.NG; q += gstride) write_local_s(A, A.li_x, q, A.x[q]);
+      g.sync();
+      s_tiles_phase(A, R, sm, xs, xacc, 1, false, 0.0);
+      g.sync();
+      for (long long q = gtid; q < A.NG; q += gstride) {
+        const double y = s_reduce(A, q);
+        A.q[q] = y;
+        halo_pack_one(A.H, int(q / A.n_iface), int(q % A.n_iface), y);
+      }
+      break;
+    }
+    case PH_T2: {  // r_true = b - S x (kept in q), its squared norm
+      for (long long t = gtid; t < (long long)A.H.n_shared * A.NT; t += gstride) {
+        const int c = int(t % A.H.n_shared), j = int(t / A.H.n_shared);
+        const long long q = (long long)j * A.n_iface + A.H.cnode[c];
+        A.q[q] = halo_combine_one(A.H, c, j, A.q[q]);
+      }
+      g.sync();
+      double acc = 0.0;
+      for (long long q = gtid; q < A.NG; q += gstride) {
+        const double v = A.b[q] - __ldcg(A.q + q);
+        A.q[q] = v;
+        if (owned(A, q)) acc += v * v;
+      }
+      const double rt = grid_sum(acc, A.part, 3, g, sm);
+      if (leader) A.xch[NC + 3] = rt;
+      break;
+    }
+    case PH_R: {  // restart from the true residual (p kept): r = r_true, NN2 up to d
+      for (long long q = gtid; q < A.NG; q += gstride) {
+        const double v = __ldcg(A.q + q);
+        A.r[q] = v;
+        write_local(A, q, v);
+      }
+      if (leader) A.st[ST_EXIT] = EX_RUN;
+      g.sync();
+      ph_nn2a(A, R, sm, g, xs, xacc);
+      break;
+    }
+    default:
+      break;
+  }
+  if (threadIdx.x == 0)
+    for (int c = R.consumed; c < R.issued; ++c) mb_wait(&R.full[c % R.nst], (c / R.nst) & 1);
+  __syncthreads();
+}
+
+// the true-residual verdict (src/pcg.cpp:31-40): converged, or restart
+__global__ void pcg_phase_verdict_kernel(FusedPcg A) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double rel = sqrt(A.xch[A.NC + 3]) / A.sc[SC_BNORM];
+  const int hl = A.st[ST_HL];
+  if (hl < A.hist_cap) A.hist[hl] = rel;
+  A.st[ST_HL] = hl + 1;
+  A.st[ST_EXIT] = rel <= A.tol ? EX_CONV : EX_RESTART;
+}
+
 // --------------------------------------------------------------- host ----
 // Contiguous tile ranges per CTA over a pack whose matrix s holds tiles
 // [tile_base[s], tile_base[s + 1]) in row-major order: lower tiles of an
@@ -722,6 +1037,13 @@ void GpuSolver::setup_fused_pcg() {
   SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fused_smem_));
   SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pcg_fused_kernel, 256, fused_smem_));
+  {  // the phase-split kernel walks the same CTA ranges: same grid, co-resident too
+    int nb2 = 0;
+    SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)fused_smem_));
+    SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, pcg_phase_kernel, 256, fused_smem_));
+    nb = std::min(nb, nb2);
+  }
   fused_grid_ = std::max(1, std::min(nb, bps)) * sms;
   SGW_CUDA(cudaFuncSetAttribute((const void*)walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fused_smem_));
@@ -735,16 +1057,221 @@ void GpuSolver::setup_fused_pcg() {
     psi_ncs_.upload(ncs);
   }
   ucl_.alloc(std::max<long long>(1, coff_.back())), ucl_.zero(st_);
-  if (comm_) {      // sharded: the host-driven loop with a sum over ranks after each scatter
-    use_fused_ = false;
-    return;
-  }
   fused_part_.alloc(size_t(8) * fused_grid_);
   fused_out_.alloc(4);
   fused_hist_.alloc(P.max_iter + 8);
   for (DBuf<double>* b : {&li_z_, &li_p_, &li_xx_}) b->alloc(Sp.xlen), b->zero(st_);  // padding stays 0
+  ph_xch_.alloc(NC + 8), ph_xch_.zero(st_);
+  ph_sc_.alloc(8), ph_sc_.zero(st_);
+  ph_st_.alloc(8), ph_st_.zero(st_);
+  // sharded runs (and SGW_PCG=phase): the phase-split PCG; SGW_PCG=host: the host-driven loop
   const char* e = std::getenv("SGW_PCG");
-  use_fused_ = !(e && std::string(e) == "host");
+  const std::string mode = e ? e : "";
+  use_fused_ = !comm_ && mode != "host" && mode != "phase";
+  use_phase_ = mode != "host";
+}
+
+FusedPcg GpuSolver::fused_args(const double* b, double* x) const {
+  FusedPcg A{};
+  A.NG = NG;
+  A.n_iface = G.n_iface, A.NT = NT, A.NS = NS, A.n_corner = G.n_corner, A.NC = NC;
+  A.max_iter = P.max_iter, A.hist_cap = (int)fused_hist_.n, A.tol = P.tol;
+  A.b = b, A.x = x, A.r = vr.p, A.z = vz.p, A.p = vp.p, A.q = vq.p;
+  A.s_xoff = Sp.d_xoff.p, A.q_xoff = Qp.d_xoff.p;
+  A.fr = r_x.p, A.fc = c_f.p;
+  A.inv_cnt = inv_cnt.p, A.inv_s = inv_s.p, A.inv_p = inv_p.p, A.ip_off = ip_off.p, A.ng = ng_d.p, A.nr = nr_d.p,
+  A.nc = nc_d.p, A.pkind = pkind_.p, A.iface_w = iface_w.p;
+  A.cinv_cnt = cinv_cnt.p, A.cinv_s = cinv_s.p, A.cinv_c = cinv_c.p;
+  A.roff = d_roff.p, A.coff = d_coff.p;
+  A.Finv = Finv.p, A.dco = dcoarse.p, A.uco = ucoarse.p, A.ucl = ucl_.p;
+  A.part = fused_part_.p, A.out = fused_out_.p, A.hist = fused_hist_.p;
+  A.li_z = li_z_.p, A.li_p = li_p_.p, A.li_x = li_xx_.p;
+  A.tphase = KP.on ? tphase_.p : nullptr;
+  A.rs = RangePack{Sp.tiles.p, nullptr, nullptr, Sp.d_ntile.p, nullptr, 0, rs_.t_first.p, rs_.start.p, rs_.c0.p,
+                   rs_.ncta.p, rs_.pbase.p, rs_.part.p};
+  A.rq = RangePack{Qp.tiles.p, nullptr, nullptr, Qp.d_ntile.p, nullptr, 0, rq_.t_first.p, rq_.start.p, rq_.c0.p,
+                   rq_.ncta.p, rq_.pbase.p, rq_.part.p};
+  A.rp = RangePack{psi_tiles_.p, psi_toff_.p, psi_tbytes_.p, psi_dnI_.p, psi_dnJ_.p, 1, rp_.t_first.p, rp_.start.p,
+                   rp_.c0.p, rp_.ncta.p, rp_.pbase.p, rp_.part.p};
+  A.nst = fused_nst_, A.maxlen = fused_maxlen_;
+  A.H = halo_dev();
+  A.own = dot_mask();
+  A.xch = ph_xch_.p, A.sc = ph_sc_.p, A.st = ph_st_.p;
+  A.cond = 0, A.use_cond = 0;
+  return A;
+}
+
+// ------------------------------------------------ phase-split PCG (host) --
+// Sequences of the phase-split solve (see pcg_phase_kernel).  xch layout:
+// [0, NC) d, NC r.r | b.b, NC+1 p.q, NC+2 r.z, NC+3 rt.rt.
+void GpuSolver::phase_seq(int which, const FusedPcg& A0) {
+  FusedPcg A = A0;
+  auto K = [&](int ph) {
+    void* args[] = {&A, &ph};
+    SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_phase_kernel, dim3(fused_grid_), dim3(256), args,
+                                         fused_smem_, st_));
+    SGW_LAUNCHED();
+  };
+  auto AR = [&](int off, int cnt) {
+    if (comm_) comm_->allreduce_sum(ph_xch_.p + off, cnt, st_);
+  };
+  auto XH = [&]() {
+    if (comm_ && !G.halo.peers.empty()) halo_exchange();
+  };
+  switch (which) {
+    case 0:  // start: x = 0, r = b, z = NN2(b), r.z
+      K(PH_INIT), AR(0, NC + 1), K(PH_C0), XH(), AR(NC + 2, 1);
+      break;
+    case 1:  // one iteration
+      K(PH_A), XH(), AR(NC + 1, 1), K(PH_B), AR(0, NC + 1), K(PH_C), XH(), AR(NC + 2, 1);
+      break;
+    case 2:  // true residual and its verdict
+      K(PH_T1), XH(), K(PH_T2), AR(NC + 3, 1);
+      pcg_phase_verdict_kernel<<<1, 32, 0, st_>>>(A);
+      SGW_LAUNCHED();
+      break;
+    case 3:  // restart from the true residual
+      K(PH_R), AR(0, NC), K(PH_RC0), XH(), AR(NC + 2, 1);
+      break;
+  }
+}
+
+// Graphs of the four sequences; the iteration is the body of a WHILE
+// conditional node (the loop condition is set by the PH_C kernel), so a solve
+// runs without host synchronisation until the recurrence residual meets the
+// tolerance.  Rebuilt when the solve's b / x buffers change.
+bool GpuSolver::build_phase_graphs(const double* b, double* x) {
+  for (auto& ge : ph_graph_)
+    if (ge) cudaGraphExecDestroy(ge), ge = nullptr;
+  ph_graph_b_ = b, ph_graph_x_ = x;
+  const bool kp = KP.on;
+  KP.on = false;
+  const FusedPcg A = fused_args(b, x);
+  bool ok = true;
+  const long long l0 = g_launches.load();
+  for (int k = 0; k < 4 && ok; ++k) {
+    const long long c0 = g_launches.load();
+    cudaGraph_t gr = nullptr;
+    if (k == 1) {  // WHILE { iteration }
+      ok = cudaGraphCreate(&gr, 0) == cudaSuccess;
+      cudaGraphConditionalHandle h = 0;
+      ok = ok && cudaGraphConditionalHandleCreate(&h, gr, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      ok = ok && cudaGraphAddNode(&node, gr, nullptr, 0, &cp) == cudaSuccess;
+      if (ok) {
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        FusedPcg Ab = A;
+        Ab.cond = h, Ab.use_cond = 1;
+        ok = cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
+             cudaSuccess;
+        if (ok) {
+          try {
+            phase_seq(1, Ab);
+          } catch (const Error&) {
+            ok = false;
+          }
+          cudaGraph_t out = nullptr;
+          ok = cudaStreamEndCapture(st_, &out) == cudaSuccess && ok;
+        }
+      }
+    } else {
+      ok = cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+      if (ok) {
+        try {
+          phase_seq(k, A);
+        } catch (const Error&) {
+          ok = false;
+        }
+        ok = cudaStreamEndCapture(st_, &gr) == cudaSuccess && ok;
+      }
+    }
+    ok = ok && cudaGraphInstantiate(&ph_graph_[k], gr, 0) == cudaSuccess;
+    if (gr) cudaGraphDestroy(gr);
+    ph_graph_launches_[k] = g_launches.load() - c0;
+  }
+  g_launches = l0;  // counted per replay
+  KP.on = kp;
+  if (!ok) {
+    cudaGetLastError();  // clear a capture / instantiation failure: fall back to stream launches
+    for (auto& ge : ph_graph_)
+      if (ge) cudaGraphExecDestroy(ge), ge = nullptr;
+    ph_graph_b_ = nullptr, ph_graph_x_ = nullptr;
+  }
+  return ok;
+}
+
+int GpuSolver::pcg_phase(const double* b, double* x, bool* converged, std::vector<double>* hist) {
+  cudaEventRecord(ev_[0], st_);
+  if (!h_st_) SGW_CUDA(cudaMallocHost(&h_st_, 8 * sizeof(int)));
+  const bool graphs = (!comm_ || comm_->capturable()) && ph_graph_ok_;
+  if (graphs && (ph_graph_b_ != b || ph_graph_x_ != x || !ph_graph_[0]))
+    ph_graph_ok_ = build_phase_graphs(b, x);
+  const bool use_graphs = graphs && ph_graph_ok_;
+  const FusedPcg A = fused_args(b, x);
+  auto run = [&](int k) {
+    if (use_graphs) {
+      SGW_CUDA(cudaGraphLaunch(ph_graph_[k], st_));
+      g_launches += ph_graph_launches_[k];
+    } else {
+      phase_seq(k, A);
+    }
+  };
+  auto state = [&]() {
+    SGW_CUDA(cudaMemcpyAsync(h_st_, ph_st_.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+    SGW_CUDA(cudaStreamSynchronize(st_));
+    if (comm_) comm_->poll();
+    return h_st_[ST_EXIT];
+  };
+  auto loop = [&]() {
+    if (use_graphs) {
+      run(1);
+      return state();
+    }
+    for (;;) {  // host-driven iterations (non-capturable exchange): one state read per iteration
+      run(1);
+      const int ex = state();
+      if (ex != EX_RUN) return ex;
+    }
+  };
+  run(0);
+  int ex = state();
+  bool conv = false;
+  if (ex == EX_ZERO) {
+    conv = true;
+  } else {
+    for (;;) {
+      ex = loop();
+      if (ex != EX_CHECK) break;  // max_iter without meeting the tolerance
+      run(2);
+      ex = state();
+      if (ex == EX_CONV) {
+        conv = true;
+        break;
+      }
+      if (h_st_[ST_IT] >= P.max_iter) break;
+      run(3);
+    }
+  }
+  cudaEventRecord(ev_[1], st_);
+  SGW_CUDA(cudaEventSynchronize(ev_[1]));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev_[0], ev_[1]);
+  const int it = h_st_[ST_IT], hl = std::min<int>(h_st_[ST_HL], (int)fused_hist_.n);
+  T.pcg_ms += ms;
+  T.iterations += it;
+  T.matvecs += it;
+  T.nn2s += it;
+  std::vector<double> h(hl);
+  if (hl) SGW_CUDA(cudaMemcpy(h.data(), fused_hist_.p, hl * sizeof(double), cudaMemcpyDeviceToHost));
+  last_rel = hl ? h.back() : 0.0;
+  if (hist) *hist = std::move(h);
+  *converged = conv;
+  return it;
 }
 
 RangePack GpuSolver::range_pack(int which) const {
@@ -792,28 +1319,7 @@ int GpuSolver::pcg_fused(const double* b, double* x, bool* converged, std::vecto
 void GpuSolver::pcg_fused_launch(const double* b, double* x) {
   if (!h_fused_) SGW_CUDA(cudaMallocHost(&h_fused_, (4 + fused_hist_.n) * sizeof(double)));
   cudaEventRecord(ev_[0], st_);
-  FusedPcg A{};
-  A.NG = NG;
-  A.n_iface = G.n_iface, A.NT = NT, A.NS = NS, A.n_corner = G.n_corner, A.NC = NC;
-  A.max_iter = P.max_iter, A.hist_cap = (int)fused_hist_.n, A.tol = P.tol;
-  A.b = b, A.x = x, A.r = vr.p, A.z = vz.p, A.p = vp.p, A.q = vq.p;
-  A.s_xoff = Sp.d_xoff.p, A.q_xoff = Qp.d_xoff.p;
-  A.fr = r_x.p, A.fc = c_f.p;
-  A.inv_cnt = inv_cnt.p, A.inv_s = inv_s.p, A.inv_p = inv_p.p, A.ip_off = ip_off.p, A.ng = ng_d.p, A.nr = nr_d.p,
-  A.nc = nc_d.p, A.pkind = pkind_.p, A.iface_w = iface_w.p;
-  A.cinv_cnt = cinv_cnt.p, A.cinv_s = cinv_s.p, A.cinv_c = cinv_c.p;
-  A.roff = d_roff.p, A.coff = d_coff.p;
-  A.Finv = Finv.p, A.dco = dcoarse.p, A.uco = ucoarse.p, A.ucl = ucl_.p;
-  A.part = fused_part_.p, A.out = fused_out_.p, A.hist = fused_hist_.p;
-  A.li_z = li_z_.p, A.li_p = li_p_.p, A.li_x = li_xx_.p;
-  A.tphase = KP.on ? tphase_.p : nullptr;
-  A.rs = RangePack{Sp.tiles.p, nullptr, nullptr, Sp.d_ntile.p, nullptr, 0, rs_.t_first.p, rs_.start.p, rs_.c0.p,
-                   rs_.ncta.p, rs_.pbase.p, rs_.part.p};
-  A.rq = RangePack{Qp.tiles.p, nullptr, nullptr, Qp.d_ntile.p, nullptr, 0, rq_.t_first.p, rq_.start.p, rq_.c0.p,
-                   rq_.ncta.p, rq_.pbase.p, rq_.part.p};
-  A.rp = RangePack{psi_tiles_.p, psi_toff_.p, psi_tbytes_.p, psi_dnI_.p, psi_dnJ_.p, 1, rp_.t_first.p, rp_.start.p,
-                   rp_.c0.p, rp_.ncta.p, rp_.pbase.p, rp_.part.p};
-  A.nst = fused_nst_, A.maxlen = fused_maxlen_;
+  FusedPcg A = fused_args(b, x);
   void* args[] = {&A};
   SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_fused_kernel, dim3(fused_grid_), dim3(256), args,
                                        fused_smem_, st_));

@@ -443,6 +443,9 @@ GpuSolver::~GpuSolver() {
   if (graph_pc_) cudaGraphExecDestroy(graph_pc_);
   if (h_scal_) cudaFreeHost(h_scal_);
   if (h_fused_) cudaFreeHost(h_fused_);
+  if (h_st_) cudaFreeHost(h_st_);
+  for (auto& ge : ph_graph_)
+    if (ge) cudaGraphExecDestroy(ge);
   if (own_stream_ && st_) cudaStreamDestroy(st_);
 }
 
@@ -733,6 +736,9 @@ void GpuSolver::finish_nn2(std::vector<double>& fcc) {
     SGW_CUDA(cudaMemcpyAsync(fcc.data(), Finv.p, fcc.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
     SGW_CUDA(cudaStreamSynchronize(st_));
   }
+  if (comm_ && comm_->solo())  // one rank alone: corners no owned subdomain touches get a unit row
+    for (int c = 0; c < NC; ++c)
+      if (fcc[(size_t)c * NC + c] == 0.0) fcc[(size_t)c * NC + c] = 1.0;
   fcc_host_ = fcc;
   if (NC > 0) {
     Finv.upload(fcc);

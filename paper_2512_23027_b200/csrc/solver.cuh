@@ -351,6 +351,20 @@ class GpuSolver {
   void pcg_fused_launch(const double* b, double* x);
   int pcg_fused_finish(bool* converged, std::vector<double>* hist);
   bool fused_ok() const { return use_fused_ && !comm_ && P.precond == 0 && !P.implicit_schur; }
+  bool phase_ok() const { return use_phase_ && walk_ok_ && P.precond == 0 && !P.implicit_schur; }
+  // phase-split PCG (pcg_fused.cu): sharded runs, or SGW_PCG=phase on one GPU
+  struct FusedPcg fused_args(const double* b, double* x) const;
+  void phase_seq(int which, const struct FusedPcg& A);
+  bool build_phase_graphs(const double* b, double* x);
+  int pcg_phase(const double* b, double* x, bool* converged, std::vector<double>* hist);
+  bool use_phase_ = true, ph_graph_ok_ = true;
+  DBuf<double> ph_xch_, ph_sc_;
+  DBuf<int> ph_st_;
+  int* h_st_ = nullptr;
+  cudaGraphExec_t ph_graph_[4] = {nullptr, nullptr, nullptr, nullptr};
+  long long ph_graph_launches_[4] = {0, 0, 0, 0};
+  const double* ph_graph_b_ = nullptr;
+  const double* ph_graph_x_ = nullptr;
   double* h_fused_ = nullptr;  // pinned: persistent PCG outputs [4 ints as doubles' room][history]
   DBuf<int> fused_out_;
   RangeBufs rs_, rq_, rp_;

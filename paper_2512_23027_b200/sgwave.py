@@ -100,6 +100,7 @@ def load_library():
     L.sgw_shard_plan.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp]
     L.sgw_local_group_new.argtypes = [ip, C.POINTER(vp)]
     L.sgw_local_group_free.argtypes = [vp]
+    L.sgw_create_solo.argtypes = [C.POINTER(_Problem), ip, ip, C.POINTER(vp)]
     L.sgw_create_local_group.argtypes = [C.POINTER(_Problem), ip, ip, vp, C.POINTER(vp)]
     _LIB = L
     return L
@@ -444,7 +445,7 @@ class SgSolver:
 
     def __init__(self, nx, ny, px, py, coeff, tensor, density=1.0, alpha0=0.5445, alpha1=0.0174,
                  params: NewmarkParams | None = None, options: SgOptions | None = None, *, rank=0, world_size=1,
-                 nccl_id: bytes | None = None, local_group: "LocalGroup | None" = None):
+                 nccl_id: bytes | None = None, local_group: "LocalGroup | None" = None, solo: bool = False):
         """world_size > 1 shards the subdomains over ranks (include/sgw.h): one
         process per GPU with the rank-0 `nccl_id` (nccl_unique_id()), or, for
         tests on one device, one thread per rank sharing a LocalGroup."""
@@ -468,7 +469,9 @@ class SgSolver:
             raise SgInvalidArgument(SGW_EINVAL, "SgSolver: coefficient terms do not match tensor input size")
         self.rank, self.world_size = rank, world_size
         h = C.c_void_p()
-        if local_group is not None:
+        if solo:  # rank `rank` of a world_size decomposition, constructed alone (sgw_create_solo)
+            _check(L.sgw_create_solo(C.byref(prob), world_size, rank, C.byref(h)))
+        elif local_group is not None:
             _check(L.sgw_create_local_group(C.byref(prob), world_size, rank, local_group._g, C.byref(h)))
         else:
             if world_size > 1 and (nccl_id is None or len(nccl_id) != 128):

@@ -87,11 +87,12 @@ def test_pcg_matches_oracle_iterations(gpu, cfg):
     assert np.linalg.norm(x - xc) / np.linalg.norm(xc) <= 1e-8
 
 
-@pytest.mark.parametrize("mode", ["fused", "host"])
+@pytest.mark.parametrize("mode", ["fused", "host", "phase"])
 def test_pcg_drivers_agree_with_oracle(gpu, monkeypatch, mode):
-    # persistent cooperative PCG kernel (default) and the host-driven loop
-    if mode == "host":
-        monkeypatch.setenv("SGW_PCG", "host")
+    # persistent cooperative PCG kernel (default), the host-driven loop, and the
+    # phase-split kernels of the sharded path (CUDA graph, WHILE conditional node)
+    if mode != "fused":
+        monkeypatch.setenv("SGW_PCG", mode)
     nx = 32
     g, c = pair(nx, 4, 2, 0.3, 0.5, 2, 4, 2, 1e-3)
     node = O.nearest_node(nx, nx, 0.5, 0.5)
@@ -250,12 +251,15 @@ def test_ragged_partition_trajectory(gpu, monkeypatch, cs):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("world,case", [(2, (24, 24, 3, 2)), (3, (26, 20, 4, 3)), (4, (16, 16, 2, 2))])
+@pytest.mark.parametrize("world,case", [(2, (24, 24, 3, 2)), (3, (26, 20, 4, 3)), (4, (16, 16, 2, 2)),
+                                        (4, (26, 26, 4, 4)), (6, (24, 24, 3, 4)), (8, (32, 32, 4, 4))])
 def test_sharded_ranks_match_single_gpu(gpu, world, case):
-    # the multi-GPU decomposition (include/sgw.h): ranks own contiguous
-    # subdomain ranges and sum their partials after every subdomain scatter.
-    # Here the ranks are threads on one device (LocalGroup), exercising the
-    # same sharded code path the NCCL communicator drives across GPUs.
+    # the multi-GPU decomposition (include/sgw.h): ranks own 2D blocks of
+    # subdomains, complete the shared interface nodes by point-to-point halo
+    # exchanges and sum the coarse vector and CG scalars over the ranks; the
+    # PCG runs as the phase-split kernels.  Here the ranks are threads on one
+    # device (LocalGroup, host-synchronised exchanges), exercising the same
+    # sharded kernels the NCCL communicator drives across GPUs.
     nx, ny, px, py = case
     coeff = O.lognormal_coeff(nx, ny, 0.3, 0.5, 0.5, 2, 3)
     t = O.triple_products(2, 3, 2)
@@ -298,6 +302,24 @@ def test_nccl_one_rank_communicator(gpu):
     h1, h2 = one.run(u0, 0 * u0, 6), nc.run(u0, 0 * u0, 6)
     assert np.all(np.abs(h1.iterations - h2.iterations) <= 1)
     assert np.linalg.norm(h2.full_state - h1.full_state) / np.linalg.norm(h1.full_state) <= 1e-10
+
+
+def test_solo_rank_construction(gpu):
+    # one rank of a 4-rank decomposition built alone (sgw_create_solo): the
+    # per-rank memory and shard kernels of configurations that need several
+    # GPUs (bench.py --solo-rank); exchanges deliver zeros
+    nx = 32
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, 2, 3)
+    t = O.triple_products(2, 3, 2)
+    kw = dict(params=sg.NewmarkParams(dt=2e-3), options=sg.SgOptions(tol=1e-10, max_iter=30))
+    full = sg.SgSolver(nx, nx, 4, 4, coeff, t, **kw)
+    solo = sg.SgSolver(nx, nx, 4, 4, coeff, t, rank=1, world_size=4, solo=True, **kw)
+    assert solo.device_bytes < 0.6 * full.device_bytes
+    x, rep = solo.pcg(rand(solo.n_global, 2))
+    assert 1 <= rep["iterations"] <= 30 and np.all(np.isfinite(x))
+    S_g, _ = solo.schur().local_block(2, "S")  # subdomain 2 belongs to rank 1 (2x2 rank grid)
+    S_f, _ = full.schur().local_block(2, "S")
+    assert np.array_equal(S_g, S_f)
 
 
 def test_nonconvergence_raises(gpu):
