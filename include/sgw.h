@@ -173,7 +173,8 @@ int sgw_reset_stats(sgw_solver* s);
  * classes {S tile-SYMV, Q tile-SYMV, interior sweep, SG-operator apply}:
  * [total ms, launches, algorithmic bytes per launch]; out[12] = algorithmic
  * bytes of one PCG iteration (SURVEY 8d B_iter); out[13..20] = critical-path
- * ms of the 8 phases of the persistent PCG kernel.  out needs 21 doubles.   */
+ * ms of the 8 phases of the persistent PCG kernel; out[21] = algorithmic
+ * flops of one SG-operator apply.  out needs 22 doubles.                   */
 int sgw_kernel_profile(sgw_solver* s, int enable, double* out);
 /* Average device ms of `reps` back-to-back calls of one operation:
  * which 0 = Schur matvec, 1 = NN2 apply, 2 = global transient SG operator.  */

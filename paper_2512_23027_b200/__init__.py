@@ -30,6 +30,7 @@ from .sgwave import (  # noqa: F401
     run_precond_comparison,
     ricker,
     shard_plan,
+    ShardPlan,
     triple_products,
     write_sg_outputs,
 )

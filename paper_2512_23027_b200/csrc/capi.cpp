@@ -388,8 +388,17 @@ int sgw_kernel_profile(sgw_solver* s, int enable, double* out) {
       double tp[8] = {0};
       SGW_CUDA(cudaMemcpy(tp, g.tphase_.p, sizeof(tp), cudaMemcpyDeviceToHost));
       for (int i = 0; i < 8; ++i) out[13 + i] = tp[i] * 1e-6;  // ms per phase, persistent PCG
+      out[21] = g.flops_sgop();
     }
   });
+}
+
+// reads n doubles (the sum is written only if it is NaN, which it never is)
+__global__ void l2_flush_read_kernel(const double* __restrict__ p, long long n, double* sink) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc += __ldcg(p + i);
+  if (acc != acc) *sink = acc;
 }
 
 int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out) {
@@ -406,8 +415,7 @@ int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out) {
       if (which == 0) g.schur_matvec(x.p, y.p);
       else if (which == 1) g.apply_nn2(x.p, y.p);
       else if (which == 2) g.apply_block(2, x.p, y.p);
-      else if (which == 3) g.apply_block(3, x.p, y.p);
-      else throw Error(SGW_EINVAL, "bench_kernel: which must be 0 (matvec), 1 (nn2), 2 (sg-op), 3 (sg-op + M x2)");
+      else throw Error(SGW_EINVAL, "bench_kernel: which must be 0 (matvec), 1 (nn2), 2 (sg-op)");
     };
     once();
     cudaEvent_t a, b;
@@ -415,12 +423,16 @@ int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out) {
     SGW_CUDA(cudaEventCreate(&b));
     float total = 0;
     if (which >= 2) {
-      // the SG operator's stencils (~150 MB at C2) are about the L2 size: flush
-      // L2 before every timed launch so that each one streams from HBM
-      DBuf<char> flush;
-      flush.alloc(size_t(512) << 20);
+      // the SG operator's couplings (~110 MB at C2) are about the L2 size: flush
+      // L2 before every timed launch so that each one streams from HBM.  The
+      // flush READS a 512 MB buffer: L2 is left holding clean lines, so the
+      // timed kernel does not share HBM with the write-back of a memset.
+      DBuf<double> flush;
+      DBuf<double> sink;
+      flush.alloc(size_t(64) << 20), sink.alloc(1);
+      SGW_CUDA(cudaMemsetAsync(flush.p, 0, flush.n * sizeof(double), g.stream()));
       for (int r = 0; r < reps; ++r) {
-        SGW_CUDA(cudaMemsetAsync(flush.p, r & 0xff, flush.n, g.stream()));
+        l2_flush_read_kernel<<<4 * 148, 512, 0, g.stream()>>>(flush.p, (long long)flush.n, sink.p);
         SGW_CUDA(cudaEventRecord(a, g.stream()));
         once();
         SGW_CUDA(cudaEventRecord(b, g.stream()));

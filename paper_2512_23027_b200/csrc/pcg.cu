@@ -5,6 +5,8 @@
 // Reference: src/dd.cpp:142-157 (matvec), :199-253 (apply_nn2), src/pcg.cpp:7-50.
 #include <cmath>
 
+#include <set>
+
 #include "solver.cuh"
 #include "tiles.cuh"
 
@@ -285,8 +287,21 @@ double GpuSolver::bytes_iter() const {
   return b;
 }
 double GpuSolver::bytes_sgop() const {
-  // SURVEY 8d minimal stored-operator form: 8 n [3 n_in + 2 (P+1)]
-  return 8.0 * n * (3.0 * NIN + 2.0 * NT);
+  // JIT operator: 2 stored couplings per node and input term (sgop.cu), x read
+  // and y written once: 8 n [2 n_in + 2 (P+1)].  Table-driven kernel: the
+  // SURVEY 8d 3-value stored form 8 n [3 n_in + 2 (P+1)].
+  return 8.0 * n * ((sgop_ ? 2.0 : 3.0) * NIN + 2.0 * NT);
+}
+double GpuSolver::flops_sgop() const {
+  if (sgop_) return sgop_flops(*sgop_, n);
+  // SURVEY 8d F_op = 2 n [5 N_ij + nnzG_full + 7 (P+1)] (5-point stencils)
+  std::set<std::pair<int, int>> ij;
+  long long full = 0;
+  for (size_t e = 0; e < P.tensor.v.size(); ++e) {
+    ij.insert({P.tensor.i[e], P.tensor.j[e]}), ij.insert({P.tensor.i[e], P.tensor.k[e]});
+    full += P.tensor.j[e] == P.tensor.k[e] ? 1 : 2;
+  }
+  return 2.0 * n * (5.0 * double(ij.size()) + double(full) + 7.0 * NT);
 }
 
 // ---------------------------------------------------- gather / scatter -----

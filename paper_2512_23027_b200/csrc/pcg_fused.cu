@@ -843,8 +843,10 @@ __global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
       g.sync();
       if (leader) {
         A.st[ST_IT] = it;
-        if (hl < A.hist_cap) A.hist[hl] = rel;
-        A.st[ST_HL] = hl + 1;
+        if (ex != EX_CHECK) {  // a confirmed step records the true residual instead (verdict kernel)
+          if (hl < A.hist_cap) A.hist[hl] = rel;
+          A.st[ST_HL] = hl + 1;
+        }
         A.st[ST_EXIT] = ex;
         if (ex != EX_RUN && A.use_cond) cudaGraphSetConditional(A.cond, 0);
       }

@@ -501,18 +501,22 @@ void GpuSolver::build_device_inputs(const Stencils& stc) {
   gk_ptr.upload(kptr), gk_i.upload(ki), gk_j.upload(kj), gk_v.upload(kv);
   gp_ptr.upload(pptr), gp_i.upload(pi), gp_v.upload(pv);
   Kg.upload(stc.Kg), Mg.upload(stc.Mg), Kl.upload(stc.Kl), Ml.upload(stc.Ml);
-  // JIT SG operator (sgop.cu) on the global grid, stencils stored tile by tile
+  // JIT SG operator (sgop.cu) on the global grid, couplings stored strip by strip
   sgop_ = build_sgop(NT, NIN, P.tensor);
   if (sgop_) {
-    std::vector<double> kt, mt;
+    std::vector<double> kt;
     SgOpArgs& a = sgop_args_;
-    sgop_tile_stencils(*sgop_, stc.Kg.data(), stc.Mg.data(), P.nx - 1, P.ny - 1, 1, NIN, kt, mt, a);
-    Kp_.upload(kt), Mp_.upload(mt);
-    a.K = Kp_.p, a.M = Mp_.p, a.Mg = Mg.p;
-    a.xterm = a.yterm = n;
-    a.xpitch = a.ypitch = P.nx - 1;
-    if (sgop_packs_x(*sgop_)) Xt_.alloc(sgop_xt_doubles(*sgop_, a));
-    a.xt = Xt_.p;
+    if (!sgop_pack_stencils(*sgop_, stc.Kg.data(), stc.Mg.data(), P.nx - 1, P.ny - 1, NIN, kt, a)) {
+      sgop_.reset();  // non-constant mass stencil: the table-driven kernel
+    } else {
+      Kp_.upload(kt);
+      Kpart_.alloc(sgop_scratch_doubles(*sgop_, P.nx - 1, P.ny - 1));
+      a.K = Kp_.p, a.part = Kpart_.p;
+      a.xterm = a.yterm = n;
+      a.xpitch = a.ypitch = P.nx - 1;
+    }
+  }
+  if (sgop_) {
     yglob_.alloc(NSTATE);
   }
 }

@@ -34,25 +34,24 @@ struct SweepLayout;
 // Arguments of the JIT-compiled SG operator (sgop.cu); identical layout to the
 // device-side struct in the generated source.
 struct SgOpArgs {
-  const double *K, *M;  // tiled stencils (sgop_tile_stencils)
-  const double* xt;     // tiled input scratch (sgop_xt_doubles), packed by launch_sgop
-  const double *x, *x2;
+  const double* K;  // couplings in block layout (sgop_pack_stencils)
+  const double* x;
   double* y;
-  long long xterm, xitem, yterm, yitem;
-  int W, H, xpitch, ypitch, tiles_x, tiles_y, items;
-  double alpha, beta, gamma;
-  const double* Mg;  // mass stencils in grid layout [item][4][H][W] (read directly by the kernel)
+  double* part;  // partial rows scratch (sgop_scratch_doubles)
+  long long xterm, yterm;
+  int W, H, xpitch, ypitch, strips, pad_;
+  double alpha, beta, md, mo;  // y = alpha M x + beta K x; constant mass stencil (diag, off-diagonal)
 };
 struct SgOpJit;
+// nullptr when the basis is too large for the register-resident kernel
 std::shared_ptr<SgOpJit> build_sgop(int NT, int NIN, const TensorHost& T);
 void launch_sgop(const SgOpJit& J, const SgOpArgs& a, cudaStream_t st);
-int sgop_rows(const SgOpJit& J);
-bool sgop_packs_x(const SgOpJit& J);  // the operator reads x through packed tiles (scratch sgop_xt_doubles)
-long long sgop_xt_doubles(const SgOpJit& J, const SgOpArgs& a);
-// Tile-major copies of grid stencils K [item][i][3][H][W], M [item][4][H][W]
-// (row-major, pitch W) in the operator's tile order; sets a.tiles_x/tiles_y.
-void sgop_tile_stencils(const SgOpJit& J, const double* K, const double* M, int W, int H, int items, int nin,
-                        std::vector<double>& kt, std::vector<double>& mt, SgOpArgs& a);
+double sgop_flops(const SgOpJit& J, long long n);
+// Strip-major couplings of the reduced stencils Kg [i][3][H][W]; false when the
+// mass stencil Mg [4][H][W] is not constant (the kernel assumes it is).
+bool sgop_pack_stencils(const SgOpJit& J, const double* Kg, const double* Mg, int W, int H, int nin,
+                        std::vector<double>& kt, SgOpArgs& a);
+long long sgop_scratch_doubles(const SgOpJit& J, int W, int H);
 
 template <typename T>
 struct DBuf {
@@ -242,6 +241,7 @@ class GpuSolver {
   double bytes_Q() const;
   double bytes_sweep() const;  // one forward+backward interior solve
   double bytes_sgop() const;   // one global transient SG-operator apply
+  double flops_sgop() const;   // algorithmic flops of that apply
   double bytes_iter() const;   // one PCG iteration (SURVEY 8d B_iter)
 
   // state
@@ -303,7 +303,7 @@ class GpuSolver {
   // stencils
   DBuf<double> Kg, Mg, Kl, Ml;
   // tiled global stencils and the JIT SG operator (sgop.cu)
-  DBuf<double> Kp_, Mp_, Xt_, yglob_;
+  DBuf<double> Kp_, Kpart_, yglob_;
   // (s * nl + lid) lists: interface nodes, interior nodes next to the interface
   DBuf<int> ilist_, alist_;
   long long n_ilist_ = 0, n_alist_ = 0;

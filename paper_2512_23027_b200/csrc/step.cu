@@ -93,8 +93,7 @@ void GpuSolver::apply_block(int op, const double* x, double* y) {
     SGW_LAUNCHED();
   } else {
     SgOpArgs a = sgop_args_;
-    a.x = x, a.x2 = op == 3 ? x : nullptr, a.y = y;  // op 3: the step's form (+ M x2), for benchmarks
-    a.alpha = cm, a.beta = ck, a.gamma = op == 3 ? 1.0 : 0.0;
+    a.x = x, a.y = y, a.alpha = cm, a.beta = ck;
     launch_sgop(*sgop_, a, st_);
   }
   KP.end(st_);
@@ -675,8 +674,8 @@ int GpuSolver::step(int* iters_out) {
     // interior rows: f = M um + a0 M uc + a1 sum c K uc on the global grid (JIT
     // operator), copied into the block rows; interface rows: local stencils
     SgOpArgs sa = sgop_args_;
-    sa.x = uc.p, sa.x2 = nullptr, sa.y = yglob_.p;  // + M um in interior_from_global_kernel
-    sa.alpha = P.alpha0, sa.beta = P.alpha1, sa.gamma = 0.0;
+    sa.x = uc.p, sa.y = yglob_.p;  // + M um in interior_from_global_kernel
+    sa.alpha = P.alpha0, sa.beta = P.alpha1;
     {
       cudaEvent_t e0;
       KP.begin(K_SGOP, st_, &e0);

@@ -572,13 +572,14 @@ class SgSolver:
 
     def kernel_profile(self, enable=True):
         """Per-kernel-class device timings: {class: (total_ms, launches, algorithmic bytes/launch)}."""
-        o = np.zeros(21)
+        o = np.zeros(22)
         _check(load_library().sgw_kernel_profile(self._h, int(enable), _p(o)))
         out = {c: (o[3 * i], int(o[3 * i + 1]), o[3 * i + 2]) for i, c in enumerate(self.KERNEL_CLASSES)}
         out["bytes_per_pcg_iteration"] = o[12]
         names = ["S_tiles", "S_scatter", "update", "Q_tiles_psi", "coarse_assemble", "coarse_solve", "z_scatter",
                  "init_true_residual"]
         out["pcg_phases_ms"] = dict(zip(names, o[13:21].tolist()))
+        out["sg_operator_flops"] = o[21]
         return out
 
     def bench_kernel(self, which, reps=20):

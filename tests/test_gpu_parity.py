@@ -32,11 +32,14 @@ def relerr(a, b):
 
 
 @pytest.mark.parametrize("op", ["mass", "stiffness", "transient"])
-@pytest.mark.parametrize("cfg", [(12, 2, 4, 2), (40, 3, 2, 3), (70, 3, 3, 3), (20, 4, 2, 3)])
+@pytest.mark.parametrize("cfg", [(12, 2, 4, 2), (40, 3, 2, 3), (70, 3, 3, 3), (20, 4, 2, 3), (34, 4, 6, 3),
+                                 (14, 6, 4, 2), (11, 8, 4, 2), (3, 2, 4, 2), (4, 3, 6, 3), (5, 5, 4, 2)])
 def test_apply_block_matches_oracle(gpu, op, cfg):
     # sg.cpp:425-447 vs the oracle; test_sg.cpp:51-73 tolerance 1e-12.  The
-    # JIT-specialised operator at 1, 2 and 3 threads per node (P+1 = 6, 20, 35),
-    # grids that are not multiples of the 32 x R tile.
+    # JIT-specialised operator (sgop.cu) with 1, 2 and 4 thread groups per node
+    # (P+1 = 6, 20 / 21, 28 / 35, 45), grids that are not multiples of the
+    # 32-column strip (W = 33 leaves a 1-column strip), and the 1x1 / 2x2 dof
+    # grids where every boundary-coupling slot is used.
     nx, L, pin, pout = cfg
     g, c = pair(nx, 2, 2, 0.3, 0.5, L, pin, pout, 1e-3)
     x = rand(g.n_terms * g.n_dofs, 1)

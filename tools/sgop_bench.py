@@ -1,6 +1,9 @@
 """Standalone SG-operator apply (for ncu captures and scaling experiments):
-   python tools/sgop_bench.py [C1|C2|C3] [reps]
-   python tools/sgop_bench.py custom <reps> <nx> <px> <L> <p_in> <p_out>"""
+   python tools/sgop_bench.py [C1|C2|C3|C4|C5L8] [reps]
+   python tools/sgop_bench.py custom <reps> <nx> <px> <L> <p_in> <p_out>
+Prints one JSON line: time per launch (L2 flushed before each), algorithmic
+bytes / flops (kernel_profile) and the roofline fractions."""
+import json
 import os
 import sys
 
@@ -20,10 +23,14 @@ nx = c["nx"]
 coeff = sg.lognormal_coeff(nx, nx, c["sigma"], c["b"], c["b"], c["L"], c["p_in"])
 t = sg.triple_products(c["L"], c["p_in"], c["p_out"])
 s = sg.SgSolver(nx, nx, c["px"], c["px"], coeff, t, params=sg.NewmarkParams(dt=c["dt"]))
-which = int(os.environ.get("SGOP_WHICH", "2"))  # 3: the step's form with the M x2 term
-ms = s.bench_kernel(which, reps=reps)
-n = (nx - 1) ** 2
-pairs = len({(i, j) for i, j, k in zip(t.i, t.j, t.k)} | {(i, k) for i, j, k in zip(t.i, t.j, t.k)})
-nbytes = 8.0 * n * (3 * t.n_input + 2 * t.n_output)
-print(f"{name} nx={nx} n_in={t.n_input} P+1={t.n_output} pairs={pairs}: {ms * 1e3:.1f} us/launch, "
-      f"{nbytes / (ms / 1e3) / 1e9:.0f} GB/s, {ms * 1e6 / n / pairs * 1e3:.2f} ps per node-pair")
+ms = s.bench_kernel(2, reps=reps)
+kp = s.kernel_profile(False)
+nbytes, flops = kp["sg_operator"][2], kp["sg_operator_flops"]
+peaks = bench.load_peaks() if hasattr(bench, "load_peaks") else {}
+bw = peaks.get("hbm_gbs", 6549.8)
+fp64 = bench.FP64_TFLOPS if hasattr(bench, "FP64_TFLOPS") else 33.5
+t_roof = max(nbytes / (bw * 1e9), flops / (fp64 * 1e12)) * 1e3
+print(json.dumps({"config": name, "n_in": t.n_input, "P+1": t.n_output, "us": ms * 1e3, "bytes": nbytes,
+                  "flops": flops, "GBs": nbytes / (ms / 1e3) / 1e9, "TFLOPs": flops / (ms / 1e3) / 1e12,
+                  "hbm_frac": nbytes / (ms / 1e3) / 1e9 / bw, "roofline_us": t_roof * 1e3,
+                  "roofline_frac": t_roof / ms}))
