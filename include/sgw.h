@@ -24,6 +24,8 @@
  *   sgw_lognormal_coeff lognormal_pce(kle_exponential(...))  src/lognormal.cpp:8-40, src/kle.cpp:80-133
  *   sgw_triple_products triple_products               src/pce.cpp:96-122 (order_in <= order_out guard lifted)
  *   sgw_nearest_node    nearest_node                  src/mesh.cpp:83-96
+ *   sgw_kle_spectrum    kle_spectrum_csv's lambdas    src/kle.cpp:161-167
+ *   sgw_pce_indices     PceBasis::indices_csv's rows  src/pce.cpp:84-94
  *
  * Error classes (reference exception -> status):
  *   std::invalid_argument (sg.cpp:143-145, :382)            -> SGW_EINVAL
@@ -186,6 +188,13 @@ int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, doub
 int sgw_triple_products(int n_vars, int p_in, int p_out, int* n_in, int* n_out, int* n_entries,
                         int* ei, int* ej, int* ek, double* ev, long long cap);
 int sgw_nearest_node(int nx, int ny, double x, double y);
+/* kle_spectrum.csv / pce_indices.csv inputs (src/kle.cpp:161-167,
+ * src/pce.cpp:84-94): the n_vars sorted KLE eigenvalues of the separable
+ * exponential covariance times sigma^2 (out: n_vars doubles); the PCE multi-indices of
+ * total order <= order in basis order (out: n_terms x n_vars, row-major; out
+ * may be NULL to query n_terms).                                             */
+int sgw_kle_spectrum(double sigma, double bx, double by, int n_vars, double* out);
+int sgw_pce_indices(int n_vars, int order, int* out, long long out_cap, int* n_terms);
 
 /* Sharding plan (host only, no GPU needed): the rx x ry rank grid and rank
  * `rank`'s halo.  info[7] = {rx, ry, owned subdomains, local interface nodes,

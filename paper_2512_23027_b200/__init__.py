@@ -33,4 +33,9 @@ from .sgwave import (  # noqa: F401
     ShardPlan,
     triple_products,
     write_sg_outputs,
+    kle_spectrum,
+    kle_spectrum_csv,
+    pce_indices,
+    pce_indices_csv,
+    svg_lines,
 )

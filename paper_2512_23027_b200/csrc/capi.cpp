@@ -455,6 +455,24 @@ int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out) {
   });
 }
 
+int sgw_kle_spectrum(double sigma, double bx, double by, int n_vars, double* out) {
+  return guard([&] {
+    const auto l = kle_spectrum(sigma, bx, by, n_vars);
+    std::memcpy(out, l.data(), l.size() * sizeof(double));
+  });
+}
+
+int sgw_pce_indices(int n_vars, int order, int* out, long long cap, int* n_terms) {
+  return guard([&] {
+    const auto ix = pce_indices(n_vars, order);
+    *n_terms = int(ix.size());
+    if (out) {
+      if ((long long)ix.size() * n_vars > cap) throw Error(SGW_EINVAL, "index buffer too small");
+      for (size_t k = 0; k < ix.size(); ++k) std::memcpy(out + k * n_vars, ix[k].data(), n_vars * sizeof(int));
+    }
+  });
+}
+
 int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, double g0, int n_vars, int p_in,
                         double* out, long long cap, int* n_in) {
   return guard([&] {

@@ -434,6 +434,30 @@ std::vector<std::vector<double>> lognormal_coeff(int nx, int ny, double sigma, d
   return out;
 }
 
+// the first L eigenvalues sigma^2 lambda_i lambda_j of the 2D separable
+// exponential covariance, sorted like kle_exponential (src/kle.cpp:80-133):
+// kle_spectrum.csv's lambda column
+std::vector<double> kle_spectrum(double sigma, double bx, double by, int L) {
+  if (L < 1) throw Error(1, "kle_spectrum: n_modes must be >= 1");
+  const auto ex = roots_1d(bx, L);
+  const auto ey = (by == bx) ? ex : roots_1d(by, L);
+  std::vector<std::tuple<double, int, int>> pr;
+  for (int i = 0; i < L; ++i)
+    for (int j = 0; j < L; ++j) pr.emplace_back(ex[i].lambda * ey[j].lambda, i, j);
+  std::sort(pr.begin(), pr.end(), [](const auto& a, const auto& b) {
+    if (std::get<0>(a) != std::get<0>(b)) return std::get<0>(a) > std::get<0>(b);
+    return std::tie(std::get<1>(a), std::get<2>(a)) < std::tie(std::get<1>(b), std::get<2>(b));
+  });
+  std::vector<double> out(L);
+  for (int v = 0; v < L; ++v) out[v] = sigma * sigma * std::get<0>(pr[v]);  // KleMode::lambda
+  return out;
+}
+
+std::vector<std::vector<int>> pce_indices(int n_vars, int order) {  // PceBasis order (src/pce.cpp:19-37)
+  if (n_vars < 1 || order < 0) throw Error(1, "pce_indices: bad arguments");
+  return graded_indices(n_vars, order);
+}
+
 // src/pce.cpp:96-122 with the order_in <= order_out guard lifted.
 TensorHost triple_products(int L, int p_in, int p_out) {
   if (L < 1 || p_in < 0 || p_out < 0) throw Error(1, "triple_products: bad arguments");

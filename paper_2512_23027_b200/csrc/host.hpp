@@ -106,6 +106,8 @@ Stencils build_stencils(const Problem& p, const Geometry& g, bool need_local);
 std::vector<std::vector<double>> lognormal_coeff(int nx, int ny, double sigma, double bx, double by,
                                                  double g0, int n_vars, int p_in);
 TensorHost triple_products(int n_vars, int p_in, int p_out);
+std::vector<double> kle_spectrum(double sigma, double bx, double by, int n_vars);
+std::vector<std::vector<int>> pce_indices(int n_vars, int order);
 int nearest_node(int nx, int ny, double x, double y);
 
 }  // namespace sgw

@@ -1034,7 +1034,14 @@ void GpuSolver::setup_fused_pcg() {
     if (fused_nst_ >= 2 || bps == 1) break;
   }
   if (const char* e = std::getenv("SGW_PCG_RING")) fused_nst_ = std::min(kMaxRing, std::atoi(e));
-  if (fused_nst_ < 1) throw Error(4, "persistent PCG: local vectors exceed shared memory");
+  if (fused_nst_ < 1) {
+    // a subdomain's local interface vectors exceed one CTA's shared memory
+    // (very large PCE bases, e.g. P+1 = 153 on 32 x 32 subdomains): the
+    // host-driven PCG with the per-tile S / Q products, which keep no whole
+    // local vector in shared memory
+    use_fused_ = use_phase_ = walk_ok_ = false;
+    return;
+  }
   fused_smem_ = (size_t)fused_nst_ * kTileBytes + (size_t)vec;
   SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fused_smem_));

@@ -538,6 +538,95 @@ __global__ void extract_band_kernel(const double* __restrict__ E, double* __rest
   }
 }
 
+// ------------------------------------------------- large blocks ---------
+// The same block Thomas solve for interior blocks beyond the pipelined
+// kernel's register-resident accumulators (B > 1536, e.g. P+1 = 91 on 32 x 32
+// subdomains): one CTA per subdomain, vectors in shared memory, the D^-1 tiles
+// and band chunks read straight from global memory (L2).  z = D^-1 w in two
+// fixed-order passes (row products of the lower tiles, then column products
+// of the strictly lower ones: every tile is read twice), so results stay
+// bitwise reproducible.  Correctness path for very large PCE bases, not tuned.
+constexpr int kGenThreads = 512;
+__device__ void gen_dinv(const double* __restrict__ Fk, const SweepLayout& L, const double* __restrict__ w,
+                         double* __restrict__ rowv, double* __restrict__ z) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kGenThreads / 32;
+  // rows: warp per output row r, lanes over the columns of tiles (I, J <= I)
+  for (int r = warp; r < L.B; r += nw) {
+    const int I = r / kTile, rl = r % kTile;
+    double acc = 0.0;
+    for (int J = 0; J <= I; ++J) {
+      const int4 d = L.ent[I * (I + 1) / 2 + J];
+      const int wp = d.z & 0xffff;
+      const double* row = Fk + d.x + (long long)rl * wp;
+      for (int c = lane; c < wp; c += 32) acc = fma(__ldg(row + (c ^ (2 * (rl & 7)))), w[J * kTile + c], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) rowv[r] = acc;
+  }
+  __syncthreads();
+  // columns: warp per output column c of block J, lanes over the rows of tiles (I > J, J)
+  for (int col = warp; col < L.B; col += nw) {
+    const int J = col / kTile, cl = col % kTile;
+    double acc = 0.0;
+    for (int I = J + 1; I < L.nb; ++I) {
+      const int4 d = L.ent[I * (I + 1) / 2 + J];
+      const int h = d.z >> 16, wp = d.z & 0xffff;
+      for (int rl = lane; rl < h; rl += 32)
+        acc = fma(__ldg(Fk + d.x + (long long)rl * wp + (cl ^ (2 * (rl & 7)))), w[I * kTile + rl], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) z[col] = rowv[col] + acc;
+  }
+  __syncthreads();
+}
+// out[i] = in[i] - sum_c band[i][c] v[g0(i) + c]  (LO: g0 = (i / NT - 1) NT, UP: (i / NT) NT)
+__device__ void gen_band(const double* __restrict__ band, const SweepLayout& L, int d0, const double* __restrict__ v,
+                         const double* in, double* out) {
+  for (int i = threadIdx.x; i < L.B; i += kGenThreads) {
+    const int q = i / L.Rb, r = i % L.Rb, g0 = (i / L.NT + d0) * L.NT;
+    const double* b = band + (long long)q * L.bw * L.Rb + r;
+    double acc = 0.0;
+    for (int c = 0; c < L.bw; ++c) {
+      const int g = g0 + c;
+      if (g >= 0 && g < L.B) acc = fma(__ldg(b + (long long)c * L.Rb), v[g], acc);
+    }
+    out[i] = in[i] - acc;
+  }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(kGenThreads, 1) sweep_generic_kernel(double* __restrict__ x, const double* __restrict__ F,
+                                                                       const SweepLayout L, long long lo_off, long long up_off) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* w = reinterpret_cast<double*>(smraw);
+  double* z = w + L.VL;
+  double* rowv = z + L.VL;
+  const int s = blockIdx.x, B = L.B, H = L.H;
+  const double* Fs = F + (long long)s * L.per_sub;
+  double* xs = x + (long long)s * H * B;
+  for (int i = threadIdx.x; i < L.VL; i += kGenThreads) w[i] = i < B ? xs[i] : 0.0, z[i] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < H; ++k) {  // forward: w_k = b_k - A_{k,k-1} z_{k-1} (kept in x), z_k = D_k^-1 w_k
+    if (k > 0) {
+      for (int i = threadIdx.x; i < B; i += kGenThreads) rowv[i] = xs[(long long)k * B + i];
+      __syncthreads();
+      gen_band(Fs + (long long)(k - 1) * L.blk + lo_off, L, -1, z, rowv, w);
+      for (int i = threadIdx.x; i < B; i += kGenThreads) xs[(long long)k * B + i] = w[i];
+    }
+    gen_dinv(Fs + (long long)k * L.blk, L, w, rowv, z);
+  }
+  for (int i = threadIdx.x; i < B; i += kGenThreads) xs[(long long)(H - 1) * B + i] = z[i];
+  for (int k = H - 2; k >= 0; --k) {  // backward: x_k = D_k^-1 (w_k - A_{k,k+1} x_{k+1})
+    for (int i = threadIdx.x; i < B; i += kGenThreads) rowv[i] = xs[(long long)k * B + i];
+    __syncthreads();
+    gen_band(Fs + (long long)k * L.blk + up_off, L, 0, z, rowv, w);
+    gen_dinv(Fs + (long long)k * L.blk, L, w, rowv, z);
+    for (int i = threadIdx.x; i < B; i += kGenThreads) xs[(long long)k * B + i] = z[i];
+    __syncthreads();
+  }
+}
+
 using SweepFn = void (*)(double*, const double*, const SweepLayout);
 static SweepFn sweep_fn(int cs, int nbm) {
 #define SGW_SW(C)                                                  \
@@ -561,11 +650,13 @@ static size_t smem_bytes(int stages, int VL, int CS, int slot_len, int tpart_len
 
 void GpuSolver::build_sweep_layout() {
   const int H = G.H, nb = (B + kTile - 1) / kTile, VL = nb * kTile;
-  if (B > kPre * kSwWarps * 32) throw Error(1, "interior block too large for the sweep kernel");
   const int bw = 2 * NT;
   int Rb = 64;
   while (Rb > 16 && Rb * bw > kTileD) Rb /= 2;
-  if (Rb * bw > kTileD) throw Error(1, "interior band too wide for the sweep kernel");
+  // blocks beyond the pipelined kernel's limits: the large-block kernel
+  sweep_generic_ = B > kPre * kSwWarps * 32 || Rb * bw > kTileD || std::getenv("SGW_SWEEP_GENERIC") != nullptr;
+  if (sweep_generic_ && 3 * (size_t)VL * 8 > (size_t)kSmemMax)
+    throw Error(1, "interior block too large for the sweep kernels (3 B doubles of shared memory)");
   const int nch = (B + Rb - 1) / Rb;
   auto hgt = [&](int I) { return std::min(kTile, B - I * kTile); };
   // stored tile width: a multiple of 16 so that the swizzle (column pairs
@@ -587,6 +678,23 @@ void GpuSolver::build_sweep_layout() {
   const long long blk = (up_off + (long long)nch * bw * Rb + 31) & ~31LL;
   if (blk >= (1LL << 31)) throw Error(1, "interior block too large for the sweep layout");
 
+  if (sweep_generic_) {
+    SweepLayout L{};
+    std::vector<int> raw(ent.size() * 4);
+    std::memcpy(raw.data(), ent.data(), raw.size() * sizeof(int));
+    sw_off.upload(raw);
+    L.ent = reinterpret_cast<const int4*>(sw_off.p);
+    L.blk = blk, L.per_sub = (long long)H * blk;
+    L.B = B, L.H = H, L.nb = nb, L.VL = VL, L.NT = NT, L.Rb = Rb, L.bw = bw;
+    L.n_sym = n_sym, L.n_ent = (int)ent.size();
+    delete sweep_layout_;
+    sweep_layout_ = new SweepLayout(L);
+    sweep_lo_off_ = lo_off, sweep_up_off_ = up_off, sweep_nch_ = nch, sweep_cs_ = 1;
+    Fcomp.alloc(size_t(NS) * L.per_sub);
+    SGW_CUDA(cudaFuncSetAttribute((const void*)sweep_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(3 * (size_t)VL * 8)));
+    return;
+  }
   // cluster size: about one wave of CTAs over the 148 SMs
   int CS = NS >= 100 ? 1 : NS >= 48 ? 2 : NS >= 24 ? 4 : NS >= 12 ? 8 : 16;
   if (const char* e = std::getenv("SGW_SWEEP_CS")) {  // test hook: force a cluster size
@@ -762,6 +870,7 @@ void destroy_sweep_layout(SweepLayout* p) { delete p; }
 
 size_t GpuSolver::sweep_smem_bytes() const {
   const SweepLayout& L = *sweep_layout_;
+  if (sweep_generic_) return 3 * (size_t)L.VL * 8;
   return smem_bytes(L.stages, L.VL, sweep_cs_, L.slot_len, L.tpart_len);
 }
 
@@ -769,6 +878,12 @@ void GpuSolver::sweep(double* x) {
   const SweepLayout& L = *sweep_layout_;
   cudaEvent_t e0;
   KP.begin(K_SWEEP, st_, &e0);
+  if (sweep_generic_) {
+    sweep_generic_kernel<<<NS, kGenThreads, sweep_smem_bytes(), st_>>>(x, Fcomp.p, L, sweep_lo_off_, sweep_up_off_);
+    SGW_LAUNCHED();
+    KP.end(st_);
+    return;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(NS * sweep_cs_);
   cfg.blockDim = dim3(kSwThreads);

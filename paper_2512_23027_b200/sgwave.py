@@ -96,6 +96,8 @@ def load_library():
     L.sgw_triple_products.argtypes = [ip, ip, ip, C.POINTER(ip), C.POINTER(ip), C.POINTER(ip), vp, vp, vp, vp,
                                       C.c_longlong]
     L.sgw_nearest_node.argtypes = [ip, ip, dp, dp]
+    L.sgw_kle_spectrum.argtypes = [dp, dp, dp, ip, vp]
+    L.sgw_pce_indices.argtypes = [ip, ip, vp, C.c_longlong, C.POINTER(ip)]
     L.sgw_nccl_unique_id.argtypes = [vp]
     L.sgw_shard_plan.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp]
     L.sgw_local_group_new.argtypes = [ip, C.POINTER(vp)]
@@ -155,6 +157,23 @@ def lognormal_coeff(nx, ny, sigma, bx, by, n_vars, p_in, g0=0.0) -> np.ndarray:
     _check(L.sgw_lognormal_coeff(nx, ny, sigma, bx, by, g0, n_vars, p_in, None, 0, C.byref(n_in)))
     out = np.zeros((n_in.value, (nx + 1) * (ny + 1)))
     _check(L.sgw_lognormal_coeff(nx, ny, sigma, bx, by, g0, n_vars, p_in, _p(out), out.size, C.byref(n_in)))
+    return out
+
+
+def kle_spectrum(sigma, bx, by, n_vars) -> np.ndarray:
+    """The n_vars sorted KleMode::lambda of kle_exponential (src/kle.cpp:80-133)."""
+    out = np.zeros(n_vars)
+    _check(load_library().sgw_kle_spectrum(sigma, bx, by, n_vars, _p(out)))
+    return out
+
+
+def pce_indices(n_vars, order) -> np.ndarray:
+    """PceBasis(n_vars, order) multi-indices in basis order (src/pce.cpp:19-37): n_terms x n_vars."""
+    L = load_library()
+    n = C.c_int()
+    _check(L.sgw_pce_indices(n_vars, order, None, 0, C.byref(n)))
+    out = np.zeros((n.value, n_vars), np.int32)
+    _check(L.sgw_pce_indices(n_vars, order, _p(out), out.size, C.byref(n)))
     return out
 
 
@@ -246,15 +265,87 @@ def moments(flat_state, n_dofs):
     return u[:n_dofs].copy(), np.sqrt(var)
 
 
-def write_sg_outputs(out_dir, hist: SgHistory, nx, ny, dt, snapshot_times=()):
-    """The `solve-sg` data files (experiments.cpp:393-434, docs/outputs.md:19-30),
-    values in %.17g like CsvWriter (io.cpp:15-44):
+def kle_spectrum_csv(lambdas) -> str:
+    """src/kle.cpp:161-167 (ostream precision 17)"""
+    return "n,lambda\n" + "".join(f"{n + 1},{_g17(v)}\n" for n, v in enumerate(lambdas))
+
+
+def pce_indices_csv(indices) -> str:
+    """PceBasis::indices_csv (src/pce.cpp:84-94)"""
+    return "term,total_order,exponents\n" + "".join(
+        f"{k},{int(sum(a))},{';'.join(str(int(v)) for v in a)}\n" for k, a in enumerate(indices))
+
+
+def svg_lines(title, xlabel, ylabel, series, logx=False, logy=False) -> str:
+    """write_svg_lines (src/io.cpp:58-123): series = [(label, xs, ys)]; numbers in
+    the ostream default format (%g)."""
+    width, height, ml, mr, mt, mb = 720, 480, 70, 160, 40, 50
+    def ax(v, lg):
+        return math.log10(v) if lg else v
+    def skip(x, y):
+        return (logx and x <= 0) or (logy and y <= 0) or not math.isfinite(y)
+    xmin, xmax, ymin, ymax = 1e300, -1e300, 1e300, -1e300
+    for _, xs, ys in series:
+        for x, y in zip(xs, ys):
+            if skip(x, y):
+                continue
+            xmin, xmax = min(xmin, ax(x, logx)), max(xmax, ax(x, logx))
+            ymin, ymax = min(ymin, ax(y, logy)), max(ymax, ax(y, logy))
+    if xmax <= xmin:
+        xmax = xmin + 1
+    if ymax <= ymin:
+        ymax = ymin + 1
+    def px(x):
+        return ml + (ax(x, logx) - xmin) / (xmax - xmin) * (width - ml - mr)
+    def py(y):
+        return height - mb - (ax(y, logy) - ymin) / (ymax - ymin) * (height - mt - mb)
+    g = "{:g}".format
+    colors = ["#1f77b4", "#d62728", "#2ca02c", "#9467bd", "#ff7f0e", "#8c564b", "#17becf", "#7f7f7f"]
+    o = [f'<svg xmlns="http://www.w3.org/2000/svg" width="{width}" height="{height}">\n'
+         '<rect width="100%" height="100%" fill="white"/>\n',
+         f'<text x="{width // 2}" y="20" text-anchor="middle" font-size="15">{title}</text>\n',
+         f'<text x="{width // 2}" y="{height - 12}" text-anchor="middle" font-size="12">{xlabel}</text>\n',
+         f'<text x="16" y="{height // 2}" text-anchor="middle" font-size="12" transform="rotate(-90 16 '
+         f'{height // 2})">{ylabel}</text>\n',
+         f'<rect x="{ml}" y="{mt}" width="{width - ml - mr}" height="{height - mt - mb}" fill="none" '
+         'stroke="black"/>\n']
+    for k in range(5):
+        fx, fy = xmin + (xmax - xmin) * k / 4.0, ymin + (ymax - ymin) * k / 4.0
+        gx, gy = ml + (width - ml - mr) * k / 4.0, height - mb - (height - mt - mb) * k / 4.0
+        lx, ly = "%.3g" % (10 ** fx if logx else fx), "%.3g" % (10 ** fy if logy else fy)
+        o.append(f'<text x="{g(gx)}" y="{height - mb + 16}" text-anchor="middle" font-size="10">{lx}</text>\n')
+        o.append(f'<text x="{ml - 6}" y="{g(gy + 3)}" text-anchor="end" font-size="10">{ly}</text>\n')
+    for ci, (label, xs, ys) in enumerate(series):
+        color = colors[ci % 8]
+        pts = "".join(f"{g(px(x))},{g(py(y))} " for x, y in zip(xs, ys) if not skip(x, y))
+        o.append(f'<polyline fill="none" stroke="{color}" stroke-width="1.5" points="{pts}"/>\n')
+        o.append(f'<text x="{width - mr + 10}" y="{mt + 14 + 16 * ci}" font-size="11" fill="{color}">{label}</text>\n')
+    o.append("</svg>\n")
+    return "".join(o)
+
+
+def write_sg_outputs(out_dir, hist: SgHistory, nx, ny, dt, snapshot_times=(), kle=None, pce=None, manifest=None):
+    """The `solve-sg` output set (driver_solve_sg, experiments.cpp:393-449, and
+    run_driver's manifest, :741-754), values in %.17g like CsvWriter
+    (io.cpp:15-44), in the reference's output order:
       probe_<k>.csv     t,mean,std,u0..uP       (needs hist.probe_coeffs)
+      kle_spectrum.csv  n,lambda                (kle = (sigma, bx, by, n_vars))
+      pce_indices.csv   term,total_order,exponents (pce = (n_vars, p_out))
       iterations.csv    step,iterations,final_residual
       snapshot_<k>.csv  node_id,x,y,mean,std    (needs hist.full_state)
-    Returns the written file names."""
+      probes.svg        probe mean / std lines  (write_svg_lines)
+      manifest.json     command, config, seed, wall_seconds, version, outputs
+                        (manifest = {"command", "config", "seed", "wall_seconds"})
+    Every .csv is a pure function of the history: reruns are byte-identical
+    (acceptance criterion 16).  Returns the written file names."""
     os.makedirs(out_dir, exist_ok=True)
     names = []
+
+    def emit(name, text):
+        with open(os.path.join(out_dir, name), "w", newline="") as f:
+            f.write(text)
+        names.append(name)
+
     pc = hist.probe_coeffs
     nt = 0 if pc is None or pc.size == 0 else pc.shape[1]
     for p in range(hist.probe_mean.shape[0]):
@@ -263,6 +354,10 @@ def write_sg_outputs(out_dir, hist: SgHistory, nx, ny, dt, snapshot_times=()):
                 for s in range(len(hist.times))]
         names.append(f"probe_{p}.csv")
         _write_csv(os.path.join(out_dir, names[-1]), header, rows)
+    if kle is not None:
+        emit("kle_spectrum.csv", kle_spectrum_csv(kle_spectrum(*kle)))
+    if pce is not None:
+        emit("pce_indices.csv", pce_indices_csv(pce_indices(*pce)))
     if len(hist.iterations):
         _write_csv(os.path.join(out_dir, "iterations.csv"), "step,iterations,final_residual",
                    [[s + 1, int(hist.iterations[s]), hist.residual[s]] for s in range(len(hist.iterations))])
@@ -281,6 +376,18 @@ def write_sg_outputs(out_dir, hist: SgHistory, nx, ny, dt, snapshot_times=()):
             rows = [[i, gi[i] / nx, gj[i] / ny, mean_n[i], sd_n[i]] for i in range(nodes)]
             names.append(f"snapshot_{k}.csv")
             _write_csv(os.path.join(out_dir, names[-1]), "node_id,x,y,mean,std", rows)
+    if hist.probe_mean.shape[0]:
+        series = []
+        for p in range(hist.probe_mean.shape[0]):
+            series.append((f"mean p{p}", hist.times, hist.probe_mean[p]))
+            series.append((f"std p{p}", hist.times, hist.probe_std[p]))
+        emit("probes.svg", svg_lines("SG pressure statistics", "t (s)", "pressure", series))
+    if manifest is not None:
+        import json
+        m = {"command": manifest.get("command", "solve-sg"), "config": manifest.get("config", {}),
+             "seed": manifest.get("seed", 0), "wall_seconds": manifest.get("wall_seconds", 0.0),
+             "version": "0.1.0", "outputs": list(names)}
+        emit("manifest.json", json.dumps(m, indent=2, sort_keys=True) + "\n")  # nlohmann::json dump(2)
     return names
 
 

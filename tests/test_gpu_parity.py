@@ -48,6 +48,22 @@ def test_apply_block_matches_oracle(gpu, op, cfg):
     assert relerr(a, b) <= 1e-12
 
 
+@pytest.mark.parametrize("case", [(20, 2, 2, 3, 4, 2), (17, 3, 2, 2, 4, 2)])
+def test_large_block_sweep_matches_oracle(gpu, monkeypatch, case):
+    # the large-block interior sweep (sweep.cu sweep_generic_kernel, used when
+    # B = W (P+1) > 1536), forced here on small blocks: Schur products (which
+    # stand on the setup only) and the trajectory (two sweeps per step)
+    monkeypatch.setenv("SGW_SWEEP_GENERIC", "1")
+    nx, px, py, L, pin, pout = case
+    g, c = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 1e-3)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 6, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 6, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
 @pytest.mark.parametrize("cfg", [(8, 2, 1, 1, 1, 1), (12, 2, 2, 2, 2, 2), (16, 4, 4, 2, 4, 2), (24, 3, 2, 3, 2, 3),
                                  (22, 4, 3, 2, 2, 2), (13, 5, 2, 1, 2, 2)])
 def test_schur_and_nn2_match_oracle(gpu, cfg):
