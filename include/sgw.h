@@ -21,6 +21,8 @@
  *   sgw_apply_precond   make_preconditioner / apply_{lumped,nn1,nn2}  dd.hpp:86-88,102, src/dd.cpp:159-253
  *   sgw_pcg             pcg(matvec, apply_nn2, ...)   include/sgwave/pcg.hpp:20-21, src/pcg.cpp:7-50
  *   sgw_coarse_operator SchurSystem::coarse_operator  include/sgwave/dd.hpp:90
+ *   sgw_schur_from_locals / sgw_gschur_*  SchurSystem built from LocalSchur data  dd.hpp:50-96
+ *   sgw_pcg_ops         pcg(LinearOp, LinearOp, ...)  include/sgwave/pcg.hpp:15-21, src/pcg.cpp:7-50
  *   sgw_lognormal_coeff lognormal_pce(kle_exponential(...))  src/lognormal.cpp:8-40, src/kle.cpp:80-133
  *   sgw_triple_products triple_products               src/pce.cpp:96-122 (order_in <= order_out guard lifted)
  *   sgw_nearest_node    nearest_node                  src/mesh.cpp:83-96
@@ -181,6 +183,44 @@ int sgw_kernel_profile(sgw_solver* s, int enable, double* out);
 /* Average device ms of `reps` back-to-back calls of one operation:
  * which 0 = Schur matvec, 1 = NN2 apply, 2 = global transient SG operator.  */
 int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out_ms);
+
+/* Interface systems from caller-built local Schur data (the reference's
+ * LocalSchur fields, include/sgwave/dd.hpp:50-62, as test_dd.cpp:123-151
+ * builds one by hand): SchurSystem{n_global, n_corner, locals}.finalize(),
+ * matvec, apply_nn2, coarse_operator and pcg(matvec, apply_nn2, ...) on the
+ * GPU (src/dd.cpp:98-157, :199-253; src/pcg.cpp:7-50).  S is n x n
+ * column-major; every array is copied.                                     */
+typedef struct sgw_local_schur {
+  int n;                         /* flat local interface size */
+  const double* S;               /* n x n local Schur complement */
+  const long long* gmap;         /* n: local -> global flat interface index */
+  const double* weights;         /* n: partition-of-unity weights D_s */
+  int nr;                        /* remaining (non-corner) local indices */
+  const int* r_idx;
+  int nc;                        /* corner local indices */
+  const int* c_idx;
+  const long long* corner_gmap;  /* nc: corner -> global corner index */
+} sgw_local_schur;
+typedef struct sgw_schur sgw_schur;
+int sgw_schur_from_locals(long long n_global, long long n_corner, int n_locals, const sgw_local_schur* locals,
+                          sgw_schur** out);
+void sgw_schur_free(sgw_schur* h);
+int sgw_gschur_matvec(sgw_schur* h, const double* x, double* y);
+int sgw_gschur_apply_nn2(sgw_schur* h, const double* r, double* z);
+int sgw_gschur_coarse_operator(sgw_schur* h, double* F);  /* n_corner^2, column-major */
+/* pcg(matvec, apply_nn2, b, tol, max_iter) on this system (x0 = 0). */
+int sgw_gschur_pcg(sgw_schur* h, const double* b, double tol, int max_iter, double* x, int* iterations,
+                   int* converged, double* hist, int hist_cap, int* hist_len);
+
+/* pcg (include/sgwave/pcg.hpp:15-21, src/pcg.cpp:7-50) over caller-supplied
+ * operators, the reference's LinearOp: op(ctx, n, x, y) writes y = A x for
+ * host vectors of length n (precond: z = M^-1 r; NULL = identity).  The CG
+ * recurrence (vectors, dots, axpys) runs on the GPU; each operator call
+ * copies its input to the host and its output back.  Report as sgw_pcg.   */
+typedef void (*sgw_host_op)(void* ctx, long long n, const double* x, double* y);
+int sgw_pcg_ops(long long n, sgw_host_op op, void* op_ctx, sgw_host_op precond, void* precond_ctx, const double* b,
+                double tol, int max_iter, double* x, int* iterations, int* converged, double* hist, int hist_cap,
+                int* hist_len);
 
 /* Input builders (host). */
 int sgw_lognormal_coeff(int nx, int ny, double sigma, double bx, double by, double g0,

@@ -215,6 +215,24 @@ int orc_local_schur(void* hp, int s, double* S, long long* gmap, long long* a_ou
   return 0;
 }
 
+// the rest of LocalSchur s (dd.hpp:50-62): weights, r_idx, c_idx, corner_gmap
+// (NULL pointers: sizes only)
+int orc_local_maps(void* hp, int s, double* w, int* r_idx, int* c_idx, long long* corner_gmap, long long* nr,
+                   long long* nc) {
+  const SgSolver& sv = *static_cast<Handle*>(hp)->solver;
+  const LocalSchur& ls = sv.schur().locals.at(s);
+  *nr = (long long)ls.r_idx.size(), *nc = (long long)ls.c_idx.size();
+  if (w)
+    for (Index k = 0; k < ls.n_flat(); ++k) w[k] = ls.weights[k];
+  if (r_idx)
+    for (size_t k = 0; k < ls.r_idx.size(); ++k) r_idx[k] = int(ls.r_idx[k]);
+  if (c_idx)
+    for (size_t k = 0; k < ls.c_idx.size(); ++k) c_idx[k] = int(ls.c_idx[k]);
+  if (corner_gmap)
+    for (size_t k = 0; k < ls.corner_gmap.size(); ++k) corner_gmap[k] = ls.corner_gmap[k];
+  return 0;
+}
+
 // SgSolver::run (src/sg.cpp:358-423).  Force: Ricker wavelet
 //   amp * (1 - 2 pi^2 f0^2 (t - t0)^2) exp(-pi^2 f0^2 (t - t0)^2)
 // at mesh node force_node (force_node < 0: no forcing).  Outputs: iters[n_steps],

@@ -38,6 +38,7 @@ def lib():
         L.orc_lognormal_coeff.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                           C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                           C.POINTER(C.c_int)]
+        L.orc_local_maps.argtypes = [C.c_void_p, C.c_int] + [C.c_void_p] * 4 + [C.POINTER(C.c_longlong)] * 2
         L.orc_kle_lambdas.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, _dp]
         L.orc_triple_products.argtypes = [C.c_int] * 4 + [C.POINTER(C.c_int)] * 3 + [C.c_void_p] * 4
         L.orc_nearest_node.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double]
@@ -236,6 +237,17 @@ class SgSolver:
         g = np.zeros(a.value, np.int64)
         lib().orc_local_schur(self._h, s, _ptr(S), _ptr(g), C.byref(a))
         return S.reshape(a.value, a.value).T.copy(), g
+
+    def local_schur_full(self, s):
+        """LocalSchur s (dd.hpp:50-62): S, gmap, weights, r_idx, c_idx, corner_gmap"""
+        S, g = self.local_schur(s)
+        nr, nc = C.c_longlong(), C.c_longlong()
+        lib().orc_local_maps(self._h, s, None, None, None, None, C.byref(nr), C.byref(nc))
+        w = np.zeros(g.size)
+        ri, ci = np.zeros(nr.value, np.int32), np.zeros(nc.value, np.int32)
+        cg = np.zeros(nc.value, np.int64)
+        lib().orc_local_maps(self._h, s, _ptr(w), _ptr(ri), _ptr(ci), _ptr(cg), C.byref(nr), C.byref(nc))
+        return {"S": S, "gmap": g, "weights": w, "r_idx": ri, "c_idx": ci, "corner_gmap": cg}
 
     def run(self, u0, v0, n_steps, force_node=-1, f0=10.0, t0=0.1, amp=1.0, store_full=False, probes=()):
         u0 = np.ascontiguousarray(u0, np.float64)

@@ -31,6 +31,10 @@ from .sgwave import (  # noqa: F401
     ricker,
     shard_plan,
     ShardPlan,
+    LocalSchur,
+    SchurFromLocals,
+    pcg,
+    SGW_ENOCONV,
     triple_products,
     write_sg_outputs,
     kle_spectrum,

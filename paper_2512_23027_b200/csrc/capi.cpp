@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/sgw.h"
+#include "generic.cuh"
 #include "solver.cuh"
 
 using namespace sgw;
@@ -71,6 +72,34 @@ void iface_op(GpuSolver& g, const double* x, double* y, F&& op) {
   op(lx.p, ly.p);
   g.iface_to_global(ly.p, gy.p);
   d2h(y, gy.p, g.NGG, g.stream());
+}
+}  // namespace
+
+struct sgw_schur {
+  std::unique_ptr<GenericSchur> g;
+};
+
+namespace {
+template <typename F>
+int gschur_apply(sgw_schur* h, const double* in, double* out, F&& f) {
+  return guard([&] {
+    GenericSchur& g = *h->g;
+    const long long n = g.n_global();
+    DBuf<double> a, b;
+    a.alloc(std::max<long long>(1, n)), b.alloc(std::max<long long>(1, n));
+    SGW_CUDA(cudaMemcpyAsync(a.p, in, n * 8, cudaMemcpyHostToDevice, g.stream()));
+    f(g, a.p, b.p);
+    SGW_CUDA(cudaMemcpyAsync(out, b.p, n * 8, cudaMemcpyDeviceToHost, g.stream()));
+    SGW_CUDA(cudaStreamSynchronize(g.stream()));
+  });
+}
+void report_out(int it, bool conv, const std::vector<double>& h, int* iterations, int* converged, double* hist,
+                int hist_cap, int* hist_len) {
+  if (iterations) *iterations = it;
+  if (converged) *converged = conv ? 1 : 0;
+  if (hist_len) *hist_len = (int)h.size();
+  if (hist)
+    for (int i = 0; i < std::min<int>(hist_cap, (int)h.size()); ++i) hist[i] = h[i];
 }
 }  // namespace
 
@@ -452,6 +481,102 @@ int sgw_bench_kernel(sgw_solver* s, int which, int reps, double* out) {
     cudaEventDestroy(b);
     g.KP.collect();
     out[0] = total / reps;
+  });
+}
+
+
+int sgw_schur_from_locals(long long n_global, long long n_corner, int n_locals, const sgw_local_schur* locals,
+                          sgw_schur** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (n_locals < 0 || (n_locals > 0 && !locals)) throw Error(SGW_EINVAL, "schur_from_locals: no locals");
+    std::vector<GenericSchur::LocalInput> in(n_locals);
+    for (int s = 0; s < n_locals; ++s) {
+      const sgw_local_schur& l = locals[s];
+      in[s].n = l.n, in[s].nr = l.nr, in[s].nc = l.nc;
+      in[s].S = l.S, in[s].gmap = l.gmap, in[s].weights = l.weights;
+      in[s].r_idx = l.r_idx, in[s].c_idx = l.c_idx, in[s].corner_gmap = l.corner_gmap;
+    }
+    auto h = std::make_unique<sgw_schur>();
+    h->g = std::make_unique<GenericSchur>(n_global, n_corner, in);
+    *out = h.release();
+  });
+}
+
+void sgw_schur_free(sgw_schur* h) { delete h; }
+
+
+int sgw_gschur_matvec(sgw_schur* h, const double* x, double* y) {
+  return gschur_apply(h, x, y, [](GenericSchur& g, const double* a, double* b) { g.matvec(a, b); });
+}
+
+int sgw_gschur_apply_nn2(sgw_schur* h, const double* r, double* z) {
+  return gschur_apply(h, r, z, [](GenericSchur& g, const double* a, double* b) { g.apply_nn2(a, b); });
+}
+
+int sgw_gschur_coarse_operator(sgw_schur* h, double* F) {
+  return guard([&] {
+    const auto& f = h->g->coarse_operator();
+    std::memcpy(F, f.data(), f.size() * sizeof(double));
+  });
+}
+
+int sgw_gschur_pcg(sgw_schur* h, const double* b, double tol, int max_iter, double* x, int* iterations,
+                   int* converged, double* hist, int hist_cap, int* hist_len) {
+  return guard([&] {
+    GenericSchur& g = *h->g;
+    const long long n = g.n_global();
+    DBuf<double> db, dx;
+    db.alloc(std::max<long long>(1, n)), dx.alloc(std::max<long long>(1, n));
+    SGW_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, g.stream()));
+    bool conv = false;
+    std::vector<double> hh;
+    const int it = pcg_generic(
+        g.blas(), g.stream(), n, [&](const double* a, double* c) { g.matvec(a, c); },
+        [&](const double* a, double* c) { g.apply_nn2(a, c); }, db.p, dx.p, tol, max_iter, &conv, &hh);
+    SGW_CUDA(cudaMemcpy(x, dx.p, n * 8, cudaMemcpyDeviceToHost));
+    report_out(it, conv, hh, iterations, converged, hist, hist_cap, hist_len);
+  });
+}
+
+int sgw_pcg_ops(long long n, sgw_host_op op, void* op_ctx, sgw_host_op precond, void* precond_ctx, const double* b,
+                double tol, int max_iter, double* x, int* iterations, int* converged, double* hist, int hist_cap,
+                int* hist_len) {
+  return guard([&] {
+    if (!op || n < 0) throw Error(SGW_EINVAL, "pcg: no operator");
+    cudaStream_t st;
+    cublasHandle_t blas;
+    SGW_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) throw Error(SGW_ECUDA, "cublasCreate failed");
+    cublasSetStream(blas, st);
+    struct Cleanup {
+      cudaStream_t s;
+      cublasHandle_t b;
+      ~Cleanup() {
+        cublasDestroy(b);
+        cudaStreamDestroy(s);
+      }
+    } cleanup{st, blas};
+    std::vector<double> hx(std::max<long long>(1, n)), hy(std::max<long long>(1, n));
+    auto host_op = [&](sgw_host_op f, void* ctx) {
+      return [&, f, ctx](const double* a, double* c) {
+        SGW_CUDA(cudaMemcpyAsync(hx.data(), a, n * 8, cudaMemcpyDeviceToHost, st));
+        SGW_CUDA(cudaStreamSynchronize(st));
+        if (f) f(ctx, n, hx.data(), hy.data());
+        else std::memcpy(hy.data(), hx.data(), n * 8);
+        SGW_CUDA(cudaMemcpyAsync(c, hy.data(), n * 8, cudaMemcpyHostToDevice, st));
+        SGW_CUDA(cudaStreamSynchronize(st));
+      };
+    };
+    DBuf<double> db, dx;
+    db.alloc(std::max<long long>(1, n)), dx.alloc(std::max<long long>(1, n));
+    SGW_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, st));
+    bool conv = false;
+    std::vector<double> hh;
+    const int it = pcg_generic(blas, st, n, host_op(op, op_ctx), host_op(precond, precond_ctx), db.p, dx.p, tol,
+                               max_iter, &conv, &hh);
+    SGW_CUDA(cudaMemcpy(x, dx.p, n * 8, cudaMemcpyDeviceToHost));
+    report_out(it, conv, hh, iterations, converged, hist, hist_cap, hist_len);
   });
 }
 

@@ -428,6 +428,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   scal.alloc(16), scal.zero(st_);
   dpart.alloc(1024), dcount.alloc(4), dcount.zero(st_);
   setup_fused_pcg();
+  build_coupling_blocks();  // A_GI / A_IG and interface-row force blocks, memory permitting
   SGW_CUDA(cudaStreamSynchronize(st_));
   setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

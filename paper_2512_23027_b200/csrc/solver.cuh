@@ -253,7 +253,7 @@ class GpuSolver {
   DBuf<int> d_probe_dofs, d_probe_own;  // own: sharded runs, probe dof owned by this rank
   DBuf<double> probe_hist;  // [step][probe][2 + P+1]: mean, std, u_0 .. u_P
   int probe_cap = 0;
-  void record_probes(int step);
+  void record_probes(int step, const int* conv = nullptr);  // conv: skip unless *conv (device flag)
   double last_rel = 0.0;  // final true residual of the last PCG solve
 
  private:

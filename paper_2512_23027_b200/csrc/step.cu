@@ -6,6 +6,7 @@
 // src/sg.cpp:358-423 (run), src/sg.cpp:425-447 (apply_block_*),
 // src/newmark.cpp:16-49.
 #include <cmath>
+#include <cstdlib>
 
 #include "solver.cuh"
 
@@ -387,15 +388,33 @@ void GpuSolver::build_coupling_blocks() {
   }
   cpl_edge_.upload(edges), cpl_q_cls_.upload(qcls), cpl_iptr_.upload(iptr), cpl_iedge_.upload(iedge);
   cpl_aptr_.upload(aptr), cpl_aedge_.upload(aedge);
-  cpl_blk_.alloc(std::max<size_t>(1, edges.size() * (size_t)NT * NT));
-  if (!edges.empty()) {
+  // Built once at setup and only while they leave >= 1 GiB free: without them
+  // the step uses the stencil kernels (coupling_kernel / local_force_kernel),
+  // which need no extra memory.  Reduced-memory mode skips the force blocks.
+  auto fits = [&](size_t bytes) {
+    if (std::getenv("SGW_NO_CPL_BLOCKS")) return false;  // test hook: the stencil kernels
+    size_t fr = 0, tot = 0;
+    SGW_CUDA(cudaMemGetInfo(&fr, &tot));
+    return bytes + (size_t(1) << 30) <= fr;
+  };
+  auto try_alloc = [&](DBuf<double>& b, size_t count) {
+    if (!fits(count * sizeof(double))) return false;
+    try {
+      b.alloc(count);
+      return true;
+    } catch (const Error&) {
+      (void)cudaGetLastError();
+      return false;
+    }
+  };
+  const size_t cb = edges.size() * (size_t)NT * NT;
+  if (cb > 0 && try_alloc(cpl_blk_, cb)) {
     coupling_block_kernel<<<(unsigned)edges.size(), 32, 0, st_>>>(local_args(), cpl_edge_.p, cpl_blk_.p);
     SGW_LAUNCHED();
   }
-  // local-force stiffness blocks of the interface list (skipped when large)
+  // local-force stiffness blocks of the interface list
   const size_t fb = (size_t)n_ilist_ * 5 * NT * NT;
-  if (fb > 0 && fb * sizeof(double) <= (size_t(4) << 30)) {
-    frc_blk_.alloc(fb);
+  if (fb > 0 && !P.implicit_schur && fb * sizeof(double) <= (size_t(4) << 30) && try_alloc(frc_blk_, fb)) {
     force_block_kernel<<<(unsigned)(n_ilist_ * 5), 32, 0, st_>>>(local_args(), ilist_.p, frc_blk_.p);
     SGW_LAUNCHED();
   }
@@ -420,11 +439,16 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
                               const double* __restrict__ ug, const double* __restrict__ yI,
                               const double* __restrict__ wI, const int* __restrict__ iface_of_dof, int n, int nt,
                               int n_iface, int nx, int ny, int px, int py, int H, int B,
-                              const int* __restrict__ gid_local, double dt, double zeta, double gamma) {
-  const int N = n * nt;  // < 2^31 (GpuSolver ctor): 32-bit index arithmetic
+                              const int* __restrict__ gid_local, double dt, double zeta, double gamma,
+                              const int* __restrict__ conv) {
+  // conv: the persistent PCG's convergence flag; an unconverged solve leaves the
+  // state untouched (the reference throws before newmark_update, sg.cpp:412-416)
+  if (conv && *conv == 0) return;
+  const int N = n * nt;  // < 2^31 (GpuSolver ctor): 32-bit derived indices
   const double zdd = zeta * dt * dt, c1 = (1.0 - 2.0 * zeta) / (2.0 * zeta);
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N; t += gridDim.x * blockDim.x) {
-    const int d = t % n, k = t / n;
+  // 64-bit loop variable: t + stride must not overflow near N = 2^31 - 1
+  for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < N; tt += (long long)gridDim.x * blockDim.x) {
+    const int t = int(tt), d = t % n, k = t / n;
     const int q = iface_of_dof[d];
     double un;
     if (q >= 0) {
@@ -448,7 +472,8 @@ __global__ void update_kernel(double* __restrict__ u, double* __restrict__ v, do
 }
 
 __global__ void probe_kernel(const double* __restrict__ u, const int* __restrict__ pd, const int* __restrict__ own,
-                             int np, int n, int nt, double* __restrict__ out) {
+                             int np, int n, int nt, double* __restrict__ out, const int* __restrict__ conv) {
+  if (conv && *conv == 0) return;  // unconverged step: no new history row
   // per probe: mean, std, then every chaos coefficient u_0 .. u_P (sg.cpp:391-405)
   for (int p = threadIdx.x; p < np; p += blockDim.x) {
     double* o = out + (long long)p * (2 + nt);
@@ -592,12 +617,12 @@ void GpuSolver::init_state(const double* u0_nodal, const double* v0_nodal, doubl
   SGW_CUDA(cudaStreamSynchronize(st_));
 }
 
-void GpuSolver::record_probes(int k) {
+void GpuSolver::record_probes(int k, const int* conv) {
   if (probe_dofs.empty() || k >= probe_cap) return;
   const size_t w = probe_dofs.size() * (2 + NT);
   double* row = probe_hist.p + (size_t)k * w;
   probe_kernel<<<1, 128, 0, st_>>>(u.p, d_probe_dofs.p, comm_ ? d_probe_own.p : nullptr, (int)probe_dofs.size(), n,
-                                   NT, row);
+                                   NT, row, conv);
   SGW_LAUNCHED();
   allreduce(row, w);
 }
@@ -632,7 +657,9 @@ __global__ void interior_from_global_kernel(LocalArgs A, int n, const double* __
                                             double* __restrict__ yI, int ns) {
   const int total = ns * A.H * A.B;  // < 2^31 (GpuSolver ctor)
   const int rw = A.nx - 1, rh = A.ny - 1;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < total;
+       tt += (long long)gridDim.x * blockDim.x) {
+    const int t = int(tt);
     const int row = t % A.B, jl = (t / A.B) % A.H + 1, s = t / (A.B * A.H);
     const int il = row / A.nt + 1, k = row % A.nt;
     const int lid = jl * (A.mx + 1) + il;
@@ -686,7 +713,6 @@ int GpuSolver::step(int* iters_out) {
     interior_from_global_kernel<<<std::min(cdiv(tI, 256), 65535), 256, 0, st_>>>(A, n, yglob_.p, Mg.p, um.p, fvec,
                                                                                    fdof, fval, yI.p, NS);
     SGW_LAUNCHED();
-    if (!cpl_built_) build_coupling_blocks();
     if (frc_blk_.p)
       local_force_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
           A, n, um.p, uc.p, P.alpha0, P.alpha1, fvec, fdof, fval, iface_w.p, ip_off.p, fG.p, ilist_.p, n_ilist_,
@@ -701,10 +727,13 @@ int GpuSolver::step(int* iters_out) {
   }
   SGW_LAUNCHED();
   sweep(yI.p);  // y = A_II^-1 f_I
-  if (!cpl_built_) build_coupling_blocks();
-  coupling_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
-      A, 0, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_iptr_.p, cpl_iedge_.p, ilist_.p, n_ilist_, yI.p, fG.p,
-      nullptr, li_y.p, nullptr);
+  if (cpl_blk_.p)
+    coupling_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+        A, 0, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_iptr_.p, cpl_iedge_.p, ilist_.p, n_ilist_, yI.p, fG.p,
+        nullptr, li_y.p, nullptr);
+  else  // no room for the coupling blocks: the stencil form
+    coupling_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+        A, 0, yI.p, fG.p, nullptr, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
   SGW_LAUNCHED();
   scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
   halo_sum(vb.p);
@@ -726,25 +755,31 @@ int GpuSolver::step(int* iters_out) {
   // A_IG u_G is non-zero only on interior nodes next to the interface
   SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
   if (n_alist_ > 0) {
-    coupling_blk_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
-        A, 1, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_aptr_.p, cpl_aedge_.p, alist_.p, n_alist_, nullptr,
-        nullptr, li_x.p, nullptr, wI.p);
+    if (cpl_blk_.p)
+      coupling_blk_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
+          A, 1, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_aptr_.p, cpl_aedge_.p, alist_.p, n_alist_, nullptr,
+          nullptr, li_x.p, nullptr, wI.p);
+    else
+      coupling_kernel<<<std::max(1, std::min(cdiv(ta, 128), 65535)), 128, 0, st_>>>(
+          A, 1, nullptr, nullptr, li_x.p, ip_off.p, iface_lid_.p, nullptr, wI.p, NS, alist_.p, n_alist_);
     SGW_LAUNCHED();
   }
   sweep(wI.p);  // A_II^-1 A_IG u_G
   update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
-                                       P.ny, G.px, G.py, G.H, B, gid_local_d_.p, P.dt, P.zeta, P.gamma);
+                                       P.ny, G.px, G.py, G.H, B, gid_local_d_.p, P.dt, P.zeta, P.gamma,
+                                       deferred ? fused_out_.p + 1 : nullptr);
   SGW_LAUNCHED();
-  t_now = t_now + P.dt;
-  ++step_index;
-  record_probes(step_index);
+  record_probes(step_index + 1, deferred ? fused_out_.p + 1 : nullptr);
   cudaEventRecord(ev_[5], st_);
   SGW_CUDA(cudaEventSynchronize(ev_[5]));
   if (deferred) {
+    // the update and the probe row were conditional on the device-side flag:
+    // on non-convergence the state, time and step index stay where they were
     it = pcg_fused_finish(&conv, nullptr);
-    if (!conv)
-      throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index - 1));
+    if (!conv) throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
   }
+  t_now = t_now + P.dt;
+  ++step_index;
   KP.collect();
   float ms_rhs = 0, ms_rec = 0, ms_all = 0;
   cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);

@@ -97,6 +97,15 @@ def load_library():
                                       C.c_longlong]
     L.sgw_nearest_node.argtypes = [ip, ip, dp, dp]
     L.sgw_kle_spectrum.argtypes = [dp, dp, dp, ip, vp]
+    L.sgw_schur_from_locals.argtypes = [C.c_longlong, C.c_longlong, ip, vp, C.POINTER(vp)]
+    L.sgw_schur_free.argtypes = [vp]
+    L.sgw_schur_free.restype = None
+    for nm in ("sgw_gschur_matvec", "sgw_gschur_apply_nn2"):
+        getattr(L, nm).argtypes = [vp, vp, vp]
+    L.sgw_gschur_coarse_operator.argtypes = [vp, vp]
+    L.sgw_gschur_pcg.argtypes = [vp, vp, dp, ip, vp, C.POINTER(ip), C.POINTER(ip), vp, ip, C.POINTER(ip)]
+    L.sgw_pcg_ops.argtypes = [C.c_longlong, _HOST_OP, vp, _HOST_OP, vp, vp, dp, ip, vp, C.POINTER(ip), C.POINTER(ip), vp, ip,
+                              C.POINTER(ip)]
     L.sgw_pce_indices.argtypes = [ip, ip, vp, C.c_longlong, C.POINTER(ip)]
     L.sgw_nccl_unique_id.argtypes = [vp]
     L.sgw_shard_plan.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp]
@@ -454,6 +463,117 @@ class SchurSystem:
 
 
 PRECONDS = ("nn2", "nn1", "lumped")
+
+
+class _LocalSchurC(C.Structure):  # sgw_local_schur
+    _fields_ = [("n", C.c_int), ("S", C.c_void_p), ("gmap", C.c_void_p), ("weights", C.c_void_p),
+                ("nr", C.c_int), ("r_idx", C.c_void_p), ("nc", C.c_int), ("c_idx", C.c_void_p),
+                ("corner_gmap", C.c_void_p)]
+
+
+@dataclass
+class LocalSchur:
+    """include/sgwave/dd.hpp:50-62: a subdomain's dense local Schur complement S
+    (n x n), local -> global flat interface map, weights D_s, the remaining
+    (r_idx) and corner (c_idx) local indices and the corners' global indices."""
+    S: np.ndarray
+    gmap: np.ndarray
+    weights: np.ndarray
+    r_idx: np.ndarray
+    c_idx: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    corner_gmap: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+
+
+class SchurFromLocals:
+    """SchurSystem{n_global, n_corner, locals} with finalize() done on the GPU
+    (src/dd.cpp:98-140), built from hand-made LocalSchur data as
+    test_dd.cpp:123-151 does: matvec, apply_nn2, coarse_operator, pcg."""
+
+    def __init__(self, n_global, n_corner, locals_):
+        self.n_global, self.n_corner = int(n_global), int(n_corner)
+        self._keep = []
+        arr = (_LocalSchurC * max(1, len(locals_)))()
+        for s, ls in enumerate(locals_):
+            n = int(np.asarray(ls.gmap).size)
+            S = np.asfortranarray(np.asarray(ls.S, np.float64).reshape(n, n))
+            gm = np.ascontiguousarray(ls.gmap, np.int64)
+            w = np.ascontiguousarray(ls.weights, np.float64)
+            ri = np.ascontiguousarray(ls.r_idx, np.int32)
+            ci = np.ascontiguousarray(ls.c_idx, np.int32)
+            cg = np.ascontiguousarray(ls.corner_gmap, np.int64)
+            self._keep += [S, gm, w, ri, ci, cg]
+            arr[s] = _LocalSchurC(n, S.ctypes.data, gm.ctypes.data, w.ctypes.data, ri.size, ri.ctypes.data,
+                                  ci.size, ci.ctypes.data, cg.ctypes.data)
+        self._h = C.c_void_p()
+        _check(load_library().sgw_schur_from_locals(self.n_global, self.n_corner, len(locals_), arr,
+                                                    C.byref(self._h)))
+        self._keep = []
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load_library().sgw_schur_free(self._h)
+            self._h = None
+
+    def _apply(self, fn, x):
+        x = _f64(x)
+        y = np.zeros(self.n_global)
+        _check(fn(self._h, _p(x), _p(y)))
+        return y
+
+    def matvec(self, x):
+        return self._apply(load_library().sgw_gschur_matvec, x)
+
+    def apply_nn2(self, r):
+        return self._apply(load_library().sgw_gschur_apply_nn2, r)
+
+    def coarse_operator(self):
+        F = np.zeros((self.n_corner, self.n_corner), order="F")
+        _check(load_library().sgw_gschur_coarse_operator(self._h, _p(F)))
+        return np.asarray(F)
+
+    def pcg(self, rhs, tol=1e-10, max_iter=500):
+        rhs = _f64(rhs)
+        x = np.zeros(self.n_global)
+        it, conv, hl = C.c_int(), C.c_int(), C.c_int()
+        hist = np.zeros(max_iter + 2)
+        _check(load_library().sgw_gschur_pcg(self._h, _p(rhs), tol, max_iter, _p(x), C.byref(it), C.byref(conv),
+                                             _p(hist), hist.size, C.byref(hl)))
+        return x, {"iterations": it.value, "converged": bool(conv.value), "residual_history": hist[:hl.value].copy()}
+
+
+_HOST_OP = C.CFUNCTYPE(None, C.c_void_p, C.c_longlong, C.POINTER(C.c_double), C.POINTER(C.c_double))
+
+
+def pcg(apply_op, apply_precond, rhs, tol, max_iter):
+    """pcg(LinearOp, LinearOp, rhs, tol, max_iter) -> (x, PcgReport)
+    (include/sgwave/pcg.hpp:15-21, src/pcg.cpp:7-50): the CG recurrence runs on
+    the GPU (sgw_pcg_ops); apply_op / apply_precond are Python callables on
+    numpy vectors (apply_precond None: identity)."""
+    rhs = _f64(rhs)
+    n = rhs.size
+    err = []
+
+    def wrap(f):
+        def cb(_ctx, m, x, y):
+            try:
+                xv = np.ctypeslib.as_array(x, shape=(m,))
+                np.ctypeslib.as_array(y, shape=(m,))[:] = np.asarray(f(xv.copy()), np.float64)
+            except BaseException as e:  # noqa: BLE001 - re-raised after the call
+                err.append(e)
+                np.ctypeslib.as_array(y, shape=(m,))[:] = np.nan
+        return _HOST_OP(cb)
+
+    cop = wrap(apply_op)
+    cpre = wrap(apply_precond) if apply_precond is not None else _HOST_OP()
+    x = np.zeros(n)
+    it, conv, hl = C.c_int(), C.c_int(), C.c_int()
+    hist = np.zeros(max_iter + 2)
+    rc = load_library().sgw_pcg_ops(n, cop, None, cpre, None, _p(rhs), tol, max_iter, _p(x), C.byref(it),
+                                    C.byref(conv), _p(hist), hist.size, C.byref(hl))
+    if err:
+        raise err[0]
+    _check(rc)
+    return x, {"iterations": it.value, "converged": bool(conv.value), "residual_history": hist[:hl.value].copy()}
 
 
 def precond_from_string(name) -> int:

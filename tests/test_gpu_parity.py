@@ -467,3 +467,41 @@ def test_reduced_memory_mode_matches_oracle(gpu, cfg):
     hc = c.run(z, z, 8, force_node=node, store_full=True)
     assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["fused", "host", "phase"])
+def test_nonconvergence_leaves_state_unadvanced(gpu, monkeypatch, mode):
+    # sg.cpp:412-416: a step whose interface PCG fails throws before
+    # newmark_update.  The persistent PCG's verdict is read after the step's
+    # update is queued, so the update and the probe row are conditional on the
+    # device-side flag: the state, the time and the step index stay put.
+    if mode != "fused":
+        monkeypatch.setenv("SGW_PCG", mode)
+    nx = 16
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, 2, 2)
+    t = O.triple_products(2, 2, 2)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    g = sg.SgSolver(nx, nx, 2, 2, coeff, t, params=sg.NewmarkParams(dt=1e-3),
+                    options=sg.SgOptions(tol=1e-14, max_iter=1, probe_nodes=[node]))
+    z = np.zeros((nx + 1) ** 2)
+    g.init_state(O.gaussian_pulse(nx, nx), z)
+    u0 = g.state()
+    with pytest.raises(sg.SgError) as e:
+        g.advance(1)
+    assert e.value.code == sg.SGW_ENOCONV
+    assert np.array_equal(g.state(), u0)
+
+
+def test_step_without_coupling_blocks_matches_oracle(gpu, monkeypatch):
+    # the coupling / interface-force blocks are built at setup only while
+    # memory allows; without them the step takes the stencil
+    # kernels (coupling_kernel, local_force_kernel): same trajectory
+    monkeypatch.setenv("SGW_NO_CPL_BLOCKS", "1")
+    nx = 24
+    g, c = pair(nx, 3, 2, 0.3, 0.5, 2, 4, 2, 1e-3)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(z, z, 6, sg.ForceSpec(node=node))
+    hc = c.run(z, z, 6, force_node=node, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
