@@ -51,6 +51,11 @@ def workload_desc(name, c):
             f"alpha0={ALPHA0} alpha1={ALPHA1}, PCG tol {TOL}, fp64")
 
 
+# FP64 FMA peak measured on this pool's B200s (tools/bench_fp64.cu,
+# profiles/r02_fp64_peak.txt: 16.77 TFMA/s with 32 warps/SM x 8 chains)
+FP64_TFLOPS = 2 * 16.77
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -138,8 +143,8 @@ def cpu_oracle_run(c, warmup, steps, threads):
     else:
         t_run, t_pcg, iters = out["t_run"], out["t_pcg"], out["total_iterations"]
     gdof = s.n_terms * (nx + 1) ** 2
-    return {"value": gdof * iters / t_pcg / 1e9, "s_per_step": t_run / steps, "iterations": iters,
-            "setup_s": setup, "pcg_s": t_pcg, "n_terms": s.n_terms}
+    return {"value": gdof * iters / t_pcg / 1e9, "value_step": gdof * iters / t_run / 1e9, "s_per_step": t_run / steps,
+            "iterations": iters, "setup_s": setup, "pcg_s": t_pcg, "n_terms": s.n_terms}
 
 
 def run_reference(args, c, name):
@@ -157,7 +162,10 @@ def run_reference(args, c, name):
             "config": {"workload": workload_desc(name, c), "GDOF": r["n_terms"] * (c["nx"] + 1) ** 2 / 1e9},
             "s_per_newmark_step": r["s_per_step"], "pcg_iterations": r["iterations"],
             "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
-            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            # e2e: iterations over the WHOLE time-loop wall time (RHS, interior
+            # solves, recovery included): the same definition as the GPU arm's e2e
+            "e2e": {"value": r["value_step"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "sum(iterations) (P+1) N / whole time-loop wall time (as the GPU arm's e2e)"},
             "note": "reference C++ needs Eigen3 and vendored doctest/CLI11/json (absent): oracle/ restatement timed"}
     print(json.dumps(line), flush=True)
 
@@ -307,10 +315,20 @@ def main():
                for k, v in classes.items()}
     # standalone fused SG-operator apply (apply_block_transient, K11), outside the timed region
     sgop_ms = solver.bench_kernel(2, reps=20)
-    sgop_bytes = kp["sg_operator"][2]
-    kernels["sg_operator_standalone"] = {"ms_per_launch": sgop_ms, "algorithmic_bytes_per_launch": sgop_bytes,
-                                         "achieved_GBs": sgop_bytes / (sgop_ms / 1e3) / 1e9,
-                                         "frac_of_peak": sgop_bytes / (sgop_ms / 1e3) / 1e9 / peak}
+    sgop_bytes, sgop_flops = kp["sg_operator"][2], kp["sg_operator_flops"]
+    # roofline = max(bytes / HBM peak, flops / FP64 peak); the
+    # 3-value stored-stencil form's bytes 8 n (3 n_in + 2 (P+1)) for reference
+    n_dofs = (nx - 1) ** 2
+    b3 = 8.0 * n_dofs * (3 * tensor.n_input + 2 * tensor.n_output)
+    t_roof = max(sgop_bytes / (peak * 1e9), sgop_flops / (FP64_TFLOPS * 1e12))
+    kernels["sg_operator_standalone"] = {
+        "ms_per_launch": sgop_ms, "algorithmic_bytes_per_launch": sgop_bytes, "algorithmic_flops_per_launch": sgop_flops,
+        "achieved_GBs": sgop_bytes / (sgop_ms / 1e3) / 1e9, "achieved_TFLOPs": sgop_flops / (sgop_ms / 1e3) / 1e12,
+        "frac_of_peak": sgop_bytes / (sgop_ms / 1e3) / 1e9 / peak,
+        "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (sgop_ms / 1e3),
+        "fp64_peak_TFLOPs": FP64_TFLOPS,
+        "frac_vs_3value_stored_form": b3 / (sgop_ms / 1e3) / 1e9 / peak,
+        "note": "2 stored couplings per node and term (sgop.cu); L2 flushed (read) before each launch"}
     b_iter = kp["bytes_per_pcg_iteration"]
     iter_ms = pcg_ms / max(iters, 1)
     line = {
@@ -372,7 +390,11 @@ def main():
         line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"{args.config} full problem, setup excluded ({r['setup_s']:.0f} s), "
                                           f"1 warm-up + {args.cpu_steps} timed Newmark steps, PCG time only",
-                                "s_per_newmark_step": r["s_per_step"]}
+                                "s_per_newmark_step": r["s_per_step"], "e2e_value": r["value_step"]}
+        # per Newmark step, device-resident GPU step vs the oracle's whole step
+        line["per_step_speedup_vs_cpu_baseline"] = r["s_per_step"] / (ms / args.steps / 1e3)
+        if "e2e" in line:
+            line["e2e"]["speedup_vs_cpu_baseline_e2e"] = line["e2e"]["value"] / r["value_step"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if torch.distributed.is_initialized():

@@ -258,6 +258,9 @@ int sgw_local_group_new(int world_size, void** group);
  * configurations that need several GPUs (C4); results are not physical.     */
 int sgw_create_solo(const sgw_problem* problem, int world_size, int rank, sgw_solver** out);
 int sgw_local_group_free(void* group);
+/* a failed rank's thread releases the others: their pending and later
+ * collectives fail with SGW_ENCCL instead of waiting forever.            */
+int sgw_local_group_abort(void* group);
 int sgw_create_local_group(const sgw_problem* problem, int world_size, int rank, void* group,
                            sgw_solver** out);
 

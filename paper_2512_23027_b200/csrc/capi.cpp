@@ -185,6 +185,10 @@ int sgw_local_group_new(int world_size, void** group) {
   });
 }
 
+int sgw_local_group_abort(void* group) {
+  return guard([&] { thread_group_abort(**static_cast<std::shared_ptr<ThreadGroup>*>(group)); });
+}
+
 int sgw_local_group_free(void* group) {
   return guard([&] { delete static_cast<std::shared_ptr<ThreadGroup>*>(group); });
 }

@@ -95,18 +95,28 @@ struct ThreadGroup {
   std::condition_variable cv;
   int arrived = 0;
   long long generation = 0;
+  bool broken = false;  // a rank failed: every barrier throws from now on
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (broken) throw Error(5, "local group aborted (another rank failed)");
     const long long gen = generation;
     if (++arrived == world) {
       arrived = 0;
       ++generation;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return generation != gen; });
+      cv.wait(lk, [&] { return generation != gen || broken; });
+      if (generation == gen) throw Error(5, "local group aborted (another rank failed)");
     }
   }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
 };
+
+void thread_group_abort(ThreadGroup& g) { g.abort(); }
 
 std::shared_ptr<ThreadGroup> make_thread_group(int world) { return std::make_shared<ThreadGroup>(world); }
 

@@ -47,6 +47,7 @@ std::unique_ptr<Comm> make_nccl_comm(const void* id128, int rank, int world, int
 
 struct ThreadGroup;
 std::shared_ptr<ThreadGroup> make_thread_group(int world);
+void thread_group_abort(ThreadGroup& g);  // a failed rank releases the others (their collectives throw)
 std::unique_ptr<Comm> make_thread_comm(std::shared_ptr<ThreadGroup> group, int rank);
 std::unique_ptr<Comm> make_solo_comm(int rank, int world);
 

@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -37,6 +39,20 @@ constexpr int kNumSMs = 148;
 constexpr int kTile = 64;  // tile edge of the packed symmetric matrices
 
 inline int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-function, process-wide
+// setting: solvers of one process (e.g. LocalGroup ranks with different local
+// sizes) must leave it at the largest size any of them launches with.
+inline void ensure_dyn_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[fn];
+  if (bytes > c) {
+    SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    c = bytes;
+  }
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -42,55 +42,16 @@ __global__ void scatter_add_kernel(const double* __restrict__ v, const long long
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
     out[map[k]] += w ? v[k] * w[k] : v[k];
 }
-__global__ void shift_diag_kernel(double* a, int n, double shift) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) a[(long long)k * n + k] += shift;
-}
-__global__ void mirror_lower_kernel(double* a, int n) {  // lower -> full symmetric
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)n * n;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int r = int(t % n), c = int(t / n);
-    if (r < c) a[t] = a[(long long)r * n + c];
-  }
-}
 int grid_of(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 1024)); }
 }  // namespace
 
-// A <- A^-1 for a symmetric positive definite n x n (column-major, device):
-// Cholesky; on failure one retry with 1e-10 trace / n on the diagonal
-// (llt_regularized, src/dd.cpp:66-76); then the explicit inverse.
+// A <- A^-1 (SPD, column-major, device): setup.cu's spd_inverse, i.e.
+// llt_regularized (src/dd.cpp:66-76) then the explicit inverse
 void spd_inverse_inplace(cusolverDnHandle_t sol, cudaStream_t st, double* A, int n) {
-  if (n == 0) return;
-  DBuf<double> keep;
-  keep.alloc((size_t)n * n);
-  SGW_CUDA(cudaMemcpyAsync(keep.p, A, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, st));
-  int lw = 0;
-  if (cusolverDnDpotrf_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, n, A, n, &lw) != CUSOLVER_STATUS_SUCCESS)
-    throw Error(4, "cusolverDnDpotrf_bufferSize failed");
   DBuf<double> work;
   DBuf<int> info;
-  work.alloc(std::max(1, lw)), info.alloc(1);
-  auto factor = [&]() {
-    if (cusolverDnDpotrf(sol, CUBLAS_FILL_MODE_LOWER, n, A, n, work.p, lw, info.p) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(4, "cusolverDnDpotrf failed");
-    int h = 0;
-    SGW_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SGW_CUDA(cudaStreamSynchronize(st));
-    return h == 0;
-  };
-  if (!factor()) {
-    std::vector<double> d((size_t)n * n);
-    SGW_CUDA(cudaMemcpy(d.data(), keep.p, d.size() * 8, cudaMemcpyDeviceToHost));
-    double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += d[(size_t)i * n + i];
-    SGW_CUDA(cudaMemcpyAsync(A, keep.p, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, st));
-    shift_diag_kernel<<<grid_of(n), 256, 0, st>>>(A, n, 1e-10 * tr / n);
-    SGW_LAUNCHED();
-    if (!factor()) throw Error(2, "local Schur factorization failed");
-  }
-  if (cusolverDnDpotri(sol, CUBLAS_FILL_MODE_LOWER, n, A, n, work.p, lw, info.p) != CUSOLVER_STATUS_SUCCESS)
-    throw Error(4, "cusolverDnDpotri failed");
-  mirror_lower_kernel<<<grid_of((long long)n * n), 256, 0, st>>>(A, n);
-  SGW_LAUNCHED();
+  info.alloc(1);
+  spd_inverse(sol, st, A, n, work, info, "local Schur");
 }
 
 GenericSchur::GenericSchur(long long n_global, long long n_corner, const std::vector<LocalInput>& in)

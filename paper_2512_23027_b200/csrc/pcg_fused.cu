@@ -66,6 +66,13 @@ struct FusedPcg {
   int* st;                       // [ST_IT], [ST_HL], [ST_EXIT], [ST_FIRST], [ST_PFIRST]
   unsigned long long cond;       // conditional handle of the graph's WHILE loop
   int use_cond;
+  int l2_keep;                   // tile loads with the default L2 policy (the tile set fits in L2)
+  // glue descriptors per (interface node gq, slot e): 4 * gq + e (build_scatter_desc)
+  const int4* ifd;   // {S-local base (-1: unused slot), S-local term stride, fr / fc base, fr stride (> 0) or -(fc stride)}
+  const double* ifw; // partition-of-unity weight of the slot
+  const int4* sred;  // S partials {base, term stride, CTA stride, CTAs} (CTAs 0: unused)
+  const int4* zred;  // Q partials {base, term stride, CTA stride, CTAs}; CTAs -1: corner (ucl base, stride); -2: unused
+  const int4* pred;  // Psi (remaining-dof part) partials {base, term stride, CTA stride, CTAs}
 };
 enum { SC_RZ = 0, SC_BNORM = 1, SC_BETA = 2 };
 enum { ST_IT = 0, ST_HL = 1, ST_EXIT = 2, ST_FIRST = 3, ST_PFIRST = 4 };
@@ -114,8 +121,17 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
 // Streamed tiles are read once per phase and are far larger than L2: load
 // them evict-first so that Psi, F_cc^-1, the partials and the vectors stay
 // resident in L2 across phases.
-__device__ __forceinline__ void mb_load(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+// keep: the whole tile set fits in L2 (small configs such as C1): the default
+// policy, so the tiles stay L2-resident across iterations.
+__device__ __forceinline__ void mb_load(void* dst, const void* src, unsigned bytes, unsigned long long* b, bool keep) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+  if (keep) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(b))
+                 : "memory");
+    return;
+  }
   asm volatile(
       "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
       " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}" ::"r"(
@@ -134,6 +150,7 @@ struct Ring {
   int nst;
   int consumed, issued;  // consumed: uniform; issued: thread 0
   int pre_kind;          // tile set whose first tiles are already issued for the next phase
+  int keep;              // L2 policy of the tile loads (mb_load)
 };
 
 // tile k of this CTA's range of P, continuing into the range of `next` past
@@ -151,7 +168,7 @@ __device__ __forceinline__ void ring_issue(Ring& R, const RangePack& P, long lon
   const double* src = Q->tiles + (Q->toff ? Q->toff[t] : t * (kTile * kTile));
   const unsigned bytes = Q->tbytes ? (unsigned)Q->tbytes[t] : kTileBytes;
   const int st = R.issued % R.nst;
-  mb_load(R.stage + (size_t)st * kTile * kTile, src, bytes, &R.full[st]);
+  mb_load(R.stage + (size_t)st * kTile * kTile, src, bytes, &R.full[st], R.keep != 0);
   ++R.issued;
 }
 // issue the first tiles of set `kind` for the next tile phase (thread 0).
@@ -199,21 +216,24 @@ __device__ __forceinline__ double grid_sum(double v, double* part, int slot, cg:
 // D_s R_s val for interface flat index q into the NN2 local inputs.
 __device__ __forceinline__ void write_local(const FusedPcg& A, long long q, double val) {
   const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
-  for (int e = 0; e < A.inv_cnt[gq]; ++e) {
-    const int s = A.inv_s[4 * gq + e], pp = A.inv_p[4 * gq + e];
-    const int kind = A.pkind[A.ip_off[s] + pp];
-    const double wv = A.iface_w[A.ip_off[s] + pp] * val;
-    if (kind >= 0) A.fr[A.roff[s] + (long long)j * A.nr[s] + kind] = wv;
-    else A.fc[A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)] = wv;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {  // every slot's descriptor loads at once (unused slots: x < 0)
+    const int4 d = __ldg(A.ifd + 4 * gq + e);
+    const double wv = __ldg(A.ifw + 4 * gq + e) * val;
+    if (d.x >= 0) {
+      if (d.w > 0) A.fr[d.z + (long long)j * d.w] = wv;
+      else A.fc[d.z - (long long)j * d.w] = wv;
+    }
   }
 }
 
 // R_s val into an S-local buffer for every subdomain sharing interface index q.
 __device__ __forceinline__ void write_local_s(const FusedPcg& A, double* li, long long q, double val) {
   const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
-  for (int e = 0; e < A.inv_cnt[gq]; ++e) {
-    const int s = A.inv_s[4 * gq + e];
-    li[A.s_xoff[s] + (long long)j * A.ng[s] + A.inv_p[4 * gq + e]] = val;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int4 d = __ldg(A.ifd + 4 * gq + e);
+    if (d.x >= 0) li[d.x + (long long)j * d.y] = val;
   }
 }
 
@@ -326,14 +346,40 @@ __device__ void s_tiles_phase(const FusedPcg& A, Ring& R, Smem& sm, double* xs, 
   });
 }
 
+// sum over the sharing subdomains (ascending s) of their S partials at q
 __device__ __forceinline__ double s_reduce(const FusedPcg& A, long long q) {
   const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
+  int4 d[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) d[e] = __ldg(A.sred + 4 * gq + e);
   double y = 0.0;
-  for (int e = 0; e < A.inv_cnt[gq]; ++e) {
-    const int s = A.inv_s[4 * gq + e], pp = A.inv_p[4 * gq + e];
-    y += range_reduce(A.rs, s, j * A.ng[s] + pp);
-  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (d[e].w > 0) y += partial_sum(A.rs.part + d[e].x + (long long)j * d[e].y, d[e].z, d[e].w);
   return y;
+}
+
+// z_q = sum_s w_s [Q_s f_r - Psi_s u_c ; u_c]_q (NN2 step 7), ascending s
+__device__ __forceinline__ double z_reduce(const FusedPcg& A, int j, int gq, bool coarse) {
+  int4 d[4], p[4];
+  double w[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) d[e] = __ldg(A.zred + 4 * gq + e), p[e] = __ldg(A.pred + 4 * gq + e), w[e] = __ldg(A.ifw + 4 * gq + e);
+  double zq = 0.0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    double v;
+    if (d[e].w >= 0) {
+      v = partial_sum(A.rq.part + d[e].x + (long long)j * d[e].y, d[e].z, d[e].w);
+      if (coarse) v -= partial_sum(A.rp.part + p[e].x + (long long)j * p[e].y, p[e].z, p[e].w);
+    } else if (d[e].w == -1) {
+      v = coarse ? __ldcg(A.ucl + d[e].x + (long long)j * d[e].y) : 0.0;
+    } else {
+      continue;
+    }
+    zq += w[e] * v;
+  }
+  return zq;
 }
 
 
@@ -438,21 +484,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
   double rz = 0.0;
   for (long long q = gtid; q < A.NG; q += gstride) {
     const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
-    double zq = 0.0;
-    for (int e = 0; e < A.inv_cnt[gq]; ++e) {
-      const int s = A.inv_s[4 * gq + e], pp = A.inv_p[4 * gq + e];
-      const int kind = A.pkind[A.ip_off[s] + pp];
-      const double wgt = A.iface_w[A.ip_off[s] + pp];
-      double v;
-      if (kind >= 0) {
-        const int ar = j * A.nr[s] + kind;
-        v = range_reduce(A.rq, s, ar);
-        if (coarse) v -= rect_reduce(A.rp, s, kTile * A.rp.nI[s] + ar);  // u_r = Q f_r - Psi u_c
-      } else {
-        v = coarse ? __ldcg(A.ucl + A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)) : 0.0;
-      }
-      zq += wgt * v;
-    }
+    const double zq = z_reduce(A, j, gq, coarse);  // u_r = Q f_r - Psi u_c ; u_c
     A.z[q] = zq;
     write_local_s(A, A.li_z, q, zq);
     rz += A.r[q] * zq;
@@ -468,7 +500,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   __shared__ unsigned long long ring_bar[kMaxRing];
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
   const bool leader = gtid == 0;
-  Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0};
+  Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0, A.l2_keep};
   double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;  // local input vector, then the accumulator
   double* xacc = xs + A.maxlen;
   PhaseClock pc{leader && A.tphase != nullptr, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
@@ -710,21 +742,7 @@ __device__ double ph_nn2b(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_group& 
   double rz = 0.0;
   for (long long q = gtid; q < A.NG; q += gstride) {
     const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
-    double zq = 0.0;
-    for (int e = 0; e < A.inv_cnt[gq]; ++e) {
-      const int s = A.inv_s[4 * gq + e], pp = A.inv_p[4 * gq + e];
-      const int kind = A.pkind[A.ip_off[s] + pp];
-      const double wgt = A.iface_w[A.ip_off[s] + pp];
-      double v;
-      if (kind >= 0) {
-        const int ar = j * A.nr[s] + kind;
-        v = range_reduce(A.rq, s, ar);
-        if (coarse) v -= rect_reduce(A.rp, s, kTile * A.rp.nI[s] + ar);
-      } else {
-        v = coarse ? __ldcg(A.ucl + A.coff[s] + (long long)j * A.nc[s] + (-1 - kind)) : 0.0;
-      }
-      zq += wgt * v;
-    }
+    const double zq = z_reduce(A, j, gq, coarse);
     A.z[q] = zq;
     write_local_s(A, A.li_z, q, zq);  // shared nodes are rewritten after their halo
     halo_pack_one(A.H, j, gq, zq);
@@ -739,7 +757,7 @@ __global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
   __shared__ unsigned long long ring_bar[kMaxRing];
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
   const bool leader = gtid == 0;
-  Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0};
+  Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0, A.l2_keep};
   double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;
   double* xacc = xs + A.maxlen;
   for (int i = threadIdx.x; i < A.nst * kTile * kTile; i += blockDim.x) dyn_smem[i] = 0.0;
@@ -950,6 +968,7 @@ void RangeBufs::plan(const std::vector<long long>& tile_base, const std::vector<
   }
   t_first.upload(tf), start.upload(st);
   this->c0.upload(c0), ncta.upload(nc), pbase.upload(pb);
+  h_pbase = pb, h_ncta = nc;
   part.alloc(std::max<long long>(1, pb[nmat]));
   SGW_CUDA(cudaMemset(part.p, 0, part.n * sizeof(double)));  // slots of CTAs with empty ranges stay 0
 }
@@ -1025,7 +1044,11 @@ void GpuSolver::setup_fused_pcg() {
     fused_maxlen_ = std::max({fused_maxlen_, kTile * Sp.ntile[s], kTile * (Qp.ntile[s] + cdiv(NT * nc_[s], kTile))});
   cudaFuncAttributes fa{};
   SGW_CUDA(cudaFuncGetAttributes(&fa, (const void*)pcg_fused_kernel));
-  int bps = 2;
+  // small tile sets (C1: 12 MB per iteration) are latency-bound: one CTA per
+  // SM halves the CTA partials every scatter sums and the grid-barrier cost
+  // (measured at C1: 61 vs 73 us per iteration; at C2 two CTAs per SM win,
+  // 0.54 vs 0.64 ms)
+  int bps = bytes_S() + bytes_Q() < 64e6 ? 1 : 2;
   if (const char* e = std::getenv("SGW_PCG_BPS")) bps = std::max(1, std::atoi(e));
   const long long vec = 2LL * fused_maxlen_ * 8;
   for (;; --bps) {
@@ -1043,23 +1066,28 @@ void GpuSolver::setup_fused_pcg() {
     return;
   }
   fused_smem_ = (size_t)fused_nst_ * kTileBytes + (size_t)vec;
-  SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)fused_smem_));
+  ensure_dyn_smem((const void*)pcg_fused_kernel, fused_smem_);
   SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pcg_fused_kernel, 256, fused_smem_));
   {  // the phase-split kernel walks the same CTA ranges: same grid, co-resident too
     int nb2 = 0;
-    SGW_CUDA(cudaFuncSetAttribute((const void*)pcg_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)fused_smem_));
+    ensure_dyn_smem((const void*)pcg_phase_kernel, fused_smem_);
     SGW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, pcg_phase_kernel, 256, fused_smem_));
     nb = std::min(nb, nb2);
   }
   fused_grid_ = std::max(1, std::min(nb, bps)) * sms;
-  SGW_CUDA(cudaFuncSetAttribute((const void*)walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)fused_smem_));
+  if (const char* e = std::getenv("SGW_PCG_GRID"))  // tuning hook (<= the co-resident maximum)
+    fused_grid_ = std::max(1, std::min(fused_grid_, std::atoi(e)));
+  ensure_dyn_smem((const void*)walk_kernel, fused_smem_);
   rs_.plan(Sp.tile_base, Sp.ntile, {}, fused_grid_);
   rq_.plan(Qp.tile_base, Qp.ntile, {}, fused_grid_);
   walk_ok_ = true;  // the host-driven loop streams S / Q / Psi with walk_kernel too
   build_psi_tiles();
+  build_scatter_desc();
+  {  // tiles of S, Q and Psi within ~half of L2 (C1: 12 MB): keep them resident
+    const double tile_bytes = bytes_S() + bytes_Q();
+    l2_keep_ = tile_bytes <= 48e6 ? 1 : 0;
+    if (const char* e = std::getenv("SGW_PCG_L2KEEP")) l2_keep_ = std::atoi(e) != 0;  // tuning hook
+  }
   {
     std::vector<int> ncs(NS);
     for (int s = 0; s < NS; ++s) ncs[s] = NT * nc_[s];
@@ -1078,6 +1106,43 @@ void GpuSolver::setup_fused_pcg() {
   const std::string mode = e ? e : "";
   use_fused_ = !comm_ && mode != "host" && mode != "phase";
   use_phase_ = mode != "host";
+}
+
+void GpuSolver::build_scatter_desc() {
+  const int ni = G.n_iface;
+  std::vector<int4> ifd(4 * (size_t)ni, make_int4(-1, 0, 0, 0)), sred(4 * (size_t)ni, make_int4(0, 0, 0, 0));
+  std::vector<int4> zred(4 * (size_t)ni, make_int4(0, 0, 0, -2)), pred(4 * (size_t)ni, make_int4(0, 0, 0, 0));
+  std::vector<double> ifw(4 * (size_t)ni, 0.0);
+  std::vector<int> cnt(ni, 0);
+  auto i32 = [](long long v) {
+    if (v < 0 || v >= (1LL << 31)) throw Error(1, "PCG glue descriptor out of 32-bit range");
+    return int(v);
+  };
+  for (int s = 0; s < NS; ++s) {  // ascending s: the reference's reduction order
+    const auto& sd = G.sub[s];
+    std::vector<int> kind(ng_[s], 0);
+    for (int r = 0; r < nr_[s]; ++r) kind[sd.r_local[r]] = r;
+    for (int c = 0; c < nc_[s]; ++c) kind[sd.c_local[c]] = -1 - c;
+    for (int pp = 0; pp < ng_[s]; ++pp) {
+      const int gq = sd.iface_pos[pp], e = cnt[gq]++;
+      if (e >= 4) throw Error(1, "more than four subdomains share an interface node");
+      const size_t k = 4 * (size_t)gq + e;
+      const int kd = kind[pp];
+      ifd[k] = make_int4(i32(Sp.xoff[s] + pp), ng_[s], i32(kd >= 0 ? roff_[s] + kd : coff_[s] + (-1 - kd)),
+                         kd >= 0 ? nr_[s] : -nc_[s]);
+      ifw[k] = sd.w[pp];
+      sred[k] = make_int4(i32(rs_.h_pbase[s] + pp), ng_[s], kTile * Sp.ntile[s], rs_.h_ncta[s]);
+      if (kd >= 0) {
+        zred[k] = make_int4(i32(rq_.h_pbase[s] + kd), nr_[s], kTile * Qp.ntile[s], rq_.h_ncta[s]);
+        if (!psi_nI_.empty() && !rp_.h_pbase.empty())
+          pred[k] = make_int4(i32(rp_.h_pbase[s] + (long long)kTile * psi_nI_[s] + kd), nr_[s],
+                              kTile * (psi_nI_[s] + psi_nJ_[s]), rp_.h_ncta[s]);
+      } else {
+        zred[k] = make_int4(i32(coff_[s] + (-1 - kd)), nc_[s], 0, -1);
+      }
+    }
+  }
+  d_ifd_.upload(ifd), d_ifw_.upload(ifw), d_sred_.upload(sred), d_zred_.upload(zred), d_pred_.upload(pred);
 }
 
 FusedPcg GpuSolver::fused_args(const double* b, double* x) const {
@@ -1107,6 +1172,8 @@ FusedPcg GpuSolver::fused_args(const double* b, double* x) const {
   A.own = dot_mask();
   A.xch = ph_xch_.p, A.sc = ph_sc_.p, A.st = ph_st_.p;
   A.cond = 0, A.use_cond = 0;
+  A.l2_keep = l2_keep_;
+  A.ifd = d_ifd_.p, A.ifw = d_ifw_.p, A.sred = d_sred_.p, A.zred = d_zred_.p, A.pred = d_pred_.p;
   return A;
 }
 
@@ -1217,7 +1284,7 @@ bool GpuSolver::build_phase_graphs(const double* b, double* x) {
 int GpuSolver::pcg_phase(const double* b, double* x, bool* converged, std::vector<double>* hist) {
   cudaEventRecord(ev_[0], st_);
   if (!h_st_) SGW_CUDA(cudaMallocHost(&h_st_, 8 * sizeof(int)));
-  const bool graphs = (!comm_ || comm_->capturable()) && ph_graph_ok_;
+  const bool graphs = (!comm_ || comm_->capturable()) && ph_graph_ok_ && !std::getenv("SGW_PHASE_NOGRAPH");
   if (graphs && (ph_graph_b_ != b || ph_graph_x_ != x || !ph_graph_[0]))
     ph_graph_ok_ = build_phase_graphs(b, x);
   const bool use_graphs = graphs && ph_graph_ok_;

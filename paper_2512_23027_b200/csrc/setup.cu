@@ -219,6 +219,8 @@ double diag_trace_host(const double* dA, int n, int lda, cudaStream_t st) {
   return tr;
 }
 
+}  // namespace
+
 // llt_regularized (src/dd.cpp:66-76) followed by the inverse: A <- A^-1 (full).
 void spd_inverse(cusolverDnHandle_t sol, cudaStream_t st, double* A, int n, DBuf<double>& work, DBuf<int>& info,
                  const char* what) {
@@ -247,6 +249,7 @@ void spd_inverse(cusolverDnHandle_t sol, cudaStream_t st, double* A, int n, DBuf
   symmetrize_lower_kernel<<<cdiv((long long)n * n, 256), 256, 0, st>>>(A, n);
   SGW_LAUNCHED();
 }
+namespace {
 }  // namespace
 
 // ------------------------------------------------------------------ maps ---
@@ -362,6 +365,7 @@ void GpuSolver::build_maps() {
 // ---------------------------------------------------------- constructor ----
 GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), comm_(std::move(comm)) {
   const auto t0 = std::chrono::steady_clock::now();
+  const long long bytes0 = DevBytes::total.load();
   if ((int)P.coeff.size() != P.n_in * P.n_nodes() || P.n_in != P.tensor.n_in)
     throw Error(1, "SgSolver: coefficient terms do not match tensor input size");
   if (P.tensor.n_out < 1) throw Error(1, "SgSolver: tensor has no output terms");
@@ -430,6 +434,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   setup_fused_pcg();
   build_coupling_blocks();  // A_GI / A_IG and interface-row force blocks, memory permitting
   SGW_CUDA(cudaStreamSynchronize(st_));
+  setup_bytes_ = DevBytes::total.load() - bytes0;
   setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 

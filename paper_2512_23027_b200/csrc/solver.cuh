@@ -53,6 +53,11 @@ bool sgop_pack_stencils(const SgOpJit& J, const double* Kg, const double* Mg, in
                         std::vector<double>& kt, SgOpArgs& a);
 long long sgop_scratch_doubles(const SgOpJit& J, int W, int H);
 
+// device bytes held by every DBuf of the process (all element types)
+struct DevBytes {
+  static inline std::atomic<long long> total{0};
+};
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -70,7 +75,7 @@ struct DBuf {
         p = nullptr;
         throw Error(6, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
       }
-      g_bytes += count * sizeof(T);
+      DevBytes::total += count * sizeof(T);
     }
   }
   void upload(const std::vector<T>& h) {
@@ -83,15 +88,19 @@ struct DBuf {
   void reset() {
     if (p) {
       cudaFree(p);
-      g_bytes -= n * sizeof(T);
+      DevBytes::total -= n * sizeof(T);
     }
     p = nullptr;
     n = 0;
   }
-  static inline std::atomic<long long> g_bytes{0};
 };
 
 // Batch of symmetric matrices stored as lower 64x64 tiles.
+// llt_regularized (src/dd.cpp:66-76) + explicit inverse of an SPD n x n
+// column-major device matrix, in place (setup.cu)
+void spd_inverse(cusolverDnHandle_t sol, cudaStream_t st, double* A, int n, DBuf<double>& work, DBuf<int>& info,
+                 const char* what);
+
 struct TilePack {
   int nmat = 0;
   std::vector<int> dim, ntile;       // per matrix: dimension, tiles per side
@@ -114,6 +123,8 @@ struct RangeBufs {
   DBuf<int4> start;
   DBuf<int> c0, ncta;
   DBuf<double> part;
+  std::vector<long long> h_pbase;  // host copies (scatter descriptors)
+  std::vector<int> h_ncta;
   void plan(const std::vector<long long>& tile_base, const std::vector<int>& nI, const std::vector<int>& nJ, int grid);
 };
 
@@ -235,7 +246,11 @@ class GpuSolver {
   double setup_s = 0;
   Timers T;
   KProf KP;
-  long long device_bytes() const { return DBuf<double>::g_bytes.load(); }
+  // device memory this solver allocated during setup (the process-wide count
+  // grew by this much while the constructor ran; concurrent constructions
+  // in one process blur it)
+  long long device_bytes() const { return setup_bytes_; }
+  long long setup_bytes_ = 0;
   // algorithmic bytes: unique symmetric entries of all S_s / Q_s
   double bytes_S() const;
   double bytes_Q() const;
@@ -389,6 +404,13 @@ class GpuSolver {
  private:
   int fused_grid_ = 0;
   bool use_fused_ = true;
+  int l2_keep_ = 0;  // persistent PCG: tile loads keep L2 residency (small tile sets)
+  // per (interface node, sharing-subdomain slot e < 4) descriptors of the PCG
+  // glue (local-input writes and partial reductions), so that a node's slots
+  // load in parallel instead of through chains of index lookups
+  DBuf<int4> d_ifd_, d_sred_, d_zred_, d_pred_;
+  DBuf<double> d_ifw_;
+  void build_scatter_desc();
   // work vectors
   DBuf<double> li_x, li_y, r_x, r_t, c_f, c_d, dcoarse, ucoarse;
   DBuf<double> vb, vx, vr, vz, vp, vq, vrt;

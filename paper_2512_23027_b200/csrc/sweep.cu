@@ -691,12 +691,14 @@ void GpuSolver::build_sweep_layout() {
     sweep_layout_ = new SweepLayout(L);
     sweep_lo_off_ = lo_off, sweep_up_off_ = up_off, sweep_nch_ = nch, sweep_cs_ = 1;
     Fcomp.alloc(size_t(NS) * L.per_sub);
-    SGW_CUDA(cudaFuncSetAttribute((const void*)sweep_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(3 * (size_t)VL * 8)));
+    ensure_dyn_smem((const void*)sweep_generic_kernel, 3 * (size_t)VL * 8);
     return;
   }
   // cluster size: about one wave of CTAs over the 148 SMs
   int CS = NS >= 100 ? 1 : NS >= 48 ? 2 : NS >= 24 ? 4 : NS >= 12 ? 8 : 16;
+  // small blocks (C1: B = 90, two tile rows) gain nothing from more CTAs than
+  // about half their tile rows, and every rank adds cluster traffic per phase
+  while (CS > 1 && CS > nb / 2) CS /= 2;
   if (const char* e = std::getenv("SGW_SWEEP_CS")) {  // test hook: force a cluster size
     const int v = std::atoi(e);
     if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) CS = v;
@@ -741,7 +743,7 @@ void GpuSolver::build_sweep_layout() {
     attr[0].val.clusterDim.x = 16, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr, cfg.numAttrs = 1;
     if (smem > (size_t)kSmemMax || cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        (ensure_dyn_smem(fn, smem), false) ||
         cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg) != cudaSuccess || nclus < NS) {
       (void)cudaGetLastError();
       CS = 8;
@@ -830,7 +832,7 @@ void GpuSolver::build_sweep_layout() {
   Fcomp.alloc(size_t(NS) * L.per_sub);
   const size_t smem = sweep_smem_bytes();
   const void* fn = (const void*)sweep_fn(CS, nbm);
-  SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem(fn, smem);
   if (CS == 16) SGW_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 

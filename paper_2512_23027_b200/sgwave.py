@@ -111,6 +111,7 @@ def load_library():
     L.sgw_shard_plan.argtypes = [ip, ip, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp]
     L.sgw_local_group_new.argtypes = [ip, C.POINTER(vp)]
     L.sgw_local_group_free.argtypes = [vp]
+    L.sgw_local_group_abort.argtypes = [vp]
     L.sgw_create_solo.argtypes = [C.POINTER(_Problem), ip, ip, C.POINTER(vp)]
     L.sgw_create_local_group.argtypes = [C.POINTER(_Problem), ip, ip, vp, C.POINTER(vp)]
     _LIB = L
@@ -644,6 +645,7 @@ class LocalGroup:
                 out[r] = fn(r)
             except BaseException as e:  # noqa: BLE001 - re-raised below
                 err.append(e)
+                load_library().sgw_local_group_abort(self._g)  # the other ranks' collectives fail instead of hanging
         th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.world_size)]
         for t in th:
             t.start()

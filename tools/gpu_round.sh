@@ -3,6 +3,7 @@
 # region and --set full captures of the sweep and persistent PCG kernels.
 set -u
 mkdir -p gpurun_out
+rm -f gpurun_out/prof_*.ncu-rep  # stale captures must not feed summarize_ncu
 timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err
@@ -12,14 +13,14 @@ timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "launch list rc=$?" >> gpurun_out/plain.log
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
+timeout 900 ncu --set full -f --clock-control none --import-source on --profile-from-start off \
     -k regex:sweep_kernel -c 2 -o gpurun_out/prof_sweep $CMD > gpurun_out/ncu_sweep.log 2>&1
 echo "sweep rc=$?" >> gpurun_out/plain.log
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
+timeout 900 ncu --set full -f --clock-control none --import-source on --profile-from-start off \
     -k regex:pcg_fused -c 1 -o gpurun_out/prof_pcg $CMD > gpurun_out/ncu_pcg.log 2>&1
 echo "rc=$?" >> gpurun_out/plain.log
 timeout 600 python tools/sgop_bench.py C2 5 > gpurun_out/sgop_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgop_kernel -s 2 -c 1 \
+timeout 900 ncu --set full -f --clock-control none --import-source on -k regex:sgop_kernel -s 2 -c 1 \
     -o gpurun_out/prof_sgop python tools/sgop_bench.py C2 5 > gpurun_out/ncu_sgop.log 2>&1
 echo "rc=$?" >> gpurun_out/plain.log
 timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3.log 2> gpurun_out/bench_C3.err
