@@ -354,6 +354,11 @@ def main():
                                    "frac": b_iter / (iter_ms / 1e3) / 1e9 / peak},
         "kernels": kernels,
         "pcg_phases_ms_per_iteration": {k: v / max(iters, 1) for k, v in kp["pcg_phases_ms"].items()},
+        # per Newmark step (CUDA events of the step): RHS (predictors, local force,
+        # first interior sweep, g assembly), interface PCG, recovery (second
+        # sweep) + update
+        "step_breakdown_ms": {"rhs": st["rhs_ms"] / args.steps, "pcg": st["pcg_ms"] / args.steps,
+                              "recovery_update": st["rec_ms"] / args.steps},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

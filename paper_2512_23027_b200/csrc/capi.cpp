@@ -65,6 +65,7 @@ void set_force(GpuSolver& g, const sgw_force* f, int rows) {
 // global interface vectors in and out (every rank passes and gets the whole vector)
 template <typename F>
 void iface_op(GpuSolver& g, const double* x, double* y, F&& op) {
+  if (g.NGG == 0) return;  // one subdomain: the interface system is empty
   DBuf<double> gx, lx, ly, gy;
   h2d(gx, x, g.NGG, g.stream());
   lx.alloc(g.NG), ly.alloc(g.NG), gy.alloc(g.NGG);

@@ -1024,8 +1024,9 @@ void GpuSolver::build_psi_tiles() {
 
 void GpuSolver::setup_fused_pcg() {
   tphase_.alloc(8), tphase_.zero(st_);
-  if (P.implicit_schur) {  // reduced-memory: the host-driven loop without S tiles
+  if (P.implicit_schur || direct_) {  // reduced-memory: the host-driven loop without S tiles; direct: no PCG
     use_fused_ = false;
+    if (direct_) use_phase_ = walk_ok_ = false;
     return;
   }
   int dev = 0, sms = 0, nb = 0, smem_sm = 0, smem_blk = 0;

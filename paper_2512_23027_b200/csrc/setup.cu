@@ -372,7 +372,11 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   if (!(P.dt > 0.0)) throw Error(1, "SgSolver: dt must be positive");
   if (comm_ && (comm_->rank() != P.rank || comm_->size() != P.world)) throw Error(1, "communicator / rank mismatch");
   G = build_geometry(P.nx, P.ny, P.px, P.py, P.rank, P.world);
-  if (G.ns_total < 2 || G.n_iface == 0) throw Error(1, "GPU path needs an interface (more than one subdomain)");
+  // one subdomain (sg.cpp:146 direct_): no interface; the step's interior
+  // solve is then the whole (P+1) n system (the reference's direct_llt_,
+  // sg.cpp:158-172, :301-305) and the interface PCG is empty (0 iterations)
+  if (G.ns_total >= 2 && G.n_iface == 0) throw Error(1, "partition without an interface");
+  direct_ = G.n_iface_global == 0;
   if (G.W < 1 || G.H < 1) throw Error(1, "GPU path needs interior dofs in every subdomain (mx, my >= 2)");
   NT = P.tensor.n_out;
   NIN = P.n_in;
@@ -403,7 +407,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   B = G.W * NT;
   amax_ = 0;
   for (int s = 0; s < NS; ++s) amax_ = std::max(amax_, NT * ng_[s]);
-  plan_nn2();
+  if (!direct_) plan_nn2();
   build_sweep_layout();
   {
     const double per = 8.0 * (3.0 * G.H * double(B) * B + double(amax_) * amax_ + 2.0 * double(B) * amax_);
@@ -413,9 +417,9 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
     for (int b0 = 0; b0 < NS; b0 += nb) {
       const int cnt = std::min(nb, NS - b0);
       setup_interior_and_schur(b0, cnt);
-      nn2_batch(b0, cnt, fcc);
+      if (!direct_) nn2_batch(b0, cnt, fcc);
     }
-    finish_nn2(fcc);
+    if (!direct_) finish_nn2(fcc);
   }
 
   // work vectors (the step kernels use 32-bit index arithmetic)
@@ -588,6 +592,8 @@ void GpuSolver::setup_interior_and_schur(int b0, int nb) {
           throw Error(2, "stochastic interior factorization failed (subdomain " + std::to_string(G.sub_gid[b0 + q]) + ")");
   }
   // S_s = A_GG - Y^T Y, Y = L^-1 A_IG by rolling block forward substitution
+  // (one subdomain, no interface: amax = 0, nothing to eliminate)
+  if (amax > 0) {
   Sdense_.alloc(size_t(ns) * amax * amax);
   Sdense_.zero(st_);
   assemble_gg_kernel<<<dim3(cdiv(amax, 128), ns), 128, 0, st_>>>(A, ip_off.p + b0, iface_lid_.p, Sdense_.p, amax, ns);
@@ -618,6 +624,7 @@ void GpuSolver::setup_interior_and_schur(int b0, int nb) {
   }
   R.reset();
   Y.reset();
+  }
   // Linv_kk = L_kk^-1 (exact zeros above the diagonal) for the per-step sweeps
   for (int k = 0; k < H; ++k)
     SGW_BLAS(cublasDtrsmBatched(blas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, B, B,

@@ -727,6 +727,28 @@ int GpuSolver::step(int* iters_out) {
   }
   SGW_LAUNCHED();
   sweep(yI.p);  // y = A_II^-1 f_I
+  if (direct_) {
+    // one subdomain (sg.cpp:301-305): y is the whole solution, no interface solve
+    SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
+    cudaEventRecord(ev_[3], st_);
+    cudaEventRecord(ev_[4], st_);
+    update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
+                                         P.ny, G.px, G.py, G.H, B, gid_local_d_.p, P.dt, P.zeta, P.gamma, nullptr);
+    SGW_LAUNCHED();
+    record_probes(step_index + 1, nullptr);
+    cudaEventRecord(ev_[5], st_);
+    SGW_CUDA(cudaEventSynchronize(ev_[5]));
+    t_now = t_now + P.dt;
+    ++step_index;
+    KP.collect();
+    float ms_rhs = 0, ms_all = 0;
+    cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);
+    cudaEventElapsedTime(&ms_all, ev_[2], ev_[5]);
+    T.rhs_ms += ms_rhs, T.step_ms += ms_all;
+    ++T.steps;
+    if (iters_out) *iters_out = 0;
+    return 0;
+  }
   if (cpl_blk_.p)
     coupling_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
         A, 0, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_iptr_.p, cpl_iedge_.p, ilist_.p, n_ilist_, yI.p, fG.p,

@@ -505,3 +505,18 @@ def test_step_without_coupling_blocks_matches_oracle(gpu, monkeypatch):
     hc = c.run(z, z, 6, force_node=node, store_full=True)
     assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
+@pytest.mark.parametrize("nx,L,pin,pout", [(12, 2, 2, 2), (17, 2, 4, 2)])
+def test_single_subdomain_direct_path(gpu, nx, L, pin, pout):
+    # sg.cpp:146 / :158-172 / :301-305: one subdomain, no interface: each step
+    # solves the whole stochastic transient system directly (the GPU's
+    # interior block-Thomas solve over all dofs), 0 PCG iterations
+    g, c = pair(nx, 1, 1, 0.3, 0.5, L, pin, pout, 1e-3)
+    assert g.n_global == 0
+    u0 = O.gaussian_pulse(nx, nx)
+    z = np.zeros((nx + 1) ** 2)
+    hg = g.run(u0, z, 5, sg.ForceSpec(node=O.nearest_node(nx, nx, 0.5, 0.5)))
+    hc = c.run(u0, z, 5, force_node=O.nearest_node(nx, nx, 0.5, 0.5), store_full=True)
+    assert np.all(hg.iterations == 0) and np.all(hc["iterations"] == 0)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10

@@ -4,8 +4,7 @@
 set -u
 mkdir -p gpurun_out
 rm -f gpurun_out/prof_*.ncu-rep  # stale captures must not feed summarize_ncu
-timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+# (the GPU test suite runs in its own call: tools/r02_suite.sh, ~50 min with the full-size parity tests)
 timeout 900 python bench.py > gpurun_out/bench_full.log 2> gpurun_out/bench_full.err
 echo "bench rc=$?" >> gpurun_out/bench_full.err
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
@@ -29,3 +28,12 @@ timeout 600 python bench.py --config C1 > gpurun_out/bench_C1.log 2> gpurun_out/
 echo "C1 rc=$?" >> gpurun_out/bench_C1.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err
 echo "ref rc=$?" >> gpurun_out/bench_ref.err
+timeout 900 python bench.py --config C5L8 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C5L8.log 2> gpurun_out/bench_C5L8.err
+echo "C5L8 rc=$?" >> gpurun_out/bench_C5L8.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --force-shard > gpurun_out/bench_C2_shard1.log 2> gpurun_out/bench_C2_shard1.err
+echo "shard1 rc=$?" >> gpurun_out/bench_C2_shard1.err
+for W in 8 4; do
+  timeout 900 python bench.py --config C4 --solo-rank 0 --solo-world $W --steps 20 > gpurun_out/solo_C4_w$W.log 2>&1
+  echo "rc=$?" >> gpurun_out/solo_C4_w$W.log
+done
