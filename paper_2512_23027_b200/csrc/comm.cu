@@ -43,7 +43,7 @@ class NcclComm final : public Comm {
   int size() const override { return world_; }
   bool capturable() const override { return true; }
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
-    if (n == 0) return;
+    if (n == 0 || world_ == 1) return;  // a sum over one rank is the identity
     SGW_NCCL(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, comm_, st));
   }
   void exchange(const std::vector<int>& peers, const std::vector<size_t>& off, const std::vector<size_t>& cnt,

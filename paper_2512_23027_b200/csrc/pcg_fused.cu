@@ -21,6 +21,7 @@
 // true-residual confirmation and the restart from the true residual are
 // evaluated on device exactly as src/pcg.cpp:30-40.
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include <algorithm>
 #include <cstdlib>
@@ -67,6 +68,7 @@ struct FusedPcg {
   unsigned long long cond;       // conditional handle of the graph's WHILE loop
   int use_cond;
   int l2_keep;                   // tile loads with the default L2 policy (the tile set fits in L2)
+  int ph_prefetch;               // phase-split kernels: L2 prefetch of the next walk's first tiles
   // glue descriptors per (interface node gq, slot e): 4 * gq + e (build_scatter_desc)
   const int4* ifd;   // {S-local base (-1: unused slot), S-local term stride, fr / fc base, fr stride (> 0) or -(fc stride)}
   const double* ifw; // partition-of-unity weight of the slot
@@ -171,6 +173,17 @@ __device__ __forceinline__ void ring_issue(Ring& R, const RangePack& P, long lon
   mb_load(R.stage + (size_t)st * kTile * kTile, src, bytes, &R.full[st], R.keep != 0);
   ++R.issued;
 }
+// the first n tiles of this CTA's range of P into L2 (thread 0)
+__device__ __forceinline__ void l2_prefetch_range(const RangePack& P, int n) {
+  if (threadIdx.x != 0) return;
+  const long long t0 = P.t_first[blockIdx.x], t1 = P.t_first[blockIdx.x + 1];
+  for (long long t = t0; t < t1 && t < t0 + n; ++t) {
+    const double* src = P.tiles + (P.toff ? P.toff[t] : t * (kTile * kTile));
+    const unsigned bytes = P.tbytes ? (unsigned)P.tbytes[t] : kTileBytes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+  }
+}
+
 // issue the first tiles of set `kind` for the next tile phase (thread 0).
 // The ring always holds the next nst tiles of the consumption sequence: a
 // walk of P chained to `next` consumes P's range, then next's; a walk without
@@ -645,19 +658,23 @@ __global__ void __launch_bounds__(256) walk_kernel(RangePack P, const double* __
 }
 
 // ------------------------------------------------- phase-split PCG -------
-// The persistent kernel's iteration cut at its three cross-rank sums, for
-// sharded runs.  One iteration = three cooperative launches with
-// the exchanges between them (captured with them in one CUDA graph whose
-// WHILE conditional node keeps the convergence test on the device):
+// The persistent kernel's iteration cut at its cross-rank sums, for sharded
+// runs.  One iteration = four cooperative launches with the
+// exchanges between them (captured with them in one CUDA graph whose WHILE
+// conditional node keeps the convergence test on the device):
 //   A  combine z's shared nodes; beta; q_partial = sum_{s owned} R_s^T S_s R_s p
 //      (tile walk + scatter), p.q partial, pack q      -> halo(q), allreduce(p.q)
-//   B  combine q; alpha; p, x, r updates; r.r partial (owned nodes); NN2 up to
-//      the coarse partial d                            -> allreduce(d, r.r)
-//   C  convergence test (loop condition); u_c = F_cc^-1 d; Psi u_c; z partial,
-//      r.z partial, pack z                             -> halo(z), allreduce(r.z)
+//   B  combine q; alpha; p, x, r updates; r.r partial (owned nodes)
+//                                                      -> allreduce(r.r)
+//   B2 convergence test (loop condition); unless it ends the loop, NN2 up to
+//      the coarse partial d                            -> allreduce(d)
+//   C  u_c = F_cc^-1 d; Psi u_c; z partial, r.z partial, pack z
+//                                                      -> halo(z), allreduce(r.z)
+// The test precedes NN2 as in src/pcg.cpp:30-44: the converged iteration
+// streams no Q / Psi tiles (a fused B + B2 did, one wasted NN2 per solve).
 // p.q and r.z are sums of per-subdomain dots (p.q = sum_s (R_s p).(S_s R_s p),
 // r.z = sum_s (R_s r).(D_s zeta_s)), so their partials need no halo.
-enum { PH_INIT = 0, PH_C0, PH_A, PH_B, PH_C, PH_T1, PH_T2, PH_R, PH_RC0 };
+enum { PH_INIT = 0, PH_C0, PH_A, PH_B, PH_C, PH_T1, PH_T2, PH_R, PH_RC0, PH_B2 };
 
 __device__ __forceinline__ bool owned(const FusedPcg& A, long long q) { return !A.own || A.own[q] != 0.0; }
 
@@ -760,8 +777,14 @@ __global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
   Ring R{dyn_smem, ring_bar, A.nst, 0, 0, 0, A.l2_keep};
   double* xs = dyn_smem + (size_t)A.nst * kTile * kTile;
   double* xacc = xs + A.maxlen;
-  for (int i = threadIdx.x; i < A.nst * kTile * kTile; i += blockDim.x) dyn_smem[i] = 0.0;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  // only the phases that walk Psi's narrow tiles need zeroed stages (rows past
+  // a narrow chunk must hold finite values); PH_B walks no tiles at all
+  const bool walks_psi = which == PH_INIT || which == PH_C0 || which == PH_B2 || which == PH_C || which == PH_R ||
+                         which == PH_RC0;
+  if (walks_psi) {
+    for (int i = threadIdx.x; i < A.nst * kTile * kTile; i += blockDim.x) dyn_smem[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < A.nst; ++i) mb_init(&ring_bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -851,10 +874,9 @@ __global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
       }
       const double rr = grid_sum(acc, A.part, 2, g, sm);
       if (leader) A.xch[NC] = rr;
-      ph_nn2a(A, R, sm, g, xs, xacc);
       break;
     }
-    case PH_C: {  // convergence test (the loop condition), then the rest of NN2
+    case PH_B2: {  // convergence test (the loop condition; r.r summed over ranks), then NN2 up to d
       const int it = A.st[ST_IT] + 1, hl = A.st[ST_HL];
       const double rel = sqrt(__ldcg(A.xch + NC)) / A.sc[SC_BNORM];
       const int ex = rel <= A.tol ? EX_CHECK : (it >= A.max_iter ? EX_MAXIT : EX_RUN);
@@ -868,7 +890,12 @@ __global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
         A.st[ST_EXIT] = ex;
         if (ex != EX_RUN && A.use_cond) cudaGraphSetConditional(A.cond, 0);
       }
-      if (ex != EX_RUN) break;
+      if (ex != EX_RUN) break;  // converged / max_iter: no NN2 for this residual (src/pcg.cpp:30-44)
+      ph_nn2a(A, R, sm, g, xs, xacc);
+      break;
+    }
+    case PH_C: {  // the rest of NN2 (skipped once the test in PH_B2 ended the loop)
+      if (A.st[ST_EXIT] != EX_RUN) break;
       const double rz = ph_nn2b(A, R, sm, g, xs, xacc);
       if (leader) A.xch[NC + 2] = rz;
       break;
@@ -918,6 +945,13 @@ __global__ void __launch_bounds__(256) pcg_phase_kernel(FusedPcg A, int which) {
   }
   if (threadIdx.x == 0)
     for (int c = R.consumed; c < R.issued; ++c) mb_wait(&R.full[c % R.nst], (c / R.nst) & 1);
+  // the next walk's first tiles into L2 (a kernel boundary empties the ring;
+  // the persistent kernel issues them across its grid barriers instead)
+  if (A.ph_prefetch) {
+    if (which == PH_A) l2_prefetch_range(A.rq, A.nst);                 // PH_B2: Q walk
+    if (which == PH_B2 && NC > 0) l2_prefetch_range(A.rp, A.nst);      // PH_C: Psi walk
+    if (which == PH_C || which == PH_RC0 || which == PH_C0) l2_prefetch_range(A.rs, A.nst);  // PH_A: S walk
+  }
   __syncthreads();
 }
 
@@ -1174,6 +1208,8 @@ FusedPcg GpuSolver::fused_args(const double* b, double* x) const {
   A.xch = ph_xch_.p, A.sc = ph_sc_.p, A.st = ph_st_.p;
   A.cond = 0, A.use_cond = 0;
   A.l2_keep = l2_keep_;
+  A.ph_prefetch = 0;  // measured: 0.565 vs 0.560 ms per C2 iteration with it (the prefetches compete)
+  if (const char* e = std::getenv("SGW_PHASE_PREFETCH")) A.ph_prefetch = std::atoi(e);  // tuning hook
   A.ifd = d_ifd_.p, A.ifw = d_ifw_.p, A.sred = d_sred_.p, A.zred = d_zred_.p, A.pred = d_pred_.p;
   return A;
 }
@@ -1183,11 +1219,27 @@ FusedPcg GpuSolver::fused_args(const double* b, double* x) const {
 // [0, NC) d, NC r.r | b.b, NC+1 p.q, NC+2 r.z, NC+3 rt.rt.
 void GpuSolver::phase_seq(int which, const FusedPcg& A0) {
   FusedPcg A = A0;
+  static const bool timing = std::getenv("SGW_PHASE_TIMING") != nullptr;  // diagnostics: per-phase event timing
+  static cudaEvent_t te[2];
+  static double tsum[16];
+  static int tcnt[16];
+  if (timing && !te[0]) cudaEventCreate(&te[0]), cudaEventCreate(&te[1]);
   auto K = [&](int ph) {
     void* args[] = {&A, &ph};
+    if (timing) cudaEventRecord(te[0], st_);
     SGW_CUDA(cudaLaunchCooperativeKernel((const void*)pcg_phase_kernel, dim3(fused_grid_), dim3(256), args,
                                          fused_smem_, st_));
     SGW_LAUNCHED();
+    if (timing) {
+      cudaEventRecord(te[1], st_);
+      cudaEventSynchronize(te[1]);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, te[0], te[1]);
+      tsum[ph] += ms, ++tcnt[ph];
+      if (tcnt[PH_A] % 40 == 0 && ph == PH_C)
+        for (int k = 0; k < 10; ++k)
+          if (tcnt[k]) std::fprintf(stderr, "phase %d: %d launches, %.1f us avg\n", k, tcnt[k], 1e3 * tsum[k] / tcnt[k]);
+    }
   };
   auto AR = [&](int off, int cnt) {
     if (comm_) comm_->allreduce_sum(ph_xch_.p + off, cnt, st_);
@@ -1200,7 +1252,7 @@ void GpuSolver::phase_seq(int which, const FusedPcg& A0) {
       K(PH_INIT), AR(0, NC + 1), K(PH_C0), XH(), AR(NC + 2, 1);
       break;
     case 1:  // one iteration
-      K(PH_A), XH(), AR(NC + 1, 1), K(PH_B), AR(0, NC + 1), K(PH_C), XH(), AR(NC + 2, 1);
+      K(PH_A), XH(), AR(NC + 1, 1), K(PH_B), AR(NC, 1), K(PH_B2), AR(0, NC), K(PH_C), XH(), AR(NC + 2, 1);
       break;
     case 2:  // true residual and its verdict
       K(PH_T1), XH(), K(PH_T2), AR(NC + 3, 1);
