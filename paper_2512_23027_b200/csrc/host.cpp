@@ -45,6 +45,10 @@ Geometry build_geometry(int nx, int ny, int px, int py, int rank, int world) {
   Geometry g;
   g.nx = nx, g.ny = ny, g.px = px, g.py = py;
   g.mx = (nx + px - 1) / px, g.my = (ny + py - 1) / py;  // widest block (partition.cpp:70-76)
+  // blocks of one cell (no interior dofs, test_dd.cpp:98-107) live in a frame
+  // of at least 2 x 2 cells: its interior slot is then a unit row, like the
+  // padding slots of a ragged block, and S_s = K~_GG
+  g.mx = std::max(g.mx, 2), g.my = std::max(g.my, 2);
   g.n = (nx - 1) * (ny - 1);
   g.ns_total = px * py;
   if (world < 1 || rank < 0 || rank >= world) throw Error(1, "bad rank / world_size");

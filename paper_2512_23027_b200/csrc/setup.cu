@@ -377,7 +377,6 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   // sg.cpp:158-172, :301-305) and the interface PCG is empty (0 iterations)
   if (G.ns_total >= 2 && G.n_iface == 0) throw Error(1, "partition without an interface");
   direct_ = G.n_iface_global == 0;
-  if (G.W < 1 || G.H < 1) throw Error(1, "GPU path needs interior dofs in every subdomain (mx, my >= 2)");
   NT = P.tensor.n_out;
   NIN = P.n_in;
   NS = G.ns;

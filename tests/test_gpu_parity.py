@@ -520,3 +520,19 @@ def test_single_subdomain_direct_path(gpu, nx, L, pin, pout):
     hc = c.run(u0, z, 5, force_node=O.nearest_node(nx, nx, 0.5, 0.5), store_full=True)
     assert np.all(hg.iterations == 0) and np.all(hc["iterations"] == 0)
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg", [(8, 8, 4), (7, 4, 7)])
+def test_one_cell_subdomains_sg_trajectory(gpu, cfg):
+    # SG system (P+1 = 6) on partitions with one-cell blocks (no interior
+    # dofs, test_dd.cpp:98-107): S_s = K~_GG, blocks mixed with two-cell ones
+    nx, px, py = cfg
+    g, c = pair(nx, px, py, 0.3, 0.5, 2, 4, 2, 1e-2)
+    x = rand(g.n_global, 5)
+    assert relerr(g.schur().matvec(x), c.schur_matvec(x)) <= 1e-11
+    assert relerr(g.schur().apply_nn2(x), c.apply_nn2(x)) <= 1e-10
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 4)
+    hc = c.run(u0, 0 * u0, 4, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10

@@ -105,3 +105,30 @@ def test_stochastic_solver_with_nn1_matches_oracle(gpu):
     hc = c.run(z, z, 6, force_node=node, store_full=True)
     assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
     assert np.linalg.norm(hg.full_state - hc["full"]) <= 1e-8 * np.linalg.norm(hc["full"])
+
+
+def test_subdomain_without_interior_dofs_keeps_schur_equal_to_k_gg(gpu):
+    # test_dd.cpp:98-107: one cell per subdomain, the only free node is the
+    # shared centre, so S = K~_GG (the oracle's dense restatement)
+    g, c = det_pair(2, 2, 2, 0.1, "nn2", alpha0=0.0, alpha1=0.0)
+    assert c.n_global == 1
+    one = np.ones(1)
+    assert relerr(g.schur().matvec(one), c.schur_matvec(one)) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("cfg", [(4, 4, 4), (6, 6, 2), (5, 4, 3)])
+def test_one_cell_subdomains_match_oracle(gpu, kind, cfg):
+    # blocks one cell wide (all of them, one direction only, or mixed with
+    # two-cell blocks by the floor-division split): Schur, preconditioner and
+    # a short trajectory against the oracle
+    nx, px, py = cfg
+    g, c = det_pair(nx, px, py, 0.05, kind, alpha0=0.2, alpha1=0.01)
+    r = rand(c.n_global, 3)
+    assert relerr(g.schur().matvec(r), c.schur_matvec(r)) <= 1e-11
+    assert relerr(g.schur().apply_precond(kind, r), c.apply_precond(kind, r)) <= 1e-10
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 3)
+    hc = c.run(u0, 0 * u0, 3, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_u - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-9
