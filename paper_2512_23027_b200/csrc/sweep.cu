@@ -134,50 +134,91 @@ __device__ __forceinline__ void seg_info(int seg, int H, int& type, int& k, bool
   }
 }
 
-// Row products of a swizzled tile (row stride W): lane accumulates rows lane
-// and lane + 32 against v_J (broadcast), four chains per row.  Rows >= h of the
-// stage hold stale (finite) data: they only reach padding rows of the output.
-template <int W>
-__device__ __forceinline__ void tile_rows(const double* __restrict__ buf, const double* __restrict__ vj, int lane,
-                                          int wp, double (&ra)[4], double (&rb)[4]) {
-  const int sw = 2 * (lane & 7);
-  const int ws = W > 0 ? W : wp;
-  const double* pa = buf + lane * ws;
-  const double* pb = pa + 32 * ws;
-#pragma unroll(W > 0 ? 16 : 4)
-  for (int c = 0; c < ws; c += 4) {
-    const double2 v0 = *reinterpret_cast<const double2*>(vj + c);
-    const double2 v1 = *reinterpret_cast<const double2*>(vj + c + 2);
-    const int o0 = (c & ~15) | ((c & 15) ^ sw), o1 = ((c + 2) & ~15) | (((c + 2) & 15) ^ sw);
-    const double2 a0 = *reinterpret_cast<const double2*>(pa + o0);
-    const double2 a1 = *reinterpret_cast<const double2*>(pa + o1);
-    const double2 b0 = *reinterpret_cast<const double2*>(pb + o0);
-    const double2 b1 = *reinterpret_cast<const double2*>(pb + o1);
-    ra[0] = fma(a0.x, v0.x, ra[0]);
-    ra[1] = fma(a0.y, v0.y, ra[1]);
-    ra[2] = fma(a1.x, v1.x, ra[2]);
-    ra[3] = fma(a1.y, v1.y, ra[3]);
-    rb[0] = fma(b0.x, v0.x, rb[0]);
-    rb[1] = fma(b0.y, v0.y, rb[1]);
-    rb[2] = fma(b1.x, v1.x, rb[2]);
-    rb[3] = fma(b1.y, v1.y, rb[3]);
+// Swizzle of the stored tiles: element (r, c) of a tile of row stride wp sits at
+// r wp + (c ^ 8 ((r >> 3) & 1)).  wp is a multiple of 16, so the XOR stays in
+// the row.
+__host__ __device__ __forceinline__ int sw_col(int r, int c) { return c ^ (((r >> 3) & 1) << 3); }
+
+// One pass over a tile in shared memory gives both products.  Lane
+// (rg = lane >> 2, cg = lane & 3) reads rows 8 rg + a (a < 8) and the 16-byte
+// column chunks cg + 4 b (b < 8): every element is loaded once (a quarter
+// warp covers two rows x four chunks, which the swizzle puts in distinct bank
+// groups) and feeds the row partial rp[a] (against v_J) and, with COLS, the
+// column partials cp[2 b], cp[2 b + 1] (against v_I).  Reading each tile twice
+// (a row pass and a column pass) made the consumers shared-memory bound.
+// Rows >= h of a stage hold stale finite data: they only reach padding rows
+// (row products) or meet v_I = 0 (column products).  W > 0: full-width tile
+// (constant offsets); W = 0: row stride ws < 64 (the diagonal corner tile).
+template <int W, bool COLS>
+__device__ __forceinline__ void tile_pass(const double* __restrict__ buf, const double* __restrict__ vj,
+                                          const double* __restrict__ vi, int lane, int ws_, double (&rp)[8],
+                                          double (&cp)[16]) {
+  const int ws = W > 0 ? W : ws_;
+  const int rg = lane >> 2, cg = lane & 3, sx = rg & 1;
+  const double* base = buf + 8 * rg * ws + 2 * cg;
+  double xi[8];
+  if (COLS) {
+#pragma unroll
+    for (int a = 0; a < 8; a += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(vi + 8 * rg + a);
+      xi[a] = t.x, xi[a + 1] = t.y;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (W == 0 && 8 * b >= ws) break;
+    const double2 xj = *reinterpret_cast<const double2*>(vj + 2 * cg + 8 * b);
+    const double* col = base + 8 * (b ^ sx);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const double2 t = *reinterpret_cast<const double2*>(col + a * ws);
+      rp[a] = fma(t.x, xj.x, rp[a]);
+      rp[a] = fma(t.y, xj.y, rp[a]);
+      if (COLS) {
+        cp[2 * b] = fma(t.x, xi[a], cp[2 * b]);
+        cp[2 * b + 1] = fma(t.y, xi[a], cp[2 * b + 1]);
+      }
+    }
   }
 }
 
-// Column products of a full-width swizzled tile: lane holds columns 2 lane,
-// 2 lane + 1, summed over all 64 rows against v_I (rows >= h meet v_I = 0).
-__device__ __forceinline__ void tile_cols(const double* __restrict__ buf, const double* __restrict__ vi, int lane,
-                                          double (&cc)[4]) {
-  const int q = 2 * lane;
+// Column partials over the 8 row groups (lane bits 2-4), halving the live
+// values per step: lane ends with chunk cg + 4 rg = lane, i.e. the sums of
+// columns 2 lane, 2 lane + 1 in cp[0], cp[1].  Fixed order.
+__device__ __forceinline__ void reduce_cols(int lane, double (&cp)[16]) {
 #pragma unroll
-  for (int r = 0; r < kTile; r += 2) {
-    const double2 w = *reinterpret_cast<const double2*>(vi + r);
-    const double2 a = *reinterpret_cast<const double2*>(buf + r * kTile + (q ^ (2 * (r & 7))));
-    const double2 b = *reinterpret_cast<const double2*>(buf + (r + 1) * kTile + (q ^ (2 * ((r + 1) & 7))));
-    cc[0] = fma(a.x, w.x, cc[0]);
-    cc[1] = fma(a.y, w.x, cc[1]);
-    cc[2] = fma(b.x, w.y, cc[2]);
-    cc[3] = fma(b.y, w.y, cc[3]);
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    const double send = up ? cp[i] : cp[i + 8], keep = up ? cp[i + 8] : cp[i];
+    cp[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    const double send = up ? cp[i] : cp[i + 4], keep = up ? cp[i + 4] : cp[i];
+    cp[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    const double send = up ? cp[i] : cp[i + 2], keep = up ? cp[i + 2] : cp[i];
+    cp[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+}
+// Row partials over the 4 column groups (lane bits 0-1): lane ends with rows
+// 8 rg + 2 cg + {0, 1} = 2 lane, 2 lane + 1 in rp[0], rp[1].
+__device__ __forceinline__ void reduce_rows(int lane, double (&rp)[8]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 2;
+    const double send = up ? rp[i] : rp[i + 4], keep = up ? rp[i + 4] : rp[i];
+    rp[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 1;
+    const double send = up ? rp[i] : rp[i + 2], keep = up ? rp[i + 2] : rp[i];
+    rp[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
   }
 }
 
@@ -321,8 +362,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       double cx[NBM], cy[NBM];
 #pragma unroll
       for (int q = 0; q < NBM; ++q) cx[q] = cy[q] = 0.0;
-      // row sums of rows lane / lane + 32 of the current row run
-      double ra[4] = {0.0, 0.0, 0.0, 0.0}, rb[4] = {0.0, 0.0, 0.0, 0.0};
+      // row partials of the current row run (rows 8 rg + a against the lane's columns)
+      double rp[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       const int4* ws = L.wsched + (long long)((rank * T_N + type) * kSwWarps + warp) * kMaxW;
       const int nw = L.nwsched[(rank * T_N + type) * kSwWarps + warp];
       int4 e = __ldg(ws);
@@ -335,28 +376,30 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
         const double* buf = stage + (size_t)st * kTileD;
         if (e.y & 1) {  // first tile of a row run
 #pragma unroll
-          for (int c = 0; c < 4; ++c) ra[c] = rb[c] = 0.0;
+          for (int c = 0; c < 8; ++c) rp[c] = 0.0;
         }
         while (ticket[st] != int(gp)) {
         }
         mbar_wait(&full[st], cpar);
-        if (wp == kTile)
-          tile_rows<kTile>(buf, wv + J * kTile, lane, wp, ra, rb);
-        else  // the corner tile of a grid row whose width is not a multiple of 64 (diagonal)
-          tile_rows<0>(buf, wv + J * kTile, lane, wp, ra, rb);
-        if (I != J) {  // column products T^T v_I from the same stage
-          double cc[4] = {0.0, 0.0, 0.0, 0.0};
-          tile_cols(buf, wv + I * kTile, lane, cc);
-          add_at(cx, cy, J, cc[0] + cc[2], cc[1] + cc[3]);
+        double cp[16];
+        if (I != J) {  // row products T v_J and column products T^T v_I from one pass
+#pragma unroll
+          for (int c = 0; c < 16; ++c) cp[c] = 0.0;
+          tile_pass<kTile, true>(buf, wv + J * kTile, wv + I * kTile, lane, wp, rp, cp);
+        } else if (wp == kTile) {
+          tile_pass<kTile, false>(buf, wv + J * kTile, wv, lane, wp, rp, cp);
+        } else {  // the corner tile of a grid row whose width is not a multiple of 64 (diagonal)
+          tile_pass<0, false>(buf, wv + J * kTile, wv, lane, wp, rp, cp);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
-        if (e.y & 2) {  // last tile of the row run: rows (lane, lane + 32) -> (2 lane, 2 lane + 1)
-          const double va = (ra[0] + ra[1]) + (ra[2] + ra[3]), vb = (rb[0] + rb[1]) + (rb[2] + rb[3]);
-          const int s0 = (2 * lane) & 31, s1 = (2 * lane + 1) & 31;
-          const double a0 = __shfl_sync(0xffffffffu, va, s0), b0 = __shfl_sync(0xffffffffu, vb, s0);
-          const double a1 = __shfl_sync(0xffffffffu, va, s1), b1 = __shfl_sync(0xffffffffu, vb, s1);
-          add_at(cx, cy, I, lane < 16 ? a0 : b0, lane < 16 ? a1 : b1);
+        if (I != J) {
+          reduce_cols(lane, cp);
+          add_at(cx, cy, J, cp[0], cp[1]);
+        }
+        if (e.y & 2) {  // last tile of the row run
+          reduce_rows(lane, rp);
+          add_at(cx, cy, I, rp[0], rp[1]);
         }
         e = en;
       }
@@ -425,26 +468,27 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
         while (ticket[st] != int(gp)) {
         }
         mbar_wait(&full[st], cpar);
+        // rows lane and lane + 32 of the chunk against the owned part of their
+        // column windows [c0, c0 + bw): four chains per row, fixed order
         double val[2] = {0.0, 0.0};
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int r = lane + 32 * u, i = q * Rb + r;
           if (r < Rb && i < B) {
             const int c0 = (i / NT + d0) * NT;
-            double v0 = 0.0, v1 = 0.0;
-            int c = 0;
-            for (; c + 1 < bw; c += 2) {
-              const int g0 = c0 + c, g1 = g0 + 1;
-              const double z0 = (g0 >= own_lo && g0 < own_hi) ? zv[g0] : 0.0;
-              const double z1 = (g1 >= own_lo && g1 < own_hi) ? zv[g1] : 0.0;
-              v0 = fma(buf[c * Rb + r], z0, v0);
-              v1 = fma(buf[(c + 1) * Rb + r], z1, v1);
+            const int ca = max(0, own_lo - c0), cb = min(bw, own_hi - c0);
+            const double* bp = buf + r;
+            const double* zp = zv + c0;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+            int c = ca;
+            for (; c + 3 < cb; c += 4) {
+              v0 = fma(bp[c * Rb], zp[c], v0);
+              v1 = fma(bp[(c + 1) * Rb], zp[c + 1], v1);
+              v2 = fma(bp[(c + 2) * Rb], zp[c + 2], v2);
+              v3 = fma(bp[(c + 3) * Rb], zp[c + 3], v3);
             }
-            if (c < bw) {
-              const int g0 = c0 + c;
-              v0 = fma(buf[c * Rb + r], (g0 >= own_lo && g0 < own_hi) ? zv[g0] : 0.0, v0);
-            }
-            val[u] = v0 + v1;
+            for (; c < cb; ++c) v0 = fma(bp[c * Rb], zp[c], v0);
+            val[u] = (v0 + v1) + (v2 + v3);
           }
         }
         __syncwarp();
@@ -478,9 +522,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
 
 // ------------------------------------------------------------ storage ---
 // D_k^-1 (dense column-major, lower triangle valid) -> lower tiles, diagonal
-// tiles mirrored to full.  Element (r, c) of a tile sits at r wp + (c ^ 2 (r & 7)):
-// 16-byte column pairs swizzled by row, so that 8 lanes reading one column pair
-// of 8 consecutive rows, or 8 column pairs of one row, hit distinct banks.
+// tiles mirrored to full, swizzled by sw_col (conflict-free quarter-warp loads
+// in tile_pass).
 // One CTA per (subdomain, grid row, tile).
 __global__ void compact_dinv_kernel(const double* __restrict__ Dinv, double* __restrict__ F, const int4* __restrict__ ent,
                                     int n_sym, long long blk, int B, int H) {
@@ -492,7 +535,7 @@ __global__ void compact_dinv_kernel(const double* __restrict__ Dinv, double* __r
   double* out = F + sk * blk + d.x;
   for (int idx = threadIdx.x; idx < h * wp; idx += blockDim.x) {
     const int rl = idx / wp;
-    const int r = I * kTile + rl, c = J * kTile + ((idx % wp) ^ (2 * (rl & 7)));
+    const int r = I * kTile + rl, c = J * kTile + sw_col(rl, idx % wp);
     double v = 0.0;
     if (r < B && c < B) v = c <= r ? D[(long long)c * B + r] : D[(long long)r * B + c];
     out[idx] = v;
@@ -558,7 +601,7 @@ __device__ void gen_dinv(const double* __restrict__ Fk, const SweepLayout& L, co
       const int4 d = L.ent[I * (I + 1) / 2 + J];
       const int wp = d.z & 0xffff;
       const double* row = Fk + d.x + (long long)rl * wp;
-      for (int c = lane; c < wp; c += 32) acc = fma(__ldg(row + (c ^ (2 * (rl & 7)))), w[J * kTile + c], acc);
+      for (int c = lane; c < wp; c += 32) acc = fma(__ldg(row + sw_col(rl, c)), w[J * kTile + c], acc);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -573,7 +616,7 @@ __device__ void gen_dinv(const double* __restrict__ Fk, const SweepLayout& L, co
       const int4 d = L.ent[I * (I + 1) / 2 + J];
       const int h = d.z >> 16, wp = d.z & 0xffff;
       for (int rl = lane; rl < h; rl += 32)
-        acc = fma(__ldg(Fk + d.x + (long long)rl * wp + (cl ^ (2 * (rl & 7)))), w[I * kTile + rl], acc);
+        acc = fma(__ldg(Fk + d.x + (long long)rl * wp + sw_col(rl, cl)), w[I * kTile + rl], acc);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
