@@ -48,6 +48,7 @@ constexpr int kMaxSched = 512;                         // entries per (rank, pha
 constexpr int kPre = 12;                               // prefetched rhs values per consumer thread
 constexpr int kMaxCS = 16;                             // cluster size limit (non-portable 16)
 constexpr int kSmemMax = 227 * 1024;
+constexpr int kSwHeader = 512;                         // barriers, tickets, schedule heads
 enum { T_SYM = 0, T_BLO = 1, T_BUP = 2, T_N = 3 };
 
 constexpr int kMaxW = 256;                             // entries per (rank, phase type, warp)
@@ -256,7 +257,12 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   volatile int* ticket = reinterpret_cast<volatile int*>(empty + 8);
   unsigned long long* slot_bar = empty + 12;   // partials of a D^-1 phase have arrived (CS > 1)
   unsigned long long* tpart_bar = empty + 13;  // band partials of a band phase have arrived (CS > 1)
-  double* wv = reinterpret_cast<double*>(smraw + (size_t)S * kTileD * 8 + 256);  // D^-1 input (full vector)
+  // per-phase-type schedule heads of this CTA's warps: the phase loop reads them
+  // from shared memory instead of waiting on global loads at every phase start
+  int4* hfirst = reinterpret_cast<int4*>(smraw + (size_t)S * kTileD * 8 + 192);  // [type][warp] first entry
+  int* hnw = reinterpret_cast<int*>(smraw + (size_t)S * kTileD * 8 + 384);        // [type][warp] entries
+  int* hns = hnw + T_N * kSwWarps;                                                // [type] stream length
+  double* wv = reinterpret_cast<double*>(smraw + (size_t)S * kTileD * 8 + kSwHeader);  // D^-1 input (full vector)
   double* red = wv + VL;                       // CTA sum of the warps' D^-1 partials
   double* zv = CS > 1 ? red + VL : red;        // D^-1 output, owned rows
   double* slots = zv + VL;                     // [source rank][owned row] partials (CS > 1)
@@ -272,6 +278,12 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
   // the ring starts zeroed: rows beyond a partial tile are then always finite
   for (int i = tid; i < S * kTileD / 2; i += kSwThreads) reinterpret_cast<double2*>(stage)[i] = make_double2(0.0, 0.0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the first bulk copy overwrites it
+  if (tid < T_N * kSwWarps) {
+    const int ty = tid / kSwWarps, w = tid % kSwWarps;
+    hfirst[tid] = __ldg(L.wsched + (long long)((rank * T_N + ty) * kSwWarps + w) * kMaxW);
+    hnw[tid] = L.nwsched[(rank * T_N + ty) * kSwWarps + w];
+    if (tid < T_N) hns[tid] = L.nsched[rank * T_N + tid];
+  }
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) ticket[i] = -1;
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
     int type, k;
     bool fwd;
     seg_info(seg, H, type, k, fwd);
-    const int n = L.nsched[rank * T_N + type];
+    const int n = hns[type];
     if (type == T_SYM) {
       // input w_k (forward: b_k minus the band partials of BLO_{k-1}; backward:
       // w_k minus those of BUP_k).  The forward stores w_k for the backward pass.
@@ -365,8 +377,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
       // row partials of the current row run (rows 8 rg + a against the lane's columns)
       double rp[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       const int4* ws = L.wsched + (long long)((rank * T_N + type) * kSwWarps + warp) * kMaxW;
-      const int nw = L.nwsched[(rank * T_N + type) * kSwWarps + warp];
-      int4 e = __ldg(ws);
+      const int nw = hnw[type * kSwWarps + warp];
+      int4 e = hfirst[type * kSwWarps + warp];
       for (int p = 0; p < nw; ++p) {
         const int4 en = __ldg(ws + min(p + 1, nw - 1));
         const unsigned gp = pos + e.x;
@@ -424,18 +436,19 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
             }
         }
         consumers_sync();
-        for (int i = tid; i < nb * kTile; i += kSwWarps * 32) red[i] += red2[i];
-        consumers_sync();
       }
-      if (CS > 1) {
+      if (CS > 1) {  // the two halves summed on the way to the owner of the row
         for (int i = tid; i < VL; i += kSwWarps * 32) {
           int r = 0;
           while (i >= L.own[r + 1]) ++r;
           double* dst = cluster.map_shared_rank(slots, r);
-          dst[rank * L.slot_len + i - L.own[r]] = red[i];
+          dst[rank * L.slot_len + i - L.own[r]] = red[i] + red2[i];
         }
         consumers_sync();  // every thread's pushes precede thread 0's release
         if (tid < CS) mbar_arrive_remote(slot_bar, tid);
+      } else {
+        for (int i = tid; i < VL; i += kSwWarps * 32) red[i] += red2[i];
+        consumers_sync();
       }
     } else {
       // input z_k / x_{k+1}: the owned rows, summed over the ranks in order
@@ -457,9 +470,10 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
 #pragma unroll
       for (int r = 0; r < CS; ++r) dst[r] = CS > 1 ? cluster.map_shared_rank(tpart, r) : tpart;
       const int4* ws = L.wsched + (long long)((rank * T_N + type) * kSwWarps + warp) * kMaxW;
-      const int nw = L.nwsched[(rank * T_N + type) * kSwWarps + warp];
+      const int nw = hnw[type * kSwWarps + warp];
+      int4 e = hfirst[type * kSwWarps + warp];
       for (int p = 0; p < nw; ++p) {
-        const int4 e = __ldg(ws + p);
+        const int4 en = __ldg(ws + min(p + 1, nw - 1));
         const unsigned gp = pos + e.x;
         seek(gp);
         const int st = (int)cst;
@@ -500,6 +514,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(double* __restrict
 #pragma unroll
             for (int rr = 0; rr < CS; ++rr) dst[rr][to + i - tl] = val[u];
         }
+        e = en;
       }
       consumers_sync();  // CS > 1: every thread's pushes precede the releases below
       if (CS > 1 && tid < CS) mbar_arrive_remote(tpart_bar, tid);
@@ -688,7 +703,7 @@ static SweepFn sweep_fn(int cs, int nbm) {
 
 static size_t smem_bytes(int stages, int VL, int CS, int slot_len, int tpart_len) {
   const size_t vec = 3 * (size_t)VL + (CS > 1 ? (size_t)VL + (size_t)CS * slot_len : 0) + (size_t)tpart_len + 2;
-  return (size_t)stages * kTileD * 8 + 256 + vec * 8;
+  return (size_t)stages * kTileD * 8 + kSwHeader + vec * 8;
 }
 
 void GpuSolver::build_sweep_layout() {
