@@ -291,10 +291,9 @@ int sgw_init_state(sgw_solver* s, const double* u0, const double* v0, const sgw_
   return guard([&] {
     GpuSolver& g = *s->g;
     set_force(g, force, 0);
-    DBuf<double> du, dv;
-    h2d(du, u0, g.P.n_nodes(), g.stream());
-    h2d(dv, v0, g.P.n_nodes(), g.stream());
-    g.init_state(du.p, dv.p, 0.0);
+    h2d(g.nodal_u0_, u0, g.P.n_nodes(), g.stream());
+    h2d(g.nodal_v0_, v0, g.P.n_nodes(), g.stream());
+    g.init_state(g.nodal_u0_.p, g.nodal_v0_.p, 0.0);
   });
 }
 
@@ -341,13 +340,17 @@ int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, cons
       std::vector<int> own(np);
       for (int q = 0; q < np; ++q) own[q] = g.G.owner_of_dof(g.probe_dofs[q]) == g.rank();
       g.d_probe_own.upload(own);
-      g.probe_hist.alloc((size_t)(n_steps + 1) * np * (2 + g.NT));
+      const size_t need = (size_t)(n_steps + 1) * np * (2 + g.NT);
+      if (g.probe_hist.n < need) g.probe_hist.alloc(need);
     }
     set_force(g, force, n_steps + 1);
-    DBuf<double> du, dv;
-    h2d(du, u0, g.P.n_nodes(), g.stream());
-    h2d(dv, v0, g.P.n_nodes(), g.stream());
-    g.init_state(du.p, dv.p, 0.0);
+    struct TableScope {  // a force table is the caller's memory: it is dropped when the run ends
+      GpuSolver& g;
+      ~TableScope() { g.drop_force_table(); }
+    } table_scope{g};
+    h2d(g.nodal_u0_, u0, g.P.n_nodes(), g.stream());
+    h2d(g.nodal_v0_, v0, g.P.n_nodes(), g.stream());
+    g.init_state(g.nodal_u0_.p, g.nodal_v0_.p, 0.0);
     g.record_probes(0);
     DBuf<double> full;
     if (h && h->full_state) {

@@ -431,8 +431,15 @@ class GpuSolver {
   // forcing
   int force_kind_ = 0, force_node_ = -1, force_dof_ = -1;
   double force_f0_ = 0, force_t0_ = 0, force_amp_ = 0;
-  std::vector<double> force_table_;
+  const double* force_tab_ = nullptr;  // caller's table (valid during sgw_run)
+  size_t force_len_ = 0;
   DBuf<double> force_row_, fext_;
+ public:
+  void drop_force_table() {
+    if (force_kind_ == 2) force_kind_ = 0, force_tab_ = nullptr, force_len_ = 0;
+  }
+  DBuf<double> nodal_u0_, nodal_v0_;  // sgw_run / sgw_init_state: nodal initial fields (kept across calls)
+ private:
   cudaEvent_t ev_[8];
   // host-driven PCG: pinned residual scalar and the two per-iteration graphs
   double* h_scal_ = nullptr;

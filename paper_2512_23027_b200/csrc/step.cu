@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cstring>
+
 #include "solver.cuh"
 
 namespace sgw {
@@ -553,8 +555,11 @@ void GpuSolver::set_force_point(int node, double f0, double t0, double amp) {
 
 void GpuSolver::set_force_table(const double* table, int rows) {
   force_kind_ = 2;
-  force_table_.assign(table, table + (size_t)rows * P.n_nodes());
-  force_row_.alloc(P.n_nodes());
+  // sgw_run is synchronous: the caller's table outlives every step, so rows are
+  // uploaded straight from it (no host copy of the table)
+  force_tab_ = table;
+  force_len_ = (size_t)rows * P.n_nodes();
+  if (force_row_.n != (size_t)P.n_nodes()) force_row_.alloc(P.n_nodes());
   if (fext_.n != (size_t)n) fext_.alloc(n);
 }
 
@@ -572,8 +577,8 @@ const double* GpuSolver::force_at(double t, int row, double* fval) {
   }
   if (force_kind_ == 2) {
     const size_t nn = P.n_nodes();
-    if ((size_t)row * nn >= force_table_.size()) throw Error(1, "force table too short");
-    SGW_CUDA(cudaMemcpyAsync(force_row_.p, force_table_.data() + (size_t)row * nn, nn * sizeof(double),
+    if ((size_t)row * nn >= force_len_) throw Error(1, "force table too short");
+    SGW_CUDA(cudaMemcpyAsync(force_row_.p, force_tab_ + (size_t)row * nn, nn * sizeof(double),
                              cudaMemcpyHostToDevice, st_));
     reduce_nodal_kernel<<<cdiv(n, 256), 256, 0, st_>>>(force_row_.p, fext_.p, P.nx, P.ny);
     SGW_LAUNCHED();

@@ -4,6 +4,7 @@ import sys
 import time
 
 import numpy as np
+import torch  # noqa: F401  (before libsgw_b200: torch must bind its own bundled NCCL first)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT]
@@ -28,3 +29,26 @@ for rep in range(3):
     h = s.run(z, z, 10, f)
     w3 = time.perf_counter()
     print(f"init_state {w1 - w0:.3f} s  advance(10) {w2 - w1:.3f} s  run(10) {w3 - w2:.3f} s  stats {s.stats()}")
+
+# table force (the bench's e2e leg): run(0) = pure API overhead (uploads + initial acceleration)
+table = np.zeros((21, (nx + 1) ** 2))
+tt = 0.0
+for k in range(21):
+    table[k, node] = sg.ricker(tt, bench.F0, bench.T0)
+    tt += c["dt"]
+s.options.probe_nodes = [node]
+ft = sg.ForceSpec(table=table)
+for rep in range(3):
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    s.run(z, z, 0, sg.ForceSpec(table=table[:1].copy()))
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    h = s.run(z, z, 20, ft)
+    torch.cuda.synchronize()
+    w2 = time.perf_counter()
+    h2 = s.run(z, z, 20, f)
+    torch.cuda.synchronize()
+    w3 = time.perf_counter()
+    print(f"run(0) {1e3 * (w1 - w0):.2f} ms  run(20, table) {1e3 * (w2 - w1):.2f} ms  run(20, point) {1e3 * (w3 - w2):.2f} ms  "
+          f"iters {int(h.iterations.sum())} {int(h2.iterations.sum())} step_ms {s.stats().get('step_ms')}")
