@@ -12,6 +12,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cstdio>
+
 #include "solver.cuh"
 
 namespace sgw {
@@ -398,9 +400,23 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   P.mass_scale = mf + df * P.alpha0;
   P.stiff_scale = 1.0 + df * P.alpha1;
 
+  // SGW_SETUP_TIMING=1: wall-clock phases of the constructor on stderr
+  const bool timing = std::getenv("SGW_SETUP_TIMING") != nullptr;
+  auto tlast = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(st_);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sgw setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - tlast).count());
+    tlast = now;
+  };
+  lap("handles");
   const Stencils stc = build_stencils(P, G, true);
+  lap("build_stencils (host)");
   build_device_inputs(stc);
+  lap("device inputs + SG-op JIT");
   build_maps();
+  lap("build_maps");
   // setup in batches of subdomains sized so the dense temporaries (A_II block
   // factor, L^-1 blocks, S_s, the rolling L^-1 A_IG) stay within ~24 GB
   B = G.W * NT;
@@ -408,6 +424,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   for (int s = 0; s < NS; ++s) amax_ = std::max(amax_, NT * ng_[s]);
   if (!direct_) plan_nn2();
   build_sweep_layout();
+  lap("plan_nn2 + sweep layout");
   {
     const double per = 8.0 * (3.0 * G.H * double(B) * B + double(amax_) * amax_ + 2.0 * double(B) * amax_);
     int nb = std::max(1, std::min(NS, int(24e9 / per)));
@@ -416,9 +433,12 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
     for (int b0 = 0; b0 < NS; b0 += nb) {
       const int cnt = std::min(nb, NS - b0);
       setup_interior_and_schur(b0, cnt);
+      lap("interior factor + Schur batch");
       if (!direct_) nn2_batch(b0, cnt, fcc);
+      lap("NN2 batch");
     }
     if (!direct_) finish_nn2(fcc);
+    lap("finish_nn2");
   }
 
   // work vectors (the step kernels use 32-bit index arithmetic)
@@ -434,8 +454,11 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   yI.zero(st_), wI.zero(st_);  // unit rows of ragged blocks stay zero
   scal.alloc(16), scal.zero(st_);
   dpart.alloc(1024), dcount.alloc(4), dcount.zero(st_);
+  lap("work vectors");
   setup_fused_pcg();
+  lap("persistent PCG setup");
   build_coupling_blocks();  // A_GI / A_IG and interface-row force blocks, memory permitting
+  lap("coupling blocks");
   SGW_CUDA(cudaStreamSynchronize(st_));
   setup_bytes_ = DevBytes::total.load() - bytes0;
   setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
