@@ -59,6 +59,25 @@ def test_two_level_with_one_block_and_no_corners_is_exact_inverse(gpu):
     assert rep["converged"] and rep["iterations"] == 1
 
 
+def test_llt_regularized_retry_on_a_floating_block(gpu):
+    # dd.cpp:66-76: a singular PSD block (a floating subdomain: constants in the
+    # null space) hits an exact zero pivot in the first Cholesky; the retry
+    # factors S + 1e-10 trace(S) / n I.  The response to the null-space vector
+    # is 1 / shift, so it pins the shift the retry branch applied.
+    S = np.array([[1.0, -1.0], [-1.0, 1.0]])
+    ls = sg.LocalSchur(S=S, gmap=np.arange(2), weights=np.ones(2), r_idx=np.arange(2))
+    sys = sg.SchurFromLocals(2, 0, [ls])
+    shift = 1e-10 * np.trace(S) / 2
+    for r in (np.array([1.0, 1.0]), np.array([1.0, 0.0])):
+        z = sys.apply_nn2(r)
+        ref = np.linalg.solve(S + shift * np.eye(2), r)
+        assert np.abs(z - ref).max() <= 1e-5 * np.abs(ref).max()
+    # an indefinite block still fails after the shift (dd.cpp:72-74)
+    bad = sg.LocalSchur(S=np.array([[1.0, 2.0], [2.0, 1.0]]), gmap=np.arange(2), weights=np.ones(2), r_idx=np.arange(2))
+    with pytest.raises(Exception, match="regulariz"):
+        sg.SchurFromLocals(2, 0, [bad])
+
+
 def _random_locals(seed=3):
     """three overlapping locals on a 10-node interface whose last 2 nodes are corners"""
     rng = np.random.default_rng(seed)
