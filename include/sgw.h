@@ -103,7 +103,9 @@ typedef struct sgw_problem {
 
 /* ForceFn (det_loop.hpp:32): kind 0 none; 1 Ricker wavelet
  *   amp * (1 - 2 pi^2 f0^2 (t - t0)^2) exp(-pi^2 f0^2 (t - t0)^2) at mesh node `node`;
- * 2 nodal table, (n_steps + 1) x n_nodes rows for t_0 .. t_N.                 */
+ * 2 nodal table, (n_steps + 1) x n_nodes rows for t_0 .. t_N, read straight
+ *   from the caller's buffer during sgw_run (it must stay valid until sgw_run
+ *   returns; the solver drops it afterwards).                                */
 typedef struct sgw_force {
   int kind;
   int node;

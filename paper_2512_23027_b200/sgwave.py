@@ -766,6 +766,11 @@ class SgSolver:
         pc = np.zeros((len(probes), self.n_terms, n_steps + 1))
         full = np.zeros((n_steps + 1, self.n_terms * self.n_dofs)) if self.options.store_full else None
         hist = _History(_p(its), _p(res), len(probes), _p(probes), _p(pm), _p(ps), _p(full), _p(pc))
+        if force is not None and force.table is not None:
+            # the C ABI reads (n_steps + 1) x n_nodes doubles straight from the caller's buffer
+            tb = np.asarray(force.table)
+            if tb.ndim != 2 or tb.shape[0] < n_steps + 1 or tb.shape[1] != u0.size:
+                raise SgInvalidArgument(SGW_EINVAL, "force table must be (n_steps + 1) x n_nodes")
         f = (force or ForceSpec())._c()
         _check(load_library().sgw_run(self._h, _p(u0), _p(v0), n_steps, C.byref(f), C.byref(hist)))
         times = np.cumsum(np.r_[0.0, np.full(n_steps, self.params.dt)])

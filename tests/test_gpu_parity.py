@@ -403,6 +403,31 @@ def test_probes_match_full_state(gpu):
         assert np.allclose(h.probe_std[p], std, rtol=1e-14, atol=0)
 
 
+def test_force_table_matches_point_source(gpu):
+    # ForceFn as a nodal table (det_loop.hpp:32; rows t_0 .. t_N read straight
+    # from the caller's buffer) against the same Ricker source given as a point
+    # force, and a table that is too short is rejected
+    nx, dt, steps = 16, 2e-3, 8
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, 2, 2)
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    g = sg.SgSolver(nx, nx, 2, 2, coeff, O.triple_products(2, 2, 2), params=sg.NewmarkParams(dt=dt),
+                    options=sg.SgOptions(tol=1e-10, store_full=True))
+    z = np.zeros((nx + 1) ** 2)
+    table = np.zeros((steps + 1, (nx + 1) ** 2))
+    t = 0.0
+    for k in range(steps + 1):  # the solver's own time accumulation (t += dt)
+        table[k, node] = sg.ricker(t, 10.0, 0.1)
+        t += dt
+    hp = g.run(z, z, steps, sg.ForceSpec(node=node, f0=10.0, t0=0.1))
+    ht = g.run(z, z, steps, sg.ForceSpec(table=table))
+    assert np.array_equal(hp.iterations, ht.iterations)
+    assert np.abs(hp.full_state - ht.full_state).max() <= 1e-14 * np.abs(hp.full_state).max()
+    ht2 = g.run(z, z, steps, sg.ForceSpec(table=table))  # rerun from the same buffer: bitwise identical
+    assert np.array_equal(ht.full_state, ht2.full_state)
+    with pytest.raises(Exception):
+        g.run(z, z, steps + 2, sg.ForceSpec(table=table[: steps + 1].copy()))
+
+
 def test_constrained_probe_rejected(gpu):
     coeff = O.lognormal_coeff(8, 8, 0.2, 1.0, 1.0, 1, 1)
     g = sg.SgSolver(8, 8, 2, 2, coeff, O.triple_products(1, 1, 1), params=sg.NewmarkParams(dt=0.05),
