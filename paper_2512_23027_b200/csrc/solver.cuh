@@ -355,6 +355,7 @@ class GpuSolver {
   DBuf<int> sw_off, sw_cuts, sw_ncut, sw_wcuts, sw_nw;
   int sweep_cs_ = 1, sweep_nch_ = 0, sweep_nbm_ = 12;
   bool sweep_generic_ = false;  // large interior blocks: sweep_generic_kernel
+  bool sweep_small_ = false;    // small interior blocks (B <= 96): sweep_small_kernel, one warp per subdomain
   bool direct_ = false;          // one subdomain, no interface (sg.cpp:146): the step is one interior solve
   long long sweep_lo_off_ = 0, sweep_up_off_ = 0;
   SweepLayout* sweep_layout_ = nullptr;

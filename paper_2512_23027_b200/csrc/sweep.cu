@@ -41,6 +41,11 @@ namespace cg = cooperative_groups;
 
 namespace sgw {
 
+static bool env_off(const char* name) {  // tuning / test hook: NAME=0 disables a path
+  const char* e = std::getenv(name);
+  return e && std::atoi(e) == 0;
+}
+
 constexpr int kSwWarps = 4;                            // consumer warps
 constexpr int kSwThreads = (kSwWarps + 1) * 32;        // + one TMA producer warp
 constexpr int kTileD = kTile * kTile;                  // doubles per stage
@@ -67,6 +72,10 @@ struct SweepLayout {
   int own[kMaxCS + 1];                                  // rank r owns rows [own[r], own[r+1])
   int tlo[2][kMaxCS], thi[2][kMaxCS], toff[2][kMaxCS];  // band rows rank r contributes (LO, UP)
   int n_sym, n_ent;
+  // small-block kernel (sweep_small_kernel): D_k^-1 stored full, column-major with row pitch Bp = 32 RL,
+  // streamed in chunks of kSmCols columns; stage size in doubles
+  int Bp, nD, stage_len, nch;
+  long long lo_off, up_off;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -685,6 +694,235 @@ __global__ void __launch_bounds__(kGenThreads, 1) sweep_generic_kernel(double* _
   }
 }
 
+// ------------------------------------------------- small blocks ---------
+// The same block Thomas solve for small interior blocks (B <= 96: few PCE
+// terms or small subdomains, e.g. C1 with B = 90 or deterministic solves with
+// B = W).  There the tiled kernel is bound by its CTA barriers and cluster
+// handshakes (about 2 us per phase, 4 phases per grid row), not by bytes.
+// Here one OWNER warp holds a subdomain's vectors in registers: lane l has
+// rows l, l + 32, l + 64, so the chain w_k -> z_k = D_k^-1 w_k -> band
+// product -> w_{k+1} stays in one warp.  Three helper warps share the D^-1
+// product (each consumer warp takes 4 of a chunk's 16 columns; the owner adds
+// the partials in warp order), which costs two named barriers per grid row.
+// D_k^-1 is stored full (symmetric: column c of the stored block is row c),
+// column-major with row pitch Bp = 32 RL: lane l reads element (l + 32 u, c),
+// i.e. consecutive addresses, against the broadcast w[c].  A producer warp
+// streams chunks of kSmCols columns and the band chunks through a ring of TMA
+// bulk copies; the bands use the tiled kernel's chunk format (Rb = 64 rows, so
+// a chunk's rows lane, lane + 32 are rows the owner lane holds: u = 2 q,
+// 2 q + 1).  Fixed summation order: bitwise reproducible.
+constexpr int kSmCols = 16;     // D^-1 columns per stage
+constexpr int kSmMaxStages = 16;
+constexpr int kSmCons = 4;      // consumer warps (owner + helpers)
+constexpr int kSmThreads = 32 * (kSmCons + 1);
+__device__ __forceinline__ void small_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kSmCons * 32) : "memory"); }
+
+template <int RL>
+__global__ void __launch_bounds__(kSmThreads, 1) sweep_small_kernel(double* __restrict__ x, const double* __restrict__ F,
+                                                                    const SweepLayout L) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int Bp = 32 * RL;
+  const int s = blockIdx.x, B = L.B, H = L.H, S = L.stages;
+  double* stage = reinterpret_cast<double*>(smraw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw + (size_t)S * L.stage_len * 8);
+  unsigned long long* empty = full + kSmMaxStages;
+  double* wv = reinterpret_cast<double*>(empty + kSmMaxStages);  // D^-1 input [Bp], broadcast to the lanes
+  double* zv = wv + Bp;              // D^-1 output [32 | Bp | 32]: zero guards of >= NT entries on both sides
+  double* zpart = zv + Bp + 64;      // helpers' partial products [kSmCons - 1][Bp]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* Fs = F + (long long)s * L.per_sub;
+  double* xs = x + (long long)s * H * B;
+  const int nseg = 4 * H - 3;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], kSmCons);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 2 * Bp + 64; i += kSmThreads) wv[i] = 0.0;  // wv and zv with its guards
+  __syncthreads();
+
+  if (warp == kSmCons) {  // ------------------------------------ producer ---
+    unsigned pos = 0, st = 0, par = 1;
+    for (int seg = 0; seg < nseg; ++seg) {
+      int type, k;
+      bool fwd;
+      seg_info(seg, H, type, k, fwd);
+      const double* base = Fs + k * L.blk + (type == T_SYM ? 0 : type == T_BLO ? L.lo_off : L.up_off);
+      const int n = type == T_SYM ? L.nD : L.nch;
+      const int len = type == T_SYM ? kSmCols * Bp : L.bw * L.Rb;
+      for (int p = 0; p < n; ++p, ++pos) {
+        if (pos >= (unsigned)S) mbar_wait(&empty[st], par);
+        if (lane == 0) {
+          mbar_expect_tx(&full[st], unsigned(len * 8));
+          tma_bulk_load(stage + (size_t)st * L.stage_len, base + (long long)p * len, unsigned(len * 8), &full[st]);
+        }
+        __syncwarp();
+        if (++st == (unsigned)S) st = 0, par ^= 1u;
+      }
+    }
+    return;
+  }
+
+  // ----------------------------------------------------------- consumers ---
+  const int NT = L.NT, bw = L.bw, Rb = L.Rb;
+  const bool owner = warp == 0;
+  unsigned st = 0, par = 0;
+  auto next_stage = [&]() {
+    if (++st == (unsigned)S) st = 0, par ^= 1u;
+  };
+  double pre[RL], z[RL], t[RL];
+#pragma unroll
+  for (int u = 0; u < RL; ++u) {
+    const int r = lane + 32 * u;
+    pre[u] = owner && r < B ? __ldcg(xs + r) : 0.0;
+    z[u] = t[u] = 0.0;
+  }
+  double* zc = zv + 32;  // zc[-NT .. B + NT) is addressable; entries outside [0, B) stay zero
+  int node0[RL];         // first column of row lane + 32 u's own node (band windows start at node0 - NT / node0)
+#pragma unroll
+  for (int u = 0; u < RL; ++u) node0[u] = (lane + 32 * u) / NT * NT;
+  for (int seg = 0; seg < nseg; ++seg) {
+    int type, k;
+    bool fwd;
+    seg_info(seg, H, type, k, fwd);
+    if (type == T_SYM) {
+      if (owner) {
+        // w_k = b_k - (band partial of the previous phase); the forward stores it for the backward pass
+        const bool band_in = !(fwd && k == 0);
+#pragma unroll
+        for (int u = 0; u < RL; ++u) {
+          const int r = lane + 32 * u;
+          const double w = band_in ? pre[u] - t[u] : pre[u];
+          wv[r] = w;
+          if (fwd && k > 0 && r < B) xs[(long long)k * B + r] = w;
+        }
+        const int nxt = fwd ? (k + 1 < H ? k + 1 : H - 2) : k - 1;
+        if (nxt >= 0) {
+#pragma unroll
+          for (int u = 0; u < RL; ++u) {
+            const int r = lane + 32 * u;
+            pre[u] = r < B ? __ldcg(xs + (long long)nxt * B + r) : 0.0;
+          }
+        }
+      }
+      small_sync();  // w_k is in wv (and the owner has read the helpers' previous partials)
+      double za[RL], zb[RL];
+#pragma unroll
+      for (int u = 0; u < RL; ++u) za[u] = zb[u] = 0.0;
+      for (int q = 0; q < L.nD; ++q) {
+        // this warp's 4 of the chunk's 16 columns (columns past B are stored zeros and meet w = 0)
+        const double* buf = stage + (size_t)st * L.stage_len + 4 * warp * Bp + lane;
+        const double* wq = wv + q * kSmCols + 4 * warp;
+        mbar_wait(&full[st], par);
+        const double2 w01 = *reinterpret_cast<const double2*>(wq);
+        const double2 w23 = *reinterpret_cast<const double2*>(wq + 2);
+#pragma unroll
+        for (int u = 0; u < RL; ++u) {
+          za[u] = fma(buf[32 * u], w01.x, za[u]);
+          zb[u] = fma(buf[Bp + 32 * u], w01.y, zb[u]);
+          za[u] = fma(buf[2 * Bp + 32 * u], w23.x, za[u]);
+          zb[u] = fma(buf[3 * Bp + 32 * u], w23.y, zb[u]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        next_stage();
+      }
+      if (!owner) {
+#pragma unroll
+        for (int u = 0; u < RL; ++u) zpart[(warp - 1) * Bp + lane + 32 * u] = za[u] + zb[u];
+      }
+      small_sync();  // the helpers' partials are in zpart
+      if (owner) {
+#pragma unroll
+        for (int u = 0; u < RL; ++u) {
+          const int r = lane + 32 * u;
+          double v = za[u] + zb[u];
+#pragma unroll
+          for (int h = 0; h < kSmCons - 1; ++h) v += zpart[h * Bp + r];
+          z[u] = v;
+          if (r < B) zc[r] = v;
+        }
+        __syncwarp();
+      }
+    } else {
+      if (!owner) {  // helpers only release the band stages (the owner reads them)
+        for (int q = 0; q < L.nch; ++q) {
+          if (lane == 0) mbar_arrive(&empty[st]);
+          next_stage();
+        }
+        continue;
+      }
+      // x_{k+1} is final in the backward pass
+      if (!fwd) {
+#pragma unroll
+        for (int u = 0; u < RL; ++u) {
+          const int r = lane + 32 * u;
+          if (r < B) xs[(long long)(k + 1) * B + r] = z[u];
+        }
+      }
+      const int d0 = type == T_BLO ? -1 : 0;
+#pragma unroll
+      for (int u = 0; u < RL; ++u) t[u] = 0.0;
+      for (int q = 0; q < L.nch; ++q) {
+        const double* buf = stage + (size_t)st * L.stage_len;
+        mbar_wait(&full[st], par);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int u = 2 * q + h;  // chunk rows lane, lane + 32 = rows lane + 32 u of the block
+          const int r = lane + 32 * h, i = q * Rb + r;
+          if (u < RL && i < B) {
+            int c0 = 0;  // window [c0, c0 + bw): zc is zero outside [0, B)
+#pragma unroll
+            for (int uu = 0; uu < RL; ++uu)
+              if (uu == u) c0 = node0[uu] + d0 * NT;
+            const double* bp = buf + r;
+            const double* zp = zc + c0;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+            int c = 0;
+            for (; c + 3 < bw; c += 4) {
+              v0 = fma(bp[c * Rb], zp[c], v0);
+              v1 = fma(bp[(c + 1) * Rb], zp[c + 1], v1);
+              v2 = fma(bp[(c + 2) * Rb], zp[c + 2], v2);
+              v3 = fma(bp[(c + 3) * Rb], zp[c + 3], v3);
+            }
+            for (; c < bw; ++c) v0 = fma(bp[c * Rb], zp[c], v0);
+            const double val = (v0 + v1) + (v2 + v3);
+#pragma unroll
+            for (int uu = 0; uu < RL; ++uu)
+              if (uu == u) t[uu] = val;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        next_stage();
+      }
+    }
+  }
+  // x_0 (the last phase was SYM_0)
+  if (owner) {
+#pragma unroll
+    for (int u = 0; u < RL; ++u) {
+      const int r = lane + 32 * u;
+      if (r < B) xs[r] = z[u];
+    }
+  }
+}
+
+// D_k^-1 (dense column-major, lower triangle valid) -> the small kernel's
+// full column-major block of nD kSmCols columns with row pitch Bp (zeros
+// past B).  One CTA per (subdomain, grid row).
+__global__ void compact_dinv_small_kernel(const double* __restrict__ Dinv, double* __restrict__ F, long long blk, int B,
+                                          int Bp, int ncol) {
+  const long long sk = blockIdx.x;
+  const double* D = Dinv + sk * (long long)B * B;
+  double* out = F + sk * blk;
+  for (int idx = threadIdx.x; idx < ncol * Bp; idx += blockDim.x) {
+    const int c = idx / Bp, r = idx % Bp;
+    double v = 0.0;
+    if (r < B && c < B) v = c <= r ? D[(long long)c * B + r] : D[(long long)r * B + c];
+    out[idx] = v;
+  }
+}
+
 using SweepFn = void (*)(double*, const double*, const SweepLayout);
 static SweepFn sweep_fn(int cs, int nbm) {
 #define SGW_SW(C)                                                  \
@@ -750,6 +988,29 @@ void GpuSolver::build_sweep_layout() {
     sweep_lo_off_ = lo_off, sweep_up_off_ = up_off, sweep_nch_ = nch, sweep_cs_ = 1;
     Fcomp.alloc(size_t(NS) * L.per_sub);
     ensure_dyn_smem((const void*)sweep_generic_kernel, 3 * (size_t)VL * 8);
+    return;
+  }
+  // small blocks: one consumer warp per subdomain (sweep_small_kernel)
+  // (SGW_SWEEP_CS, the test hook that forces a cluster size, asks for the tiled kernel)
+  sweep_small_ = B <= 96 && Rb == 64 && NT <= 32 && !env_off("SGW_SWEEP_SMALL") && !std::getenv("SGW_SWEEP_CS");
+  if (sweep_small_) {
+    SweepLayout L{};
+    const int RL = (B + 31) / 32, Bp = 32 * RL, nD = (B + kSmCols - 1) / kSmCols;
+    const long long lo = ((long long)nD * kSmCols * Bp + 31) & ~31LL;
+    const long long up = (lo + (long long)nch * bw * Rb + 31) & ~31LL;
+    L.blk = (up + (long long)nch * bw * Rb + 31) & ~31LL;
+    L.per_sub = (long long)H * L.blk;
+    L.B = B, L.H = H, L.nb = nb, L.VL = VL, L.NT = NT, L.Rb = Rb, L.bw = bw;
+    L.Bp = Bp, L.nD = nD, L.nch = nch, L.lo_off = lo, L.up_off = up;
+    L.stage_len = std::max(kSmCols * Bp, bw * Rb);
+    L.stages = std::max(2, std::min<int>(kSmMaxStages, int((200 * 1024) / (L.stage_len * 8))));
+    delete sweep_layout_;
+    sweep_layout_ = new SweepLayout(L);
+    sweep_lo_off_ = lo, sweep_up_off_ = up, sweep_nch_ = nch, sweep_cs_ = 1;
+    Fcomp.alloc(size_t(NS) * L.per_sub);
+    const void* fn = RL == 1 ? (const void*)sweep_small_kernel<1> : RL == 2 ? (const void*)sweep_small_kernel<2>
+                                                                             : (const void*)sweep_small_kernel<3>;
+    ensure_dyn_smem(fn, sweep_smem_bytes());
     return;
   }
   // cluster size: about one wave of CTAs over the 148 SMs
@@ -919,6 +1180,12 @@ void GpuSolver::extract_band_batch(int b0, int nb) {
 // D_k^-1 blocks of subdomains [b0, b0 + nb) (batch-local, dense) -> tiles
 void GpuSolver::compact_dinv_batch(int b0, int nb, const double* dinv) {
   const SweepLayout& L = *sweep_layout_;
+  if (sweep_small_) {
+    compact_dinv_small_kernel<<<(unsigned)((long long)nb * L.H), 256, 0, st_>>>(dinv, Fcomp.p + (size_t)b0 * L.per_sub, L.blk,
+                                                                                L.B, L.Bp, L.nD * kSmCols);
+    SGW_LAUNCHED();
+    return;
+  }
   const long long nblk = (long long)nb * L.H * L.n_sym;
   if (nblk >= (1LL << 31)) throw Error(1, "sweep: too many tiles per setup batch");
   compact_dinv_kernel<<<(unsigned)nblk, 256, 0, st_>>>(dinv, Fcomp.p + (size_t)b0 * L.per_sub, L.ent, L.n_sym, L.blk,
@@ -931,6 +1198,8 @@ void destroy_sweep_layout(SweepLayout* p) { delete p; }
 size_t GpuSolver::sweep_smem_bytes() const {
   const SweepLayout& L = *sweep_layout_;
   if (sweep_generic_) return 3 * (size_t)L.VL * 8;
+  if (sweep_small_)
+    return (size_t)L.stages * L.stage_len * 8 + 2 * kSmMaxStages * 8 + (size_t)((2 + kSmCons - 1) * L.Bp + 64) * 8;
   return smem_bytes(L.stages, L.VL, sweep_cs_, L.slot_len, L.tpart_len);
 }
 
@@ -940,6 +1209,16 @@ void GpuSolver::sweep(double* x) {
   KP.begin(K_SWEEP, st_, &e0);
   if (sweep_generic_) {
     sweep_generic_kernel<<<NS, kGenThreads, sweep_smem_bytes(), st_>>>(x, Fcomp.p, L, sweep_lo_off_, sweep_up_off_);
+    SGW_LAUNCHED();
+    KP.end(st_);
+    return;
+  }
+  if (sweep_small_) {
+    const int RL = (L.B + 31) / 32;
+    const size_t smem = sweep_smem_bytes();
+    if (RL == 1) sweep_small_kernel<1><<<NS, kSmThreads, smem, st_>>>(x, Fcomp.p, L);
+    else if (RL == 2) sweep_small_kernel<2><<<NS, kSmThreads, smem, st_>>>(x, Fcomp.p, L);
+    else sweep_small_kernel<3><<<NS, kSmThreads, smem, st_>>>(x, Fcomp.p, L);
     SGW_LAUNCHED();
     KP.end(st_);
     return;

@@ -207,6 +207,27 @@ def test_gaussian_pulse_trajectory_matches_oracle(gpu):
     assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-8
 
 
+@pytest.mark.parametrize("case", [(8, 2, 2, 1, 1, 1), (16, 2, 2, 2, 2, 2), (24, 2, 2, 2, 4, 2), (32, 2, 2, 2, 2, 2),
+                                  (26, 4, 3, 2, 3, 2), (9, 3, 3, 1, 2, 2)])
+def test_small_block_sweep_matches_tiled_and_oracle(gpu, monkeypatch, case):
+    # sweep_small_kernel (B = W (P+1) <= 96: one consumer warp per subdomain,
+    # rows lane, lane + 32, lane + 64 in registers) for B = 6 .. 90 (one to three
+    # rows per lane), ragged frames and 2-row interiors: oracle trajectory, and
+    # the tiled kernel (SGW_SWEEP_SMALL=0) on the same problem
+    nx, px, py, L, pin, pout = case
+    g, c = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 2e-3)
+    u0 = O.gaussian_pulse(nx, nx)
+    hg = g.run(u0, 0 * u0, 6)
+    hc = c.run(u0, 0 * u0, 6, store_full=True)
+    assert np.all(np.abs(hg.iterations - hc["iterations"]) <= 1)
+    assert np.linalg.norm(hg.full_state - hc["full"]) / np.linalg.norm(hc["full"]) <= 1e-10
+    assert np.array_equal(hg.full_state, g.run(u0, 0 * u0, 6).full_state)  # bitwise reproducible
+    monkeypatch.setenv("SGW_SWEEP_SMALL", "0")
+    g2, _ = pair(nx, px, py, 0.3, 0.5, L, pin, pout, 2e-3)
+    ht = g2.run(u0, 0 * u0, 6)
+    assert np.linalg.norm(hg.full_state - ht.full_state) / np.linalg.norm(ht.full_state) <= 1e-11
+
+
 @pytest.mark.parametrize("cs", ["1", "2", "4", "8", "16"])
 def test_interior_sweep_every_cluster_size(gpu, monkeypatch, cs):
     # the batched Dirichlet solve (one thread-block cluster of CS CTAs per
