@@ -9,8 +9,17 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges show up under Nsight Systems / Compute, no-ops otherwise
 
 namespace sgw {
+
+// NVTX range over a host scope (setup phases, the phases of a Newmark step).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Status-carrying exception; capi.cpp maps it to the sgw_status codes.
 struct Error : std::runtime_error {

@@ -403,7 +403,9 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   // SGW_SETUP_TIMING=1: wall-clock phases of the constructor on stderr
   const bool timing = std::getenv("SGW_SETUP_TIMING") != nullptr;
   auto tlast = std::chrono::steady_clock::now();
+  nvtxRangePushA("sgw setup");
   auto lap = [&](const char* what) {
+    nvtxMarkA(what);
     if (!timing) return;
     cudaStreamSynchronize(st_);
     const auto now = std::chrono::steady_clock::now();
@@ -460,6 +462,7 @@ GpuSolver::GpuSolver(Problem p, std::unique_ptr<Comm> comm) : P(std::move(p)), c
   build_coupling_blocks();  // A_GI / A_IG and interface-row force blocks, memory permitting
   lap("coupling blocks");
   SGW_CUDA(cudaStreamSynchronize(st_));
+  nvtxRangePop();
   setup_bytes_ = DevBytes::total.load() - bytes0;
   setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

@@ -693,6 +693,8 @@ __global__ void interior_from_global_kernel(LocalArgs A, int n, const double* __
 int GpuSolver::step(int* iters_out) {
   const long long N = (long long)NSTATE;
   const int grid = std::min(cdiv(N, 256), 8 * kNumSMs * 8);
+  NvtxRange nvtx_step("sgw step");
+  nvtxRangePushA("rhs: predictors, local force, interior solve, interface assembly");
   cudaEventRecord(ev_[2], st_);
   predictor_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, um.p, uc.p, N, P.dt, P.zeta, P.gamma);
   SGW_LAUNCHED();
@@ -735,6 +737,7 @@ int GpuSolver::step(int* iters_out) {
   if (direct_) {
     // one subdomain (sg.cpp:301-305): y is the whole solution, no interface solve
     SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
+    nvtxRangePop();
     cudaEventRecord(ev_[3], st_);
     cudaEventRecord(ev_[4], st_);
     update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
@@ -764,19 +767,24 @@ int GpuSolver::step(int* iters_out) {
   SGW_LAUNCHED();
   scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
   halo_sum(vb.p);
+  nvtxRangePop();
   cudaEventRecord(ev_[3], st_);
   bool conv = false;
   // persistent PCG: its convergence is read after the recovery is launched
   // (no host round trip between the solve and the rest of the step)
   const bool deferred = fused_ok();
   int it = 0;
-  if (deferred) {
-    pcg_fused_launch(vb.p, vx.p);
-  } else {
-    it = pcg(vb.p, vx.p, &conv, nullptr);
-    if (!conv)
-      throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+  {
+    NvtxRange nvtx_pcg("interface PCG (NN2)");
+    if (deferred) {
+      pcg_fused_launch(vb.p, vx.p);
+    } else {
+      it = pcg(vb.p, vx.p, &conv, nullptr);
+      if (!conv)
+        throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+    }
   }
+  NvtxRange nvtx_rec("recovery: interior solve, Newmark update, probes");
   cudaEventRecord(ev_[4], st_);
   gather_li(vx.p, li_x.p, false);
   // A_IG u_G is non-zero only on interior nodes next to the interface
