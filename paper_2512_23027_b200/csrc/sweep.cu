@@ -7,7 +7,7 @@
 //   forward   w_0 = b_0,  z_k = D_k^-1 w_k,  w_{k+1} = b_{k+1} - A_{k+1,k} z_k
 //   backward  x_{H-1} = z_{H-1},  x_k = D_k^-1 (w_k - A_{k,k+1} x_{k+1})
 // D_k^-1 = L_kk^-T L_kk^-1 is symmetric and stored once (lower 64 x 64 tiles,
-// row-major, diagonal tiles full); the grid-row coupling A_{k+1,k} only joins a
+// row-major, swizzled by sw_col, diagonal tiles full); the grid-row coupling A_{k+1,k} only joins a
 // node to its S and SW neighbours (setup.cu assemble_ii_kernel), so it is kept
 // as a band of 2 (P+1) columns per row, for both orientations.  Per grid row
 // the sweep streams B (B + 1) / 2 + B 2 (P+1) doubles per direction, against
@@ -18,17 +18,22 @@
 // streams the rank's tiles (<= 32 KB each) through a ring of shared-memory
 // stages with cp.async.bulk (TMA bulk copies completing on mbarriers).
 //  * D^-1 phase: each consumer warp owns a contiguous run of lower tiles in
-//    row-major order.  Lane l holds tile columns 2l, 2l+1: one pass over a
-//    tile gives the row products T v_J (64 lane partials per row run, one
-//    butterfly at its end) and the column products T^T v_I (lane-local).  Both
-//    land in per-warp register accumulators indexed by output block; the
+//    row-major order.  One pass over a tile (tile_pass: 8 row groups x 4 column
+//    groups of lanes, every element read from shared memory once) gives the row
+//    products T v_J and the column products T^T v_I; halving exchanges over
+//    the lanes leave lane l with entries 2 l, 2 l + 1 of the output block.
+//    Both land in per-warp register accumulators indexed by output block; the
 //    warps add them into one CTA vector in warp order, which each rank pushes
 //    to the owners of the rows (DSMEM).  The owner sums the ranks in order.
 //  * band phase: each rank applies the band columns that fall in the rows it
 //    owns and pushes the partial rows to every rank; the next phase sums the
 //    ranks' partials in rank order.
-// One split cluster barrier closes every phase.  All reductions run in a fixed
+// Phases are closed by data-driven signals (remote mbarrier arrivals after a
+// consumer barrier), not by cluster-wide barriers; the producer is paced by
+// the ring alone and runs ahead across phases.  All reductions run in a fixed
 // order: results are bitwise reproducible.
+// Small blocks (B <= 96) take sweep_small_kernel, very large ones (B > 1536)
+// sweep_generic_kernel; both are described where they are defined.
 #include <cooperative_groups.h>
 
 #include <algorithm>
