@@ -302,7 +302,7 @@ int sgw_advance(sgw_solver* s, int n_steps, int* iterations) {
     GpuSolver& g = *s->g;
     for (int k = 0; k < n_steps; ++k) {
       int it = 0;
-      g.step(&it);
+      g.step(&it, k + 1 < n_steps);
       if (iterations) iterations[k] = it;
     }
   });
@@ -360,7 +360,7 @@ int sgw_run(sgw_solver* s, const double* u0, const double* v0, int n_steps, cons
     }
     for (int k = 0; k < n_steps; ++k) {
       int it = 0;
-      g.step(&it);
+      g.step(&it, k + 1 < n_steps);
       if (h && h->iterations) h->iterations[k] = it;
       if (h && h->residual) h->residual[k] = g.last_rel;
       if (h && h->full_state) {

@@ -1454,9 +1454,13 @@ void GpuSolver::pcg_fused_launch(const double* b, double* x) {
                                        fused_smem_, st_));
   SGW_LAUNCHED();
   cudaEventRecord(ev_[1], st_);  // end of the solve (the PCG time)
-  SGW_CUDA(cudaMemcpyAsync(h_fused_, fused_out_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st_));
-  SGW_CUDA(cudaMemcpyAsync(h_fused_ + 4, fused_hist_.p, fused_hist_.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  cudaEventRecord(ev_[6], st_);  // outputs in pinned memory
+  // the read-back runs on a side stream: the step's recovery kernels follow the
+  // solve on st_ without waiting for two small device-to-host copies
+  if (!side_) SGW_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  SGW_CUDA(cudaStreamWaitEvent(side_, ev_[1], 0));
+  SGW_CUDA(cudaMemcpyAsync(h_fused_, fused_out_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, side_));
+  SGW_CUDA(cudaMemcpyAsync(h_fused_ + 4, fused_hist_.p, fused_hist_.n * sizeof(double), cudaMemcpyDeviceToHost, side_));
+  cudaEventRecord(ev_[6], side_);  // outputs in pinned memory
 }
 
 int GpuSolver::pcg_fused_finish(bool* converged, std::vector<double>* hist) {

@@ -474,6 +474,7 @@ GpuSolver::~GpuSolver() {
   if (blas_) cublasDestroy(blas_);
   if (sol_) cusolverDnDestroy(sol_);
   for (auto& e : ev_) cudaEventDestroy(e);
+  if (side_) cudaStreamDestroy(side_);
   if (graph_mv_) cudaGraphExecDestroy(graph_mv_);
   if (graph_pc_) cudaGraphExecDestroy(graph_pc_);
   if (h_scal_) cudaFreeHost(h_scal_);

@@ -19,6 +19,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -158,15 +159,16 @@ struct KProf {
   double ms[K_NCLASS] = {0};
   long long count[K_NCLASS] = {0};
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
-  std::vector<cudaEvent_t> pool;
-  size_t next = 0;
+  std::vector<cudaEvent_t> free_;
   cudaEvent_t get() {
-    if (next == pool.size()) {
+    if (free_.empty()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
-      pool.push_back(e);
+      return e;
     }
-    return pool[next++];
+    cudaEvent_t e = free_.back();
+    free_.pop_back();
+    return e;
   }
   void begin(int cls, cudaStream_t st, cudaEvent_t* a) {
     if (!on) return;
@@ -180,15 +182,22 @@ struct KProf {
     cudaEventRecord(b, st);
     pending.back().second.second = b;
   }
-  void collect() {  // after a stream synchronize
-    for (auto& p : pending) {
+  size_t mark() const { return pending.size(); }
+  // after the stream has passed the first `upto` pairs (a step that has launched
+  // the next step's right-hand side ahead collects only its own)
+  void collect(size_t upto = ~size_t(0)) {
+    upto = std::min(upto, pending.size());
+    for (size_t i = 0; i < upto; ++i) {
+      auto& p = pending[i];
       float t = 0;
-      cudaEventElapsedTime(&t, p.second.first, p.second.second);
-      ms[p.first] += t;
-      ++count[p.first];
+      if (p.second.second && cudaEventElapsedTime(&t, p.second.first, p.second.second) == cudaSuccess) {
+        ms[p.first] += t;
+        ++count[p.first];
+      }
+      free_.push_back(p.second.first);
+      if (p.second.second) free_.push_back(p.second.second);
     }
-    pending.clear();
-    next = 0;
+    pending.erase(pending.begin(), pending.begin() + upto);
   }
   void reset() {
     for (int i = 0; i < K_NCLASS; ++i) ms[i] = 0, count[i] = 0;
@@ -217,7 +226,9 @@ class GpuSolver {
   void init_state(const double* u0_nodal_dev, const double* v0_nodal_dev, double f0_scale);
   void set_force_point(int node, double f0, double t0, double amp);
   void set_force_table(const double* table_host, int n_rows);
-  int step(int* iters_out);  // one Newmark step on device
+  // one Newmark step on device; `more`: another step follows in the same call, so
+  // its right-hand side may be launched before this step's verdict is read
+  int step(int* iters_out, bool more = false);
   std::vector<double> coarse_operator_host() const { return fcc_host_; }
   // dense S_s / S_rr^-1 / Psi_s of local subdomain s (verification hook)
   std::vector<double> local_block(int s, int which, std::vector<long long>* gmap);
@@ -441,7 +452,11 @@ class GpuSolver {
   }
   DBuf<double> nodal_u0_, nodal_v0_;  // sgw_run / sgw_init_state: nodal initial fields (kept across calls)
  private:
-  cudaEvent_t ev_[8];
+  cudaEvent_t ev_[10];  // [8], [9]: right-hand-side phase of a step launched ahead
+  cudaStream_t side_ = nullptr;  // read-back of the persistent PCG's outputs
+  bool rhs_ahead_ = false;  // the next step's right-hand side is already on the stream
+  int rhs_par_ = 0;         // event pair of the current step's right-hand side (0: ev_[2..3], 1: ev_[8..9])
+  void launch_rhs(double t_next, int row_next, cudaEvent_t e0, cudaEvent_t e1);
   // host-driven PCG: pinned residual scalar and the two per-iteration graphs
   double* h_scal_ = nullptr;
   cudaGraphExec_t graph_mv_ = nullptr, graph_pc_ = nullptr;

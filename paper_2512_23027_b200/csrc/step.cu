@@ -601,6 +601,7 @@ void GpuSolver::init_state(const double* u0_nodal, const double* v0_nodal, doubl
   SGW_LAUNCHED();
   t_now = 0.0;
   step_index = 0;
+  rhs_ahead_ = false;
   // resid = f0 - a0 M v - a1 K v - K u
   // work vectors kept across runs (a cudaMalloc / cudaFree per run would synchronise)
   if (init_w_.n != 4 * NSTATE) init_w_.alloc(4 * NSTATE);
@@ -690,20 +691,24 @@ __global__ void interior_from_global_kernel(LocalArgs A, int n, const double* __
   }
 }
 
-int GpuSolver::step(int* iters_out) {
+// Right-hand-side phase of the step that ends at time t_next (force row
+// row_next): predictors, local force, interior solve y = A_II^-1 f_I and the
+// interface right-hand side g.  It reads the state (u, v, a) and writes scratch
+// only, so step() may put it on the stream for the following step before it has
+// read the current step's verdict.
+void GpuSolver::launch_rhs(double t_next, int row_next, cudaEvent_t e0, cudaEvent_t e1) {
   const long long N = (long long)NSTATE;
   const int grid = std::min(cdiv(N, 256), 8 * kNumSMs * 8);
-  NvtxRange nvtx_step("sgw step");
   nvtxRangePushA("rhs: predictors, local force, interior solve, interface assembly");
-  cudaEventRecord(ev_[2], st_);
+  cudaEventRecord(e0, st_);
   predictor_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, um.p, uc.p, N, P.dt, P.zeta, P.gamma);
   SGW_LAUNCHED();
   double fval = 0.0;
-  const double* fvec = force_at(t_now + P.dt, step_index + 1, &fval);
+  const double* fvec = force_at(t_next, row_next, &fval);
   const LocalArgs A = local_args();
   const long long tl = (long long)NS * G.nl * NT;
   const int fdof = force_kind_ == 1 ? force_dof_ : -1;
-  const long long ti = (long long)n_ilist_ * NT, ta = (long long)n_alist_ * NT;
+  const long long ti = (long long)n_ilist_ * NT;
   if (sgop_) {
     // interior rows: f = M um + a0 M uc + a1 sum c K uc on the global grid (JIT
     // operator), copied into the block rows; interface rows: local stencils
@@ -711,8 +716,8 @@ int GpuSolver::step(int* iters_out) {
     sa.x = uc.p, sa.y = yglob_.p;  // + M um in interior_from_global_kernel
     sa.alpha = P.alpha0, sa.beta = P.alpha1;
     {
-      cudaEvent_t e0;
-      KP.begin(K_SGOP, st_, &e0);
+      cudaEvent_t e;
+      KP.begin(K_SGOP, st_, &e);
       launch_sgop(*sgop_, sa, st_);
       KP.end(st_);
     }
@@ -734,11 +739,37 @@ int GpuSolver::step(int* iters_out) {
   }
   SGW_LAUNCHED();
   sweep(yI.p);  // y = A_II^-1 f_I
+  if (!direct_) {
+    if (cpl_blk_.p)
+      coupling_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+          A, 0, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_iptr_.p, cpl_iedge_.p, ilist_.p, n_ilist_, yI.p, fG.p,
+          nullptr, li_y.p, nullptr);
+    else  // no room for the coupling blocks: the stencil form
+      coupling_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
+          A, 0, yI.p, fG.p, nullptr, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
+    SGW_LAUNCHED();
+    scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
+    halo_sum(vb.p);
+  }
+  nvtxRangePop();
+  cudaEventRecord(e1, st_);
+}
+
+int GpuSolver::step(int* iters_out, bool more) {
+  const long long N = (long long)NSTATE;
+  const int grid = std::min(cdiv(N, 256), 8 * kNumSMs * 8);
+  NvtxRange nvtx_step("sgw step");
+  const LocalArgs A = local_args();
+  const long long ti = (long long)n_ilist_ * NT, ta = (long long)n_alist_ * NT;
+  (void)ti;
+  const cudaEvent_t ev_rhs0 = rhs_par_ ? ev_[8] : ev_[2], ev_rhs1 = rhs_par_ ? ev_[9] : ev_[3];
+  if (!rhs_ahead_) {
+    launch_rhs(t_now + P.dt, step_index + 1, ev_rhs0, ev_rhs1);
+  }
+  rhs_ahead_ = false;
   if (direct_) {
     // one subdomain (sg.cpp:301-305): y is the whole solution, no interface solve
     SGW_CUDA(cudaMemsetAsync(wI.p, 0, wI.n * sizeof(double), st_));
-    nvtxRangePop();
-    cudaEventRecord(ev_[3], st_);
     cudaEventRecord(ev_[4], st_);
     update_kernel<<<grid, 256, 0, st_>>>(u.p, v.p, a.p, vx.p, yI.p, wI.p, iface_of_dof.p, n, NT, G.n_iface, P.nx,
                                          P.ny, G.px, G.py, G.H, B, gid_local_d_.p, P.dt, P.zeta, P.gamma, nullptr);
@@ -750,25 +781,13 @@ int GpuSolver::step(int* iters_out) {
     ++step_index;
     KP.collect();
     float ms_rhs = 0, ms_all = 0;
-    cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);
-    cudaEventElapsedTime(&ms_all, ev_[2], ev_[5]);
+    cudaEventElapsedTime(&ms_rhs, ev_rhs0, ev_rhs1);
+    cudaEventElapsedTime(&ms_all, ev_rhs0, ev_[5]);
     T.rhs_ms += ms_rhs, T.step_ms += ms_all;
     ++T.steps;
     if (iters_out) *iters_out = 0;
     return 0;
   }
-  if (cpl_blk_.p)
-    coupling_blk_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
-        A, 0, cpl_blk_.p, cpl_edge_.p, cpl_q_cls_.p, cpl_iptr_.p, cpl_iedge_.p, ilist_.p, n_ilist_, yI.p, fG.p,
-        nullptr, li_y.p, nullptr);
-  else  // no room for the coupling blocks: the stencil form
-    coupling_kernel<<<std::max(1, std::min(cdiv(ti, 128), 65535)), 128, 0, st_>>>(
-        A, 0, yI.p, fG.p, nullptr, ip_off.p, iface_lid_.p, li_y.p, nullptr, NS, ilist_.p, n_ilist_);
-  SGW_LAUNCHED();
-  scatter_li(li_y.p, vb.p, false, nullptr, nullptr);  // g = sum_s R_s^T g_s
-  halo_sum(vb.p);
-  nvtxRangePop();
-  cudaEventRecord(ev_[3], st_);
   bool conv = false;
   // persistent PCG: its convergence is read after the recovery is launched
   // (no host round trip between the solve and the rest of the step)
@@ -806,20 +825,38 @@ int GpuSolver::step(int* iters_out) {
   SGW_LAUNCHED();
   record_probes(step_index + 1, deferred ? fused_out_.p + 1 : nullptr);
   cudaEventRecord(ev_[5], st_);
+  const size_t kp_own = KP.mark();
+  static const bool no_ahead = std::getenv("SGW_NO_RHS_AHEAD") != nullptr;  // comparison hook
+  if (more && deferred && !no_ahead) {
+    // keep the GPU busy while the host reads this step's verdict: the next
+    // step's right-hand side only reads the state and writes scratch, so after
+    // a non-converged solve (state un-advanced on device) it is simply dropped
+    launch_rhs((t_now + P.dt) + P.dt, step_index + 2, rhs_par_ ? ev_[2] : ev_[8], rhs_par_ ? ev_[3] : ev_[9]);
+    rhs_ahead_ = true;
+  }
   SGW_CUDA(cudaEventSynchronize(ev_[5]));
   if (deferred) {
+    SGW_CUDA(cudaEventSynchronize(ev_[6]));  // the solve's outputs (side stream)
     // the update and the probe row were conditional on the device-side flag:
     // on non-convergence the state, time and step index stay where they were
     it = pcg_fused_finish(&conv, nullptr);
-    if (!conv) throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+    if (!conv) {
+      if (rhs_ahead_) {
+        rhs_ahead_ = false;
+        SGW_CUDA(cudaStreamSynchronize(st_));
+        KP.collect();
+      }
+      throw Error(3, "stochastic interface solve did not converge at step " + std::to_string(step_index));
+    }
   }
   t_now = t_now + P.dt;
   ++step_index;
-  KP.collect();
+  KP.collect(kp_own);
   float ms_rhs = 0, ms_rec = 0, ms_all = 0;
-  cudaEventElapsedTime(&ms_rhs, ev_[2], ev_[3]);
+  cudaEventElapsedTime(&ms_rhs, ev_rhs0, ev_rhs1);
   cudaEventElapsedTime(&ms_rec, ev_[4], ev_[5]);
-  cudaEventElapsedTime(&ms_all, ev_[2], ev_[5]);
+  cudaEventElapsedTime(&ms_all, ev_rhs0, ev_[5]);
+  if (rhs_ahead_) rhs_par_ ^= 1;
   T.rhs_ms += ms_rhs;
   T.rec_ms += ms_rec;
   T.step_ms += ms_all;

@@ -538,6 +538,43 @@ def test_nonconvergence_leaves_state_unadvanced(gpu, monkeypatch, mode):
     assert np.array_equal(g.state(), u0)
 
 
+def test_nonconvergence_with_next_rhs_launched_ahead(gpu):
+    # advance(n > 1) puts the next step's right-hand side on the stream before
+    # it reads the current step's verdict (step.cu launch_rhs): a failed solve
+    # must still leave the state, the time and the step index untouched, and
+    # the dropped right-hand side must not leak into a later step
+    nx = 16
+    coeff = O.lognormal_coeff(nx, nx, 0.3, 0.5, 0.5, 2, 2)
+    t = O.triple_products(2, 2, 2)
+    g = sg.SgSolver(nx, nx, 2, 2, coeff, t, params=sg.NewmarkParams(dt=1e-3),
+                    options=sg.SgOptions(tol=1e-14, max_iter=1))
+    z = np.zeros((nx + 1) ** 2)
+    g.init_state(O.gaussian_pulse(nx, nx), z)
+    u0 = g.state()
+    for _ in range(2):
+        with pytest.raises(sg.SgError) as e:
+            g.advance(3)
+        assert e.value.code == sg.SGW_ENOCONV
+        assert np.array_equal(g.state(), u0)
+
+
+def test_advance_in_one_call_equals_step_by_step(gpu):
+    # the right-hand side launched ahead inside advance(n) is the one a
+    # step-by-step caller computes: same iterations, bitwise the same state
+    nx = 24
+    node = O.nearest_node(nx, nx, 0.5, 0.5)
+    z = np.zeros((nx + 1) ** 2)
+    runs = []
+    for chunks in ([7], [1] * 7, [3, 4]):
+        g, _ = pair(nx, 3, 2, 0.3, 0.5, 2, 4, 2, 1e-3)
+        g.init_state(O.gaussian_pulse(nx, nx), z, sg.ForceSpec(node=node))
+        its = np.concatenate([g.advance(k) for k in chunks])
+        runs.append((its, g.state()))
+    for its, u in runs[1:]:
+        assert np.array_equal(its, runs[0][0])
+        assert np.array_equal(u, runs[0][1])
+
+
 def test_step_without_coupling_blocks_matches_oracle(gpu, monkeypatch):
     # the coupling / interface-force blocks are built at setup only while
     # memory allows; without them the step takes the stencil
