@@ -162,7 +162,11 @@ int sgw_run(sgw_solver* s, const double* u0_nodal, const double* v0_nodal, int n
             const sgw_force* force, sgw_history* history);
 
 /* Device-resident stepping (for benchmarks): set the initial state and the
- * forcing, then advance n steps without host round trips of the state.     */
+ * forcing, then advance n steps without host round trips of the state.
+ * A step whose interface solve does not converge returns SGW_ENOCONV and
+ * leaves the state, the time and the step index where they were
+ * (sg.cpp:412-416), also when the following step's right-hand side was
+ * already queued behind it.                                               */
 int sgw_init_state(sgw_solver* s, const double* u0_nodal, const double* v0_nodal,
                    const sgw_force* force);
 int sgw_advance(sgw_solver* s, int n_steps, int* iterations);

@@ -365,10 +365,21 @@ __device__ __forceinline__ double s_reduce(const FusedPcg& A, long long q) {
   int4 d[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) d[e] = __ldg(A.sred + 4 * gq + e);
+  // the (<= 4) subdomains' partial lists side by side (tiles.cuh partial_sums)
+  const double* p[4];
+  int len[4], n[4];
+  double ys[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool on = d[e].w > 0;
+    p[e] = on ? A.rs.part + d[e].x + (long long)j * d[e].y : A.rs.part;
+    len[e] = d[e].z, n[e] = on ? d[e].w : 0;
+  }
+  partial_sums<4, 2>(p, len, n, ys);
   double y = 0.0;
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    if (d[e].w > 0) y += partial_sum(A.rs.part + d[e].x + (long long)j * d[e].y, d[e].z, d[e].w);
+    if (d[e].w > 0) y += ys[e];
   return y;
 }
 
@@ -378,15 +389,33 @@ __device__ __forceinline__ double z_reduce(const FusedPcg& A, int j, int gq, boo
   double w[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) d[e] = __ldg(A.zred + 4 * gq + e), p[e] = __ldg(A.pred + 4 * gq + e), w[e] = __ldg(A.ifw + 4 * gq + e);
+  // lists 0..3: Q_s f_r partials, 4..7: Psi_s u_c partials, all in flight
+  // together; corner slots (w == -1) read u_c directly.  The descriptors are
+  // folded into pointers / counts / a slot kind before the loads start (the
+  // kernel runs two CTAs per SM: 128 registers)
+  const double* lp[8];
+  int len[8], n[8], kind[4];
+  double ys[8], uc[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool on = d[e].w >= 0, onp = on && coarse;
+    kind[e] = on ? 1 : d[e].w == -1 ? 2 : 0;
+    lp[e] = on ? A.rq.part + d[e].x + (long long)j * d[e].y : A.rq.part;
+    len[e] = d[e].z, n[e] = on ? d[e].w : 0;
+    lp[4 + e] = onp ? A.rp.part + p[e].x + (long long)j * p[e].y : A.rq.part;
+    len[4 + e] = p[e].z, n[4 + e] = onp ? p[e].w : 0;
+    uc[e] = kind[e] == 2 && coarse ? __ldcg(A.ucl + d[e].x + (long long)j * d[e].y) : 0.0;
+  }
+  partial_sums<8, 1>(lp, len, n, ys);
   double zq = 0.0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     double v;
-    if (d[e].w >= 0) {
-      v = partial_sum(A.rq.part + d[e].x + (long long)j * d[e].y, d[e].z, d[e].w);
-      if (coarse) v -= partial_sum(A.rp.part + p[e].x + (long long)j * p[e].y, p[e].z, p[e].w);
-    } else if (d[e].w == -1) {
-      v = coarse ? __ldcg(A.ucl + d[e].x + (long long)j * d[e].y) : 0.0;
+    if (kind[e] == 1) {
+      v = ys[e];
+      if (coarse) v -= ys[4 + e];
+    } else if (kind[e] == 2) {
+      v = uc[e];
     } else {
       continue;
     }
@@ -395,6 +424,19 @@ __device__ __forceinline__ double z_reduce(const FusedPcg& A, int j, int gq, boo
   return zq;
 }
 
+
+// The persistent kernel's loops over the interface dofs: runs of 32 consecutive
+// dofs (one warp reads consecutive entries) dealt round-robin over the CTAs.
+// With q = global thread id a small problem (C1: 2,268 dofs) put every dof on
+// the first 9 of 148 CTAs, whose load paths then carried all the partial-list
+// reads of a scatter phase.  Every loop uses the same map, so a dof stays with
+// one thread from loop to loop.
+#define FOR_IFACE_DOF(q)                                                                                  \
+  for (long long q##_run = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x,                       \
+                 q = q##_run * 32 + (threadIdx.x & 31);                                                  \
+       q##_run * 32 < A.NG;                                                                              \
+       q##_run += (long long)(blockDim.x >> 5) * gridDim.x, q = q##_run * 32 + (threadIdx.x & 31))       \
+    if (q < A.NG)
 
 // z = NN2(r) from the local inputs fr/fc; returns r.z.
 //  4. Q_s f_r and Psi_s^T f_r: the Q tile walk, then the Psi^T tile walk on
@@ -495,7 +537,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
   }
   // 7.
   double rz = 0.0;
-  for (long long q = gtid; q < A.NG; q += gstride) {
+  FOR_IFACE_DOF(q) {
     const int j = int(q / A.n_iface), gq = int(q % A.n_iface);
     const double zq = z_reduce(A, j, gq, coarse);  // u_r = Q f_r - Psi u_c ; u_c
     A.z[q] = zq;
@@ -507,7 +549,7 @@ __device__ double nn2_phases(const FusedPcg& A, Ring& R, Smem& sm, cg::grid_grou
   return rzv;
 }
 
-__global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
+__global__ void __launch_bounds__(256, 2) pcg_fused_kernel(FusedPcg A) {
   cg::grid_group g = cg::this_grid();
   __shared__ Smem sm;
   __shared__ unsigned long long ring_bar[kMaxRing];
@@ -529,7 +571,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
   __syncthreads();
   // x = 0, r = b, NN2 inputs of r, ||b||^2
   double acc = 0.0;
-  for (long long q = gtid; q < A.NG; q += gstride) {
+  FOR_IFACE_DOF(q) {
     const double bv = A.b[q];
     A.x[q] = 0.0;
     A.r[q] = bv;
@@ -555,7 +597,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
     g.sync();
     pc.tick(0);
     acc = 0.0;
-    for (long long q = gtid; q < A.NG; q += gstride) {
+    FOR_IFACE_DOF(q) {
       const double y = s_reduce(A, q);
       A.q[q] = y;
       acc += y * (first ? A.z[q] : A.z[q] + beta * A.p[q]);
@@ -564,7 +606,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
     pc.tick(1);
     // 3: p, x, r updates and NN2 inputs
     acc = 0.0;
-    for (long long q = gtid; q < A.NG; q += gstride) {
+    FOR_IFACE_DOF(q) {
       const double pn = first ? A.z[q] : A.z[q] + beta * A.p[q];
       A.p[q] = pn;
       write_local_s(A, A.li_p, q, pn);
@@ -581,12 +623,12 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
     double rel = sqrt(rr) / bnorm;
     if (rel <= A.tol) {
       // recurrence hit the target; confirm with the true residual b - S x
-      for (long long q = gtid; q < A.NG; q += gstride) write_local_s(A, A.li_x, q, A.x[q]);
+      FOR_IFACE_DOF(q) write_local_s(A, A.li_x, q, A.x[q]);
       g.sync();
       s_tiles_phase(A, R, sm, xs, xacc, 1, false, 0.0);
       g.sync();
       acc = 0.0;
-      for (long long q = gtid; q < A.NG; q += gstride) {
+      FOR_IFACE_DOF(q) {
         const double rt = A.b[q] - s_reduce(A, q);
         A.q[q] = rt;
         acc += rt * rt;
@@ -598,7 +640,7 @@ __global__ void __launch_bounds__(256) pcg_fused_kernel(FusedPcg A) {
         converged = true;
         break;
       }
-      for (long long q = gtid; q < A.NG; q += gstride) {  // restart from r_true, p kept
+      FOR_IFACE_DOF(q) {  // restart from r_true, p kept
         const double rt = A.q[q];
         A.r[q] = rt;
         write_local(A, q, rt);

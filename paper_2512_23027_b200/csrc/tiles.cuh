@@ -139,6 +139,31 @@ __device__ __forceinline__ double partial_sum(const double* p, int len, int n) {
   for (; k < n; ++k) y += __ldcg(p + (long long)k * len);
   return y;
 }
+// NL partial lists summed side by side: list e is what partial_sum(p[e], len[e],
+// n[e]) returns (k ascending, the same additions in the same order), but the
+// loads of all lists are in flight together, KU entries of each per round, instead of one
+// list after the other.  An interface node's reduction is then a few L2 round
+// trips, not (slots x lists x n / 4): that chain was most of the scatter phases
+// of small problems (C1).  Empty lists (n <= 0) load nothing.
+template <int NL, int KU>
+__device__ __forceinline__ void partial_sums(const double* const (&p)[NL], const int (&len)[NL], const int (&n)[NL],
+                                             double (&y)[NL]) {
+  int nmax = 0;
+#pragma unroll
+  for (int e = 0; e < NL; ++e) y[e] = 0.0, nmax = max(nmax, n[e]);
+  for (int k = 0; k < nmax; k += KU) {
+    double a[KU][NL];
+#pragma unroll
+    for (int u = 0; u < KU; ++u)
+#pragma unroll
+      for (int e = 0; e < NL; ++e) a[u][e] = k + u < n[e] ? __ldcg(p[e] + (long long)(k + u) * len[e]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < KU; ++u)
+#pragma unroll
+      for (int e = 0; e < NL; ++e)
+        if (k + u < n[e]) y[e] += a[u][e];
+  }
+}
 // y_s[i] from the partials of the CTAs covering symmetric matrix s
 __device__ __forceinline__ double range_reduce(const RangePack& P, int s, int i) {
   return partial_sum(P.part + P.pbase[s] + i, kTile * P.nI[s], P.ncta[s]);
