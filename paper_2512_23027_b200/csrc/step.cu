@@ -760,12 +760,10 @@ int GpuSolver::step(int* iters_out, bool more) {
   const int grid = std::min(cdiv(N, 256), 8 * kNumSMs * 8);
   NvtxRange nvtx_step("sgw step");
   const LocalArgs A = local_args();
-  const long long ti = (long long)n_ilist_ * NT, ta = (long long)n_alist_ * NT;
-  (void)ti;
+  const long long ta = (long long)n_alist_ * NT;
+  // the right-hand-side phase: already on the stream when the previous step launched it ahead
   const cudaEvent_t ev_rhs0 = rhs_par_ ? ev_[8] : ev_[2], ev_rhs1 = rhs_par_ ? ev_[9] : ev_[3];
-  if (!rhs_ahead_) {
-    launch_rhs(t_now + P.dt, step_index + 1, ev_rhs0, ev_rhs1);
-  }
+  if (!rhs_ahead_) launch_rhs(t_now + P.dt, step_index + 1, ev_rhs0, ev_rhs1);
   rhs_ahead_ = false;
   if (direct_) {
     // one subdomain (sg.cpp:301-305): y is the whole solution, no interface solve
